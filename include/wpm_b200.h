@@ -1,0 +1,144 @@
+/*
+ * wpm_b200.h -- C-ABI of the B200-native weak-pseudo-manifold enumerator.
+ *
+ * The drop-in boundary for the reference's enumeration path
+ * ("characteristic map in, WPM facet lists out").  Plain pointers and sizes,
+ * no torch or CUDA types.  Every entry point names the reference interface it
+ * replaces (paths relative to /root/reference/proj):
+ *
+ *   wpm_idcm_orbits         <- idcm_orbits(n, p)            include/plseeds/charmap.hpp:212-281
+ *   wpm_charmap_of_dcm      <- charmap_of_dcm(d)            include/plseeds/charmap.hpp:155-204
+ *   wpm_cyclic_facet_bound  <- cyclic_facet_bound(n)        include/plseeds/affine_property.hpp:35-45
+ *   wpm_plan_create_orbits  <- the per-orbit loop prelude   include/plseeds/pipeline.hpp:379-392
+ *                              matroid_universe (pipeline.hpp:33-35) = binary_matroid
+ *                              (charmap.hpp:117-141) on the GPU (kernel 1), then
+ *                              incidence_matrix (incidence.hpp:34-55) on the GPU (kernel 2)
+ *   wpm_plan_create_universes <- SearchJob{m, n, facets, properties} (search.hpp:46-55)
+ *                              + incidence_matrix (kernel 2); required/forbidden facet
+ *                              pins replace apply_link_constraints (kernel_basis.hpp:248-321)
+ *   wpm_plan_run            <- enumerate_wpm(const SearchJob&)  search.hpp:141-258 (kernel 3,
+ *                              the ridge-driven DFS) + the canonical merge/sort (:247-257)
+ *   wpm_plan_fetch / wpm_result_*  <- std::vector<PureComplex> return value (search.hpp:141)
+ *   wpm_enumerate           <- enumerate_wpm(job) one-shot     search.hpp:141-258
+ *   wpm_write_cplx          <- write_complexes(os, list)       include/plseeds/complex_io.hpp:21-39
+ *
+ * Status codes mirror the CLI exit codes (tools/plseeds_cli.cpp:31-35):
+ * 0 ok, 2 format/purity/invalid argument, 3 infeasible, 5 cap exceeded,
+ * 1 internal / CUDA error (wpm_last_error() has the message).  There is no
+ * CPU fallback: without a usable B200 every compute entry point returns 1.
+ *
+ * Threading: calls block (like enumerate_wpm); distinct plans may be used
+ * from distinct host threads; one plan is not re-entrant.
+ */
+#ifndef WPM_B200_H
+#define WPM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WPM_OK 0
+#define WPM_EINTERNAL 1
+#define WPM_EINVAL 2
+#define WPM_EINFEASIBLE 3
+#define WPM_ECAP 5
+
+/* facet_cap sentinels */
+#define WPM_CAP_NONE (-1)  /* no property: every WPM (classify_full_universe, pipeline.hpp:157-196) */
+#define WPM_CAP_UBT (-2)   /* ubt_property(n, M): |K| <= cyclic_facet_bound(n) (affine_property.hpp:49-54) */
+
+/* hard limits of the device layout */
+#define WPM_MAX_M 16       /* vertex labels 1..m (VertexSet bits 1..16) */
+#define WPM_MAX_FACETS 2048
+#define WPM_MAX_RIDGES 4096
+#define WPM_MAX_PARENTS 8  /* candidate facets per ridge (m - n + 1 <= 8) */
+
+typedef struct wpm_plan wpm_plan_t;
+
+/* one enumeration job over a single facet universe (SearchJob, search.hpp:46-55) */
+typedef struct {
+    int32_t m, n;
+    int32_t num_facets;          /* M */
+    const uint64_t *facets;      /* M masks, bit v = vertex v (1-based), strictly ascending */
+    int64_t facet_cap;           /* >= 0, WPM_CAP_NONE or WPM_CAP_UBT */
+    const int32_t *required;     /* facet indices pinned into every K */
+    int32_t num_required;
+    const int32_t *forbidden;    /* facet indices pinned out of every K */
+    int32_t num_forbidden;
+    int32_t device;              /* CUDA ordinal */
+    int32_t shard_index;         /* root-branch partition for multi-GPU runs: */
+    int32_t shard_count;         /* this rank takes root tasks t with t % count == index (0/1 = all) */
+} wpm_job_t;
+
+/* enumeration output: WPMs of every map of the plan, grouped by map, each
+ * group in canonical order (search.hpp:254-256), as characteristic bitsets
+ * over that map's universe (bit j = facet j), `words` uint64 per WPM. */
+typedef struct {
+    int32_t num_maps;
+    int32_t words;
+    int64_t total;               /* number of WPMs over all maps */
+    int64_t *counts;             /* num_maps */
+    int64_t *offsets;            /* num_maps + 1, prefix sums of counts */
+    uint64_t *bits;              /* total * words */
+    int64_t nodes;               /* DFS search nodes (facet-inclusion steps) */
+    int64_t duplicates;          /* adjacent equal WPMs after the sort; always 0 */
+    double ms_search;            /* device time of kernel 3 (CUDA events) */
+    double ms_sort;              /* device time of the canonical sort + gather */
+    int64_t tasks;               /* work items processed (root tasks + donations) */
+} wpm_result_t;
+
+/* ---------------------------------------------------------------- host */
+const char *wpm_last_error(void);
+int wpm_device_count(void);
+int64_t wpm_cyclic_facet_bound(int32_t n);
+/* rows_out: up to cap orbits x (n+p) rows; returns #orbits or -status */
+int32_t wpm_idcm_orbits(int32_t n, int32_t p, uint32_t *rows_out, int32_t cap);
+/* cols_out: m columns; returns n or -status */
+int32_t wpm_charmap_of_dcm(int32_t m, int32_t p, const uint32_t *rows, uint32_t *cols_out);
+
+/* ---------------------------------------------------------------- plans */
+/* Every characteristic map of idcm_orbits(n, p): universes by kernel 1 and
+ * incidence tables by kernel 2, resident on `device`. */
+int wpm_plan_create_orbits(int32_t n, int32_t p, int64_t facet_cap, int32_t device, wpm_plan_t **out);
+/* Explicit characteristic maps: num_maps x m lambda columns (n-bit each). */
+int wpm_plan_create_charmaps(int32_t n, int32_t m, int32_t num_maps, const uint32_t *cols,
+                             int64_t facet_cap, int32_t device, wpm_plan_t **out);
+/* Explicit universes (SearchJob.facets), one per map; facet_counts[i] masks
+ * each, concatenated in `facets`.  required/forbidden apply to map 0 only
+ * (pass num_maps == 1 with pins). */
+int wpm_plan_create_universes(int32_t m, int32_t n, int32_t num_maps, const int32_t *facet_counts,
+                              const uint64_t *facets, int64_t facet_cap, const int32_t *required,
+                              int32_t num_required, const int32_t *forbidden, int32_t num_forbidden,
+                              int32_t device, wpm_plan_t **out);
+int wpm_plan_num_maps(const wpm_plan_t *plan);
+/* kernel-1 / kernel-2 outputs of one map (parity hooks) */
+int32_t wpm_plan_universe(wpm_plan_t *plan, int32_t map, uint64_t *facets_out, int32_t cap);
+int32_t wpm_plan_incidence(wpm_plan_t *plan, int32_t map, uint64_t *ridges_out, int32_t ridges_cap,
+                           int32_t *cols_out, int32_t *par_out /* N*WPM_MAX_PARENTS, -1 padded */);
+/* Run the search + canonical sort on the device; results stay resident.
+ * Returns status; *total_out = number of WPMs. */
+int wpm_plan_run(wpm_plan_t *plan, int32_t shard_index, int32_t shard_count, int64_t *total_out);
+/* Copy the last run's results to the host. */
+int wpm_plan_fetch(wpm_plan_t *plan, wpm_result_t **out);
+/* Device-side timing of the last run (ms) and node count, without a fetch. */
+int wpm_plan_stats(const wpm_plan_t *plan, double *ms_search, double *ms_sort, int64_t *nodes,
+                   int64_t *tasks);
+void wpm_plan_destroy(wpm_plan_t *plan);
+
+/* ---------------------------------------------------------------- one-shot */
+int wpm_enumerate(const wpm_job_t *job, wpm_result_t **out);
+/* Algorithm-2 loop for one n: every orbit map, UBT (or given) cap. */
+int wpm_enumerate_orbits(int32_t n, int32_t p, int64_t facet_cap, int32_t device, wpm_result_t **out);
+void wpm_result_free(wpm_result_t *res);
+
+/* complex_io.hpp:21-39 for map `map` of a result; returns bytes needed,
+ * writes at most buf_len. */
+int64_t wpm_write_cplx(const wpm_result_t *res, int32_t map, int32_t m, int32_t n,
+                       const uint64_t *universe, char *buf, int64_t buf_len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,182 @@
+// oracle/ref_driver.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A thin driver around the UNMODIFIED reference library, compiled by
+// oracle/Makefile straight from the headers where they lie
+// (/root/reference/proj/include); the binary goes to oracle/_ref/ (git-ignored,
+// shipped to the GPU box by gpurun).  It is the golden generator and the
+// `--impl reference` CPU baseline.  It runs the reference path exactly as
+// pipeline.hpp:58-72 does per orbit: matroid_universe -> incidence_matrix ->
+// convenient_basis(kernel_basis) -> ubt_property -> enumerate_wpm.
+//
+// usage:
+//   plseeds_ref orbits N
+//   plseeds_ref enumerate N [--nocap] [--threads T] [--out FILE] [--maps a:b]
+//        per map prints "map i M N s space wpms seconds"; --out writes the
+//        concatenated .cplx bytes (SURVEY App. C protocol) and per-map offsets
+//   plseeds_ref universe N --out FILE
+//   plseeds_ref job FILE [--threads T] [--out FILE]
+//        FILE: "m n M cap nreq nforb" then M facet masks, then req, forb
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "plseeds/catalog.hpp"
+#include "plseeds/charmap.hpp"
+#include "plseeds/complex_io.hpp"
+#include "plseeds/incidence.hpp"
+#include "plseeds/kernel_basis.hpp"
+#include "plseeds/pipeline.hpp"
+#include "plseeds/search.hpp"
+
+using namespace plseeds;
+using Clock = std::chrono::steady_clock;
+
+static double since(Clock::time_point t) {
+    return std::chrono::duration<double>(Clock::now() - t).count();
+}
+
+static int arg_int(int argc, char** argv, const char* key, int def) {
+    for (int i = 0; i + 1 < argc; ++i)
+        if (!std::strcmp(argv[i], key)) return std::atoi(argv[i + 1]);
+    return def;
+}
+static const char* arg_str(int argc, char** argv, const char* key) {
+    for (int i = 0; i + 1 < argc; ++i)
+        if (!std::strcmp(argv[i], key)) return argv[i + 1];
+    return nullptr;
+}
+static bool has_flag(int argc, char** argv, const char* key) {
+    for (int i = 0; i < argc; ++i)
+        if (!std::strcmp(argv[i], key)) return true;
+    return false;
+}
+
+int main(int argc, char** argv) {
+    if (argc < 3) {
+        std::fprintf(stderr, "usage: plseeds_ref orbits|enumerate|universe|job ...\n");
+        return 2;
+    }
+    const std::string cmd = argv[1];
+    try {
+        if (cmd == "orbits") {
+            const int n = std::atoi(argv[2]);
+            for (const auto& d : idcm_orbits(n, 4)) {
+                for (std::size_t i = 0; i < d.rows.size(); ++i)
+                    std::printf("%s%u", i ? " " : "", d.rows[i]);
+                std::printf("\n");
+            }
+            return 0;
+        }
+        if (cmd == "universe") {
+            const int n = std::atoi(argv[2]);
+            const char* out = arg_str(argc, argv, "--out");
+            std::ofstream os(out ? out : "/dev/null", std::ios::binary);
+            for (const auto& d : idcm_orbits(n, 4))
+                write_complex(os, PureComplex(n + 4, n, matroid_universe(d), true));
+            return 0;
+        }
+        if (cmd == "enumerate") {
+            const int n = std::atoi(argv[2]);
+            const bool nocap = has_flag(argc, argv, "--nocap");
+            const int threads = arg_int(argc, argv, "--threads", 1);
+            const char* out = arg_str(argc, argv, "--out");
+            const auto orbits = idcm_orbits(n, 4);
+            int a = 0, b = static_cast<int>(orbits.size());
+            if (const char* r = arg_str(argc, argv, "--maps")) std::sscanf(r, "%d:%d", &a, &b);
+            std::ofstream os;
+            if (out) os.open(out, std::ios::binary);
+            double total_enum = 0, total_prep = 0;
+            long long total_wpm = 0;
+            unsigned long long total_space = 0;
+            for (int i = a; i < b && i < static_cast<int>(orbits.size()); ++i) {
+                const auto t0 = Clock::now();
+                SearchJob job;
+                job.m = n + 4;
+                job.n = n;
+                job.facets = matroid_universe(orbits[static_cast<std::size_t>(i)]);
+                const IncidenceMatrix A = incidence_matrix(job.facets);
+                job.basis = convenient_basis(kernel_basis(A), A);
+                if (!nocap) job.properties = {ubt_property(n, static_cast<int>(job.facets.size()))};
+                job.threads = threads;
+                job.candidate_cap = ~0ull;
+                const double prep = since(t0);
+                const auto t1 = Clock::now();
+                const auto found = enumerate_wpm(job);
+                const double dt = since(t1);
+                const unsigned long long space = combination_space(job.basis).size_saturated();
+                std::printf("map %d M %d N %d s %d space %llu wpms %zu prep %.6f seconds %.6f\n", i, A.M, A.N,
+                            job.basis.s(), space, found.size(), prep, dt);
+                std::fflush(stdout);
+                total_enum += dt;
+                total_prep += prep;
+                total_wpm += static_cast<long long>(found.size());
+                total_space += space;
+                if (out) {
+                    std::ostringstream ss;
+                    write_complexes(ss, found);
+                    const std::string s = ss.str();
+                    os.write(s.data(), static_cast<std::streamsize>(s.size()));
+                }
+            }
+            std::printf("total wpms %lld space %llu prep %.6f seconds %.6f threads %d\n", total_wpm, total_space,
+                        total_prep, total_enum, threads);
+            return 0;
+        }
+        if (cmd == "job") {
+            std::ifstream in(argv[2]);
+            int m, n, M, nreq, nforb;
+            long long cap;
+            in >> m >> n >> M >> cap >> nreq >> nforb;
+            std::vector<VertexSet> u(static_cast<std::size_t>(M));
+            for (auto& f : u) {
+                unsigned long long x;
+                in >> x;
+                f = VertexSet(x);
+            }
+            std::vector<int> req(static_cast<std::size_t>(nreq)), forb(static_cast<std::size_t>(nforb));
+            for (auto& x : req) in >> x;
+            for (auto& x : forb) in >> x;
+            SearchJob job;
+            job.m = m;
+            job.n = n;
+            job.facets = u;
+            const IncidenceMatrix A = incidence_matrix(u);
+            auto kb = convenient_basis(kernel_basis(A), A);
+            auto pinned = apply_link_constraints(kb, req, forb);
+            if (!pinned) {
+                std::printf("infeasible\n");
+                return 3;
+            }
+            job.basis = *pinned;
+            if (cap >= 0) {
+                AffineProperty g;
+                g.weights.assign(static_cast<std::size_t>(M), -1);
+                g.constant = cap + 1;
+                job.properties = {g};
+            }
+            job.threads = arg_int(argc, argv, "--threads", 1);
+            job.candidate_cap = ~0ull;
+            const auto t1 = Clock::now();
+            const auto found = enumerate_wpm(job);
+            std::printf("wpms %zu seconds %.6f\n", found.size(), since(t1));
+            if (const char* out = arg_str(argc, argv, "--out")) {
+                std::ofstream os(out, std::ios::binary);
+                write_complexes(os, found);
+            }
+            return 0;
+        }
+    } catch (const cap_exceeded_error& e) {
+        std::fprintf(stderr, "cap exceeded: %s\n", e.what());
+        return 5;
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 1;
+    }
+    return 2;
+}

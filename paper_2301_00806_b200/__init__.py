@@ -1,0 +1,454 @@
+"""paper_2301_00806_b200 -- B200-native enumeration of weak pseudo-manifolds.
+
+Python mirror of the reference's enumeration API for this one path
+(``plseeds``, /root/reference/proj/include/plseeds), bound to the C-ABI
+library ``libwpm_b200.so`` (include/wpm_b200.h).  Names and argument meaning
+follow the reference:
+
+    idcm_orbits(n, p)            charmap.hpp:212-281
+    charmap_of_dcm(rows, p)      charmap.hpp:155-204
+    matroid_universe(rows, p)    pipeline.hpp:33-35 (kernel 1 on the GPU)
+    cyclic_facet_bound(n)        affine_property.hpp:35-45
+    ubt_property(n, M)           affine_property.hpp:49-54
+    SearchJob                    search.hpp:46-55
+    enumerate_wpm(job)           search.hpp:141-258 (kernels 2-3 + canonical sort)
+    write_complexes(...)         complex_io.hpp:21-39
+
+Errors mirror the reference's exception types (errors.hpp): ``PurityError``,
+``CapExceededError`` and ``ValueError`` (std::invalid_argument).  There is
+no CPU fallback: if the CUDA library is missing the import fails, and every
+compute call raises ``RuntimeError`` when no B200 is present.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwpm_b200.so")
+
+WPM_OK = 0
+WPM_EINTERNAL = 1
+WPM_EINVAL = 2
+WPM_EINFEASIBLE = 3
+WPM_ECAP = 5
+WPM_CAP_NONE = -1
+WPM_CAP_UBT = -2
+WPM_MAX_M = 16
+
+
+class PurityError(RuntimeError):
+    """errors.hpp:10-13 (purity_error)."""
+
+
+class CapExceededError(RuntimeError):
+    """errors.hpp:28-31 (cap_exceeded_error)."""
+
+
+class WpmError(RuntimeError):
+    """Internal / CUDA failure of the B200 path (status 1)."""
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(the B200 path has no CPU fallback)"
+    )
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+_i32, _i64, _u32p, _u64p, _i32p = (
+    ctypes.c_int32,
+    ctypes.c_int64,
+    ctypes.POINTER(ctypes.c_uint32),
+    ctypes.POINTER(ctypes.c_uint64),
+    ctypes.POINTER(ctypes.c_int32),
+)
+
+
+class _Result(ctypes.Structure):
+    _fields_ = [
+        ("num_maps", ctypes.c_int32),
+        ("words", ctypes.c_int32),
+        ("total", ctypes.c_int64),
+        ("counts", ctypes.POINTER(ctypes.c_int64)),
+        ("offsets", ctypes.POINTER(ctypes.c_int64)),
+        ("bits", ctypes.POINTER(ctypes.c_uint64)),
+        ("nodes", ctypes.c_int64),
+        ("duplicates", ctypes.c_int64),
+        ("ms_search", ctypes.c_double),
+        ("ms_sort", ctypes.c_double),
+        ("tasks", ctypes.c_int64),
+    ]
+
+
+class _Job(ctypes.Structure):
+    _fields_ = [
+        ("m", ctypes.c_int32),
+        ("n", ctypes.c_int32),
+        ("num_facets", ctypes.c_int32),
+        ("facets", _u64p),
+        ("facet_cap", ctypes.c_int64),
+        ("required", _i32p),
+        ("num_required", ctypes.c_int32),
+        ("forbidden", _i32p),
+        ("num_forbidden", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("shard_index", ctypes.c_int32),
+        ("shard_count", ctypes.c_int32),
+    ]
+
+
+_ResultP = ctypes.POINTER(_Result)
+_PlanP = ctypes.c_void_p
+
+_SIGS = {
+    "wpm_last_error": (ctypes.c_char_p, []),
+    "wpm_device_count": (ctypes.c_int, []),
+    "wpm_cyclic_facet_bound": (_i64, [_i32]),
+    "wpm_idcm_orbits": (_i32, [_i32, _i32, _u32p, _i32]),
+    "wpm_charmap_of_dcm": (_i32, [_i32, _i32, _u32p, _u32p]),
+    "wpm_plan_create_orbits": (ctypes.c_int, [_i32, _i32, _i64, _i32, ctypes.POINTER(_PlanP)]),
+    "wpm_plan_create_charmaps": (ctypes.c_int, [_i32, _i32, _i32, _u32p, _i64, _i32, ctypes.POINTER(_PlanP)]),
+    "wpm_plan_create_universes": (
+        ctypes.c_int,
+        [_i32, _i32, _i32, _i32p, _u64p, _i64, _i32p, _i32, _i32p, _i32, _i32, ctypes.POINTER(_PlanP)],
+    ),
+    "wpm_plan_num_maps": (ctypes.c_int, [_PlanP]),
+    "wpm_plan_universe": (_i32, [_PlanP, _i32, _u64p, _i32]),
+    "wpm_plan_incidence": (_i32, [_PlanP, _i32, _u64p, _i32, _i32p, _i32p]),
+    "wpm_plan_run": (ctypes.c_int, [_PlanP, _i32, _i32, ctypes.POINTER(_i64)]),
+    "wpm_plan_fetch": (ctypes.c_int, [_PlanP, ctypes.POINTER(_ResultP)]),
+    "wpm_plan_stats": (
+        ctypes.c_int,
+        [_PlanP, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),
+         ctypes.POINTER(_i64)],
+    ),
+    "wpm_plan_destroy": (None, [_PlanP]),
+    "wpm_enumerate": (ctypes.c_int, [ctypes.POINTER(_Job), ctypes.POINTER(_ResultP)]),
+    "wpm_enumerate_orbits": (ctypes.c_int, [_i32, _i32, _i64, _i32, ctypes.POINTER(_ResultP)]),
+    "wpm_result_free": (None, [_ResultP]),
+    "wpm_write_cplx": (_i64, [_ResultP, _i32, _i32, _i32, _u64p, ctypes.c_char_p, _i64]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+
+def _check(rc: int) -> None:
+    if rc == WPM_OK:
+        return
+    msg = (_lib.wpm_last_error() or b"").decode()
+    if rc == WPM_ECAP:
+        raise CapExceededError(msg)
+    if rc == WPM_EINVAL:
+        if "purity" in msg or "empty facet set" in msg:
+            raise PurityError(msg)
+        raise ValueError(msg)
+    if rc == WPM_EINFEASIBLE:
+        raise ValueError(msg)
+    raise WpmError(msg or f"status {rc}")
+
+
+def _u32(a) -> "ctypes.Array":
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.uint32))
+    return arr, arr.ctypes.data_as(_u32p)
+
+
+def _u64(a):
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
+    return arr, arr.ctypes.data_as(_u64p)
+
+
+def _i32a(a):
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+    return arr, arr.ctypes.data_as(_i32p)
+
+
+# ----------------------------------------------------------------- host side
+
+def device_count() -> int:
+    return int(_lib.wpm_device_count())
+
+
+def cyclic_facet_bound(n: int) -> int:
+    """affine_property.hpp:35-45."""
+    return int(_lib.wpm_cyclic_facet_bound(n))
+
+
+@dataclass
+class AffineProperty:
+    """affine_property.hpp:16-31 (only count caps reach the device)."""
+
+    weights: List[int]
+    constant: int
+
+    def is_count_cap(self) -> bool:
+        return all(w == -1 for w in self.weights)
+
+
+def ubt_property(n: int, universe_size: int) -> AffineProperty:
+    """affine_property.hpp:49-54: g(K) = cap + 1 - |K| > 0."""
+    return AffineProperty([-1] * universe_size, cyclic_facet_bound(n) + 1)
+
+
+@dataclass
+class DualCharMatrix:
+    """charmap.hpp:64-87: one p-bit row per vertex."""
+
+    m: int
+    p: int
+    rows: List[int]
+
+
+def idcm_orbits(n: int, p: int = 4) -> List[DualCharMatrix]:
+    """charmap.hpp:212-281 (host C++ in the library)."""
+    k = int(_lib.wpm_idcm_orbits(n, p, None, 0))
+    if k < 0:
+        _check(-k)
+    m = n + p
+    buf = np.zeros(k * m, dtype=np.uint32)
+    _lib.wpm_idcm_orbits(n, p, buf.ctypes.data_as(_u32p), k)
+    return [DualCharMatrix(m, p, [int(x) for x in buf[i * m:(i + 1) * m]]) for i in range(k)]
+
+
+def charmap_of_dcm(d: DualCharMatrix) -> List[int]:
+    """charmap.hpp:155-204: lambda columns (n-bit ints)."""
+    rows, rp = _u32(d.rows)
+    cols = np.zeros(d.m, dtype=np.uint32)
+    r = int(_lib.wpm_charmap_of_dcm(d.m, d.p, rp, cols.ctypes.data_as(_u32p)))
+    if r < 0:
+        _check(-r)
+    return [int(c) for c in cols]
+
+
+# ----------------------------------------------------------------- plans
+
+class Plan:
+    """A device-resident batch of characteristic maps / universes.
+
+    Owns the kernel-1 universes, kernel-2 incidence tables, the work queue
+    and the result buffers on one GPU.  ``run()`` is the hot path (kernel 3 +
+    canonical sort, inputs and outputs resident in HBM); ``fetch()`` copies
+    the result to the host.
+    """
+
+    def __init__(self, handle, n: int, m: int):
+        self._h = ctypes.c_void_p(handle)
+        self.n = n
+        self.m = m
+        self.num_maps = int(_lib.wpm_plan_num_maps(self._h))
+
+    @classmethod
+    def orbits(cls, n: int, p: int = 4, facet_cap: int = WPM_CAP_UBT, device: int = 0) -> "Plan":
+        h = _PlanP()
+        _check(_lib.wpm_plan_create_orbits(n, p, facet_cap, device, ctypes.byref(h)))
+        return cls(h.value, n, n + p)
+
+    @classmethod
+    def charmaps(cls, n: int, m: int, cols: Sequence[Sequence[int]], facet_cap: int = WPM_CAP_UBT,
+                 device: int = 0) -> "Plan":
+        flat, fp = _u32([c for cs in cols for c in cs])
+        h = _PlanP()
+        _check(_lib.wpm_plan_create_charmaps(n, m, len(cols), fp, facet_cap, device, ctypes.byref(h)))
+        return cls(h.value, n, m)
+
+    @classmethod
+    def universes(cls, m: int, n: int, universes: Sequence[Sequence[int]], facet_cap: int = WPM_CAP_NONE,
+                  required: Sequence[int] = (), forbidden: Sequence[int] = (), device: int = 0) -> "Plan":
+        counts, cp = _i32a([len(u) for u in universes])
+        flat, fp = _u64([f for u in universes for f in u])
+        req, rp = _i32a(list(required) or [0])
+        forb, fbp = _i32a(list(forbidden) or [0])
+        h = _PlanP()
+        _check(_lib.wpm_plan_create_universes(m, n, len(universes), cp, fp, facet_cap, rp, len(required), fbp,
+                                              len(forbidden), device, ctypes.byref(h)))
+        return cls(h.value, n, m)
+
+    def universe(self, i: int) -> List[int]:
+        buf = np.zeros(1 << 12, dtype=np.uint64)
+        M = int(_lib.wpm_plan_universe(self._h, i, buf.ctypes.data_as(_u64p), len(buf)))
+        if M < 0:
+            _check(-M)
+        return [int(x) for x in buf[:M]]
+
+    def incidence(self, i: int):
+        """(ridges, cols[M][n], parents[N][<=8]) of map i, from kernel 2."""
+        M = len(self.universe(i))
+        ridges = np.zeros(1 << 13, dtype=np.uint64)
+        cols = np.zeros(M * self.n, dtype=np.int32)
+        par = np.zeros((1 << 13) * 8, dtype=np.int32)
+        N = int(_lib.wpm_plan_incidence(self._h, i, ridges.ctypes.data_as(_u64p), len(ridges),
+                                        cols.ctypes.data_as(_i32p), par.ctypes.data_as(_i32p)))
+        if N < 0:
+            _check(-N)
+        parents = [[int(g) for g in par[r * 8:(r + 1) * 8] if g >= 0] for r in range(N)]
+        return [int(x) for x in ridges[:N]], cols.reshape(M, self.n).tolist(), parents
+
+    def run(self, shard_index: int = 0, shard_count: int = 1) -> int:
+        tot = _i64()
+        _check(_lib.wpm_plan_run(self._h, shard_index, shard_count, ctypes.byref(tot)))
+        return int(tot.value)
+
+    def stats(self) -> dict:
+        a, b, c, d = ctypes.c_double(), ctypes.c_double(), _i64(), _i64()
+        _check(_lib.wpm_plan_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)))
+        return {"ms_search": a.value, "ms_sort": b.value, "nodes": c.value, "tasks": d.value}
+
+    def fetch(self) -> "Result":
+        rp = _ResultP()
+        _check(_lib.wpm_plan_fetch(self._h, ctypes.byref(rp)))
+        return Result(rp)
+
+    def close(self) -> None:
+        if self._h:
+            _lib.wpm_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+class Result:
+    """Host copy of an enumeration (wpm_result_t): per-map canonical lists."""
+
+    def __init__(self, rp):
+        r = rp.contents
+        self.num_maps = r.num_maps
+        self.words = r.words
+        self.total = r.total
+        self.nodes = r.nodes
+        self.duplicates = r.duplicates
+        self.ms_search = r.ms_search
+        self.ms_sort = r.ms_sort
+        self.tasks = r.tasks
+        self.counts = [int(r.counts[i]) for i in range(r.num_maps)]
+        self.offsets = [int(r.offsets[i]) for i in range(r.num_maps + 1)]
+        n = r.total * r.words
+        self.bits = (np.ctypeslib.as_array(r.bits, shape=(max(n, 1),))[:n].copy().reshape(r.total, r.words)
+                     if n else np.zeros((0, r.words), dtype=np.uint64))
+        _lib.wpm_result_free(rp)
+
+    def map_bits(self, i: int) -> np.ndarray:
+        return self.bits[self.offsets[i]:self.offsets[i + 1]]
+
+
+# ----------------------------------------------------------------- the drop-in
+
+@dataclass
+class SearchJob:
+    """search.hpp:46-55.  ``basis`` is not needed by the ridge-driven search;
+    pins are given directly as facet indices (apply_link_constraints
+    semantics, kernel_basis.hpp:248-321).  ``threads`` and ``candidate_cap``
+    are accepted for API compatibility; the device search has no combination
+    space to cap."""
+
+    m: int
+    n: int
+    facets: List[int]
+    properties: List[AffineProperty] = field(default_factory=list)
+    required: List[int] = field(default_factory=list)
+    forbidden: List[int] = field(default_factory=list)
+    threads: int = 1
+    candidate_cap: int = 1 << 48
+    device: int = 0
+
+
+def _facet_cap(job: SearchJob) -> int:
+    """search.hpp:181-187: a pure count cap becomes the device cap."""
+    cap = WPM_CAP_NONE
+    for g in job.properties:
+        if not g.is_count_cap():
+            raise ValueError("general affine properties are not supported by the B200 path (count caps only)")
+        c = g.constant - 1
+        cap = c if cap < 0 else min(cap, c)
+    return cap
+
+
+def bits_to_facets(bits_row: np.ndarray, universe: Sequence[int]) -> List[int]:
+    out = []
+    for w, word in enumerate(bits_row):
+        x = int(word)
+        while x:
+            b = (x & -x).bit_length() - 1
+            out.append(universe[w * 64 + b])
+            x &= x - 1
+    return out
+
+
+def enumerate_wpm_bits(job: SearchJob) -> Result:
+    """enumerate_wpm returning the canonical bitsets (no PureComplex build)."""
+    facets = list(job.facets)
+    if not facets:
+        raise PurityError("incidence of an empty facet set")
+    order = sorted(range(len(facets)), key=lambda i: facets[i])
+    if order != list(range(len(facets))):
+        raise ValueError("SearchJob.facets must be in canonical (ascending) order")
+    with Plan.universes(job.m, job.n, [facets], _facet_cap(job), job.required, job.forbidden, job.device) as p:
+        p.run()
+        return p.fetch()
+
+
+def enumerate_wpm(job: SearchJob) -> List[List[int]]:
+    """search.hpp:141-258: every nonempty WPM inside job.facets satisfying the
+    properties, canonical order; each as its ascending facet-mask list."""
+    res = enumerate_wpm_bits(job)
+    return [bits_to_facets(row, job.facets) for row in res.map_bits(0)]
+
+
+def matroid_universe(d: DualCharMatrix) -> List[int]:
+    """pipeline.hpp:33-35 via kernel 1."""
+    cols = charmap_of_dcm(d)
+    with Plan.charmaps(d.m - d.p, d.m, [cols], WPM_CAP_UBT, 0) as p:
+        return p.universe(0)
+
+
+def write_complex(m: int, n: int, facets: Sequence[int]) -> str:
+    """complex_io.hpp:21-32."""
+    lines = [f"{m} {n}"]
+    for f in facets:
+        lines.append(" ".join(str(v) for v in range(1, 64) if (f >> v) & 1))
+    return "\n".join(lines) + "\n"
+
+
+def write_complexes(m: int, n: int, complexes: Sequence[Sequence[int]]) -> str:
+    """complex_io.hpp:34-39."""
+    return "\n".join(write_complex(m, n, K) for K in complexes)
+
+
+def write_cplx_bytes(res: Result, i: int, m: int, n: int, universe: Sequence[int]) -> bytes:
+    """Serialise map i of a result through the C-ABI writer (byte-exact .cplx)."""
+    uni, up = _u64(universe)
+    # rebuild a transient wpm_result_t view for the writer
+    rr = _Result()
+    rr.num_maps = res.num_maps
+    rr.words = res.words
+    rr.total = res.total
+    counts = (ctypes.c_int64 * max(res.num_maps, 1))(*res.counts)
+    offsets = (ctypes.c_int64 * (res.num_maps + 1))(*res.offsets)
+    bits = np.ascontiguousarray(res.bits.reshape(-1) if res.bits.size else np.zeros(1, dtype=np.uint64))
+    rr.counts = counts
+    rr.offsets = offsets
+    rr.bits = bits.ctypes.data_as(_u64p)
+    need = int(_lib.wpm_write_cplx(ctypes.byref(rr), i, m, n, up, None, 0))
+    if need < 0:
+        _check(-need)
+    buf = ctypes.create_string_buffer(max(need, 1))
+    _lib.wpm_write_cplx(ctypes.byref(rr), i, m, n, up, buf, need)
+    return buf.raw[:need]

@@ -1,0 +1,725 @@
+// api.cu -- the C-ABI (include/wpm_b200.h) and the host orchestration.
+//
+// Host side of the path: IDCM orbits (charmap.hpp:212-281) and
+// charmap_of_dcm (charmap.hpp:155-204) in C++, then everything
+// data-parallel on the device: kernel 1 (universes), kernel 2 (incidence),
+// kernel 3 (search), the canonical sort.  The per-orbit sequential loop of
+// pipeline.hpp:383-397 becomes ONE persistent launch over every map's search
+// tree; job.threads / parallel_for_index (parallel.hpp:27-54) becomes the
+// device work queue.  There is no CPU fallback: no device, no result.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/wpm_b200.h"
+#include "wpm_dev.cuh"
+#include "wpm_internal.h"
+
+namespace wpm {
+int k3_layout_bytes(int maxM, int maxN, int maxDepth);
+}
+
+using namespace wpm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CU(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return fail(WPM_EINTERNAL, std::string(#call) + ": " + cudaGetErrorString(e_));       \
+    } while (0)
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    int ensure(size_t count) {
+        if (count <= n && p) return 0;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        if (cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)) != cudaSuccess) return 1;
+        n = std::max<size_t>(count, 1);
+        return 0;
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+int64_t cyclic_bound(int n) {  // affine_property.hpp:35-45
+    auto binom = [](int64_t top, int64_t k) -> int64_t {
+        if (top < k) return 0;
+        int64_t r = 1;
+        for (int64_t i = 1; i <= k; ++i) r = r * (top - k + i) / i;
+        return r;
+    };
+    return binom(n + 4 - (n + 1) / 2, 4) + binom(n + 3 - n / 2, 4);
+}
+
+}  // namespace
+
+struct wpm_plan {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 0;
+    int n = 0, m = 0, num_maps = 0;
+    int64_t facet_cap = WPM_CAP_UBT;
+    std::vector<int32_t> M, N, cap;
+    std::vector<MapDesc> desc;
+    int maxM = 0, maxN = 0, maxDepth = 0, w32 = 0, mw = 0;
+    // device tables
+    DevBuf<MapDesc> d_maps;
+    DevBuf<uint32_t> d_facets, d_ridges;
+    DevBuf<uint16_t> d_fr, d_rp;
+    DevBuf<uint8_t> d_npar;
+    DevBuf<int32_t> d_tmpi;
+    // pins (map-major mw words), optional
+    std::vector<uint32_t> pin_in, pin_out;
+    bool has_pins = false;
+    DevBuf<uint32_t> d_pin_in, d_pin_out;
+    // work queue
+    DevBuf<uint32_t> d_qrec;
+    DevBuf<unsigned long long> d_qready, d_qctl;
+    int qcap = 0, recw = 0;
+    DevBuf<int32_t> d_task_map, d_task_f, d_task_kind;
+    // outputs
+    DevBuf<uint32_t> d_out_bits, d_sorted_bits;
+    DevBuf<uint16_t> d_out_map, d_sorted_map;
+    DevBuf<unsigned long long> d_out_ctl, d_per_map;
+    DevBuf<uint32_t> d_idx_a;
+    DevBuf<uint8_t> d_temp;
+    unsigned long long out_cap = 0;
+    // last run
+    long long total = 0, nodes = 0, tasks = 0, dups = 0;
+    std::vector<unsigned long long> per_map;
+    float ms_search = 0, ms_sort = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    int warps = 0;
+};
+
+// ------------------------------------------------------------------ host
+
+extern "C" const char* wpm_last_error(void) { return g_err.c_str(); }
+
+extern "C" int wpm_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+    return c;
+}
+
+extern "C" int64_t wpm_cyclic_facet_bound(int32_t n) { return cyclic_bound(n); }
+
+// idcm_orbits (charmap.hpp:212-281): one representative per S_n x GL-free
+// (column permutation) orbit of injective [M; I_p]; representative = the
+// lexicographically least sorted row list over the p! bit shuffles; the
+// representatives sorted; identity rows appended.
+extern "C" int32_t wpm_idcm_orbits(int32_t n, int32_t p, uint32_t* rows_out, int32_t cap) {
+    if (n < 1 || p < 1 || p > 8) return -fail(WPM_EINVAL, "unsupported (n, p)");
+    if (n + p > (1 << p) - 1) return -fail(WPM_EINVAL, "no injective dual matrix: m exceeds 2^p - 1");
+    std::vector<uint32_t> pool;
+    for (uint32_t v = 1; v < (1u << p); ++v)
+        if (v & (v - 1)) pool.push_back(v);
+    if (n > (int)pool.size()) return -fail(WPM_EINVAL, "no injective dual matrix: m exceeds 2^p - 1");
+    std::vector<int> perm(p);
+    std::iota(perm.begin(), perm.end(), 0);
+    std::vector<std::vector<uint32_t>> shuffles;  // shuffles[q][v] = image of v
+    do {
+        std::vector<uint32_t> img(1u << p, 0);
+        for (uint32_t v = 0; v < (1u << p); ++v)
+            for (int b = 0; b < p; ++b)
+                if ((v >> b) & 1u) img[v] |= 1u << perm[b];
+        shuffles.push_back(std::move(img));
+    } while (std::next_permutation(perm.begin(), perm.end()));
+    std::set<std::vector<uint32_t>> reps;
+    std::vector<int> idx(n);
+    std::iota(idx.begin(), idx.end(), 0);
+    std::vector<uint32_t> cur(n), best(n);
+    const int P = (int)pool.size();
+    for (;;) {
+        bool first = true;
+        for (const auto& img : shuffles) {
+            for (int i = 0; i < n; ++i) cur[i] = img[pool[idx[i]]];
+            std::sort(cur.begin(), cur.end());
+            if (first || cur < best) best = cur;
+            first = false;
+        }
+        reps.insert(best);
+        int pos = n - 1;
+        while (pos >= 0 && idx[pos] == P - (n - pos)) --pos;
+        if (pos < 0) break;
+        ++idx[pos];
+        for (int i = pos + 1; i < n; ++i) idx[i] = idx[i - 1] + 1;
+    }
+    const int m = n + p;
+    int k = 0;
+    for (const auto& r : reps) {
+        if (k < cap && rows_out) {
+            for (int i = 0; i < n; ++i) rows_out[(size_t)k * m + i] = r[i];
+            for (int i = 0; i < p; ++i) rows_out[(size_t)k * m + n + i] = 1u << i;
+        }
+        ++k;
+    }
+    return k;
+}
+
+// charmap_of_dcm (charmap.hpp:155-204): lambda = [I_n | M^t] in standard
+// form, else a kernel basis of D^t by elimination.
+extern "C" int32_t wpm_charmap_of_dcm(int32_t m, int32_t p, const uint32_t* rows, uint32_t* cols) {
+    const int n = m - p;
+    if (n < 1 || m > 31) return -fail(WPM_EINVAL, "unsupported dual matrix shape");
+    for (int i = 0; i < m; ++i) cols[i] = 0;
+    bool standard = true;
+    for (int i = 0; i < p; ++i) standard &= rows[m - p + i] == (1u << i);
+    if (standard) {
+        for (int i = 0; i < n; ++i) cols[i] = 1u << i;
+        for (int j = 0; j < p; ++j)
+            for (int i = 0; i < n; ++i)
+                if ((rows[i] >> j) & 1u) cols[n + j] |= 1u << i;
+        return n;
+    }
+    std::vector<uint64_t> a(p, 0);
+    for (int j = 0; j < p; ++j)
+        for (int v = 0; v < m; ++v)
+            if ((rows[v] >> j) & 1u) a[j] |= 1ull << v;
+    std::vector<int> piv;
+    int rank = 0;
+    for (int c = 0; c < m && rank < p; ++c) {
+        int r0 = -1;
+        for (int r = rank; r < p; ++r)
+            if ((a[r] >> c) & 1u) { r0 = r; break; }
+        if (r0 < 0) continue;
+        std::swap(a[rank], a[r0]);
+        for (int r = 0; r < p; ++r)
+            if (r != rank && ((a[r] >> c) & 1u)) a[r] ^= a[rank];
+        piv.push_back(c);
+        ++rank;
+    }
+    if (rank != p) return -fail(WPM_EINVAL, "dual matrix is rank deficient");
+    int row = 0;
+    for (int fc = 0; fc < m; ++fc) {
+        if (std::find(piv.begin(), piv.end(), fc) != piv.end()) continue;
+        cols[fc] |= 1u << row;
+        for (int r = 0; r < rank; ++r)
+            if ((a[r] >> fc) & 1u) cols[piv[r]] |= 1u << row;
+        ++row;
+    }
+    return n;
+}
+
+// ------------------------------------------------------------------ plans
+
+static int plan_init(wpm_plan* P, int device) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        return fail(WPM_EINTERNAL, "no CUDA device: the B200 path has no CPU fallback");
+    if (device < 0 || device >= count) return fail(WPM_EINVAL, "device ordinal out of range");
+    P->device = device;
+    CU(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) return fail(WPM_EINTERNAL, "device is not sm_100 (Blackwell); this build targets sm_100a");
+    P->num_sms = prop.multiProcessorCount;
+    CU(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+    for (auto& e : P->ev) CU(cudaEventCreate(&e));
+    return WPM_OK;
+}
+
+static int resolve_cap(int64_t facet_cap, int n, int M) {
+    (void)M;
+    if (facet_cap == WPM_CAP_UBT) return (int)cyclic_bound(n);
+    if (facet_cap < 0) return INT32_MAX;
+    return (int)std::min<int64_t>(facet_cap, INT32_MAX);
+}
+
+// lay out tables once M is known per map (facets already on device at
+// d_facets with per-map offsets `foff`), run kernel 2, finish the plan.
+static int plan_build_tables(wpm_plan* P, const std::vector<uint32_t>& foff) {
+    const int K = P->num_maps;
+    P->desc.assign(K, MapDesc{});
+    size_t fr_tot = 0, r_tot = 0;
+    P->maxM = 0;
+    for (int i = 0; i < K; ++i) {
+        const int M = P->M[i];
+        if (M <= 0) return fail(WPM_EINVAL, "empty facet universe (incidence of an empty facet set)");
+        if (M > WPM_MAX_FACETS) return fail(WPM_EINVAL, "universe larger than WPM_MAX_FACETS");
+        MapDesc& d = P->desc[i];
+        d.M = M;
+        d.n = P->n;
+        d.m = P->m;
+        d.cap = P->cap[i];
+        d.facet_off = foff[i];
+        d.fr_off = (uint32_t)(fr_tot * FR);
+        const size_t rcap = std::min<size_t>(binom_small(P->m, P->n - 1), (size_t)M * P->n);
+        d.ridge_off = (uint32_t)r_tot;
+        d.rp_off = (uint32_t)(r_tot * RP);
+        d.np_off = (uint32_t)r_tot;
+        fr_tot += (size_t)M;
+        r_tot += rcap;
+        P->maxM = std::max(P->maxM, M);
+    }
+    if (P->d_maps.ensure(K) || P->d_ridges.ensure(r_tot) || P->d_fr.ensure(fr_tot * FR) ||
+        P->d_rp.ensure(r_tot * RP) || P->d_npar.ensure(r_tot) || P->d_tmpi.ensure(K + 1))
+        return fail(WPM_EINTERNAL, "device allocation failed (tables)");
+    CU(cudaMemcpyAsync(P->d_maps.p, P->desc.data(), K * sizeof(MapDesc), cudaMemcpyHostToDevice, P->stream));
+    CU(cudaMemsetAsync(P->d_tmpi.p, 0, (K + 1) * sizeof(int32_t), P->stream));
+    if (launch_k2_incidence(K, P->d_maps.p, P->m, P->n, P->d_facets.p, P->d_ridges.p, P->d_fr.p, P->d_rp.p,
+                            P->d_npar.p, P->d_tmpi.p, P->d_tmpi.p + K, P->stream))
+        return fail(WPM_EINTERNAL, std::string("kernel 2 launch: ") + cudaGetErrorString(cudaGetLastError()));
+    std::vector<int32_t> hN(K + 1);
+    CU(cudaMemcpyAsync(hN.data(), P->d_tmpi.p, (K + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaStreamSynchronize(P->stream));
+    if (hN[K]) return fail(WPM_EINVAL, "a ridge has more than WPM_MAX_PARENTS candidate facets");
+    P->N.assign(hN.begin(), hN.begin() + K);
+    P->maxN = 0;
+    P->maxDepth = 0;
+    for (int i = 0; i < K; ++i) {
+        P->desc[i].N = P->N[i];
+        if (P->N[i] > WPM_MAX_RIDGES) return fail(WPM_EINVAL, "more than WPM_MAX_RIDGES ridges");
+        P->maxN = std::max(P->maxN, P->N[i]);
+        P->maxDepth = std::max(P->maxDepth, std::min(P->cap[i], P->M[i]) + 1);
+    }
+    CU(cudaMemcpyAsync(P->d_maps.p, P->desc.data(), K * sizeof(MapDesc), cudaMemcpyHostToDevice, P->stream));
+    P->mw = (P->maxM + 31) / 32;
+    P->w32 = 2 * ((P->maxM + 63) / 64);
+    P->recw = 4 + 2 * P->mw;
+    CU(cudaStreamSynchronize(P->stream));
+    return WPM_OK;
+}
+
+static int create_from_cols(int32_t n, int32_t m, int32_t K, const uint32_t* cols, int64_t facet_cap,
+                            int32_t device, wpm_plan_t** out) {
+    *out = nullptr;
+    if (n < 1 || m < n || m > WPM_MAX_M) return fail(WPM_EINVAL, "unsupported (m, n): need 1 <= n <= m <= 16");
+    if (K < 1) return fail(WPM_EINVAL, "no characteristic maps");
+    auto* P = new wpm_plan();
+    int rc = plan_init(P, device);
+    if (rc) { delete P; return rc; }
+    P->n = n;
+    P->m = m;
+    P->num_maps = K;
+    P->facet_cap = facet_cap;
+    const int stride = (int)binom_small(m, n);
+    DevBuf<uint32_t> d_cols;
+    if (d_cols.ensure((size_t)K * m) || P->d_facets.ensure((size_t)K * stride) || P->d_tmpi.ensure(K + 1)) {
+        delete P;
+        return fail(WPM_EINTERNAL, "device allocation failed (universes)");
+    }
+    cudaMemcpyAsync(d_cols.p, cols, (size_t)K * m * sizeof(uint32_t), cudaMemcpyHostToDevice, P->stream);
+    if (launch_k1_universe(n, m, K, d_cols.p, P->d_facets.p, stride, P->d_tmpi.p, P->stream)) {
+        delete P;
+        return fail(WPM_EINTERNAL, "kernel 1 launch failed");
+    }
+    P->M.assign(K, 0);
+    cudaMemcpyAsync(P->M.data(), P->d_tmpi.p, K * sizeof(int32_t), cudaMemcpyDeviceToHost, P->stream);
+    if (cudaStreamSynchronize(P->stream) != cudaSuccess) {
+        delete P;
+        return fail(WPM_EINTERNAL, std::string("kernel 1: ") + cudaGetErrorString(cudaGetLastError()));
+    }
+    for (int i = 0; i < K; ++i)
+        if (P->M[i] < 0) {
+            delete P;
+            return fail(WPM_EINVAL, "matrix is rank deficient");
+        }
+    P->cap.resize(K);
+    std::vector<uint32_t> foff(K);
+    for (int i = 0; i < K; ++i) {
+        P->cap[i] = resolve_cap(facet_cap, n, P->M[i]);
+        foff[i] = (uint32_t)((size_t)i * stride);
+    }
+    rc = plan_build_tables(P, foff);
+    if (rc) { delete P; return rc; }
+    *out = P;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_create_charmaps(int32_t n, int32_t m, int32_t num_maps, const uint32_t* cols,
+                                        int64_t facet_cap, int32_t device, wpm_plan_t** out) {
+    return create_from_cols(n, m, num_maps, cols, facet_cap, device, out);
+}
+
+extern "C" int wpm_plan_create_orbits(int32_t n, int32_t p, int64_t facet_cap, int32_t device, wpm_plan_t** out) {
+    *out = nullptr;
+    const int32_t K = wpm_idcm_orbits(n, p, nullptr, 0);
+    if (K < 0) return -K;
+    const int m = n + p;
+    std::vector<uint32_t> rows((size_t)K * m), cols((size_t)K * m);
+    wpm_idcm_orbits(n, p, rows.data(), K);
+    for (int i = 0; i < K; ++i)
+        if (wpm_charmap_of_dcm(m, p, rows.data() + (size_t)i * m, cols.data() + (size_t)i * m) < 0)
+            return WPM_EINVAL;
+    return create_from_cols(n, m, K, cols.data(), facet_cap, device, out);
+}
+
+extern "C" int wpm_plan_create_universes(int32_t m, int32_t n, int32_t K, const int32_t* counts,
+                                         const uint64_t* facets, int64_t facet_cap, const int32_t* required,
+                                         int32_t num_required, const int32_t* forbidden, int32_t num_forbidden,
+                                         int32_t device, wpm_plan_t** out) {
+    *out = nullptr;
+    if (n < 1 || m < n || m > WPM_MAX_M) return fail(WPM_EINVAL, "unsupported (m, n): need 1 <= n <= m <= 16");
+    if (K < 1) return fail(WPM_EINVAL, "no universes");
+    if ((num_required || num_forbidden) && K != 1) return fail(WPM_EINVAL, "pins need a single universe");
+    // validate: pure, labels in 1..m, strictly ascending (PureComplex::validate, complex.hpp:37-55)
+    std::vector<uint32_t> h;
+    std::vector<uint32_t> foff(K);
+    size_t off = 0;
+    const uint64_t full = ((1ull << m) - 1ull) << 1;
+    for (int i = 0; i < K; ++i) {
+        foff[i] = (uint32_t)off;
+        if (counts[i] <= 0) return fail(WPM_EINVAL, "incidence of an empty facet set");
+        for (int j = 0; j < counts[i]; ++j) {
+            const uint64_t f = facets[off + j];
+            if (f & ~full) return fail(WPM_EINVAL, "facet uses a label outside 1..m");
+            if (__builtin_popcountll(f) != n) return fail(WPM_EINVAL, "facet size differs from n (purity)");
+            if (j > 0 && !(facets[off + j - 1] < f))
+                return fail(WPM_EINVAL, "universe not in canonical (strictly ascending) order");
+            h.push_back((uint32_t)f);
+        }
+        off += counts[i];
+    }
+    auto* P = new wpm_plan();
+    int rc = plan_init(P, device);
+    if (rc) { delete P; return rc; }
+    P->n = n;
+    P->m = m;
+    P->num_maps = K;
+    P->facet_cap = facet_cap;
+    P->M.assign(counts, counts + K);
+    P->cap.resize(K);
+    for (int i = 0; i < K; ++i) P->cap[i] = resolve_cap(facet_cap, n, P->M[i]);
+    if (P->d_facets.ensure(h.size())) { delete P; return fail(WPM_EINTERNAL, "device allocation failed"); }
+    cudaMemcpyAsync(P->d_facets.p, h.data(), h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, P->stream);
+    rc = plan_build_tables(P, foff);
+    if (rc) { delete P; return rc; }
+    if (num_required || num_forbidden) {
+        const int M = P->M[0];
+        P->pin_in.assign(P->mw, 0);
+        P->pin_out.assign(P->mw, 0);
+        for (int i = 0; i < num_required; ++i) {
+            const int f = required[i];
+            if (f < 0 || f >= M) { delete P; return fail(WPM_EINVAL, "required facet index out of range"); }
+            P->pin_in[f >> 5] |= 1u << (f & 31);
+        }
+        for (int i = 0; i < num_forbidden; ++i) {
+            const int f = forbidden[i];
+            if (f < 0 || f >= M) { delete P; return fail(WPM_EINVAL, "forbidden facet index out of range"); }
+            P->pin_out[f >> 5] |= 1u << (f & 31);
+        }
+        P->has_pins = true;
+    }
+    *out = P;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_num_maps(const wpm_plan_t* P) { return P ? P->num_maps : 0; }
+
+extern "C" int32_t wpm_plan_universe(wpm_plan_t* P, int32_t map, uint64_t* out, int32_t cap) {
+    if (!P || map < 0 || map >= P->num_maps) return -fail(WPM_EINVAL, "bad map index");
+    cudaSetDevice(P->device);
+    const int M = P->M[map];
+    std::vector<uint32_t> h(M);
+    if (cudaMemcpy(h.data(), P->d_facets.p + P->desc[map].facet_off, M * sizeof(uint32_t), cudaMemcpyDeviceToHost) !=
+        cudaSuccess)
+        return -fail(WPM_EINTERNAL, "copy failed");
+    for (int j = 0; j < M && j < cap; ++j) out[j] = h[j];
+    return M;
+}
+
+extern "C" int32_t wpm_plan_incidence(wpm_plan_t* P, int32_t map, uint64_t* ridges_out, int32_t ridges_cap,
+                                      int32_t* cols_out, int32_t* par_out) {
+    if (!P || map < 0 || map >= P->num_maps) return -fail(WPM_EINVAL, "bad map index");
+    cudaSetDevice(P->device);
+    const MapDesc& d = P->desc[map];
+    const int M = d.M, N = d.N, n = d.n;
+    if (ridges_cap < N) return N;
+    std::vector<uint32_t> r(N);
+    std::vector<uint16_t> fr((size_t)M * FR), rp((size_t)N * RP);
+    if (cudaMemcpy(r.data(), P->d_ridges.p + d.ridge_off, N * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(fr.data(), P->d_fr.p + d.fr_off, fr.size() * 2, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(rp.data(), P->d_rp.p + d.rp_off, rp.size() * 2, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -fail(WPM_EINTERNAL, "copy failed");
+    for (int i = 0; i < N; ++i) ridges_out[i] = r[i];
+    if (cols_out)
+        for (int j = 0; j < M; ++j)
+            for (int k = 0; k < n; ++k) cols_out[j * n + k] = fr[(size_t)j * FR + k];
+    if (par_out)
+        for (int i = 0; i < N; ++i)
+            for (int q = 0; q < RP; ++q) {
+                const uint16_t g = rp[(size_t)i * RP + q];
+                par_out[i * RP + q] = g == NONE16 ? -1 : (int32_t)g;
+            }
+    return N;
+}
+
+static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
+    const int K = P->num_maps;
+    // root tasks: (f, map) f-major so the largest subtrees start first;
+    // pinned universes get one ENTRY task
+    std::vector<int32_t> tm, tf, tk;
+    if (P->has_pins) {
+        tm.push_back(0);
+        tf.push_back(0);
+        tk.push_back(3);
+    } else {
+        int maxM = 0;
+        for (int i = 0; i < K; ++i) maxM = std::max(maxM, P->M[i]);
+        for (int f = 0; f < maxM; ++f)
+            for (int i = 0; i < K; ++i)
+                if (f < P->M[i] && P->n + 1 <= P->cap[i]) {
+                    tm.push_back(i);
+                    tf.push_back(f);
+                    tk.push_back(0);
+                }
+    }
+    if (shard_count > 1) {
+        size_t k = 0;
+        for (size_t t = 0; t < tm.size(); ++t)
+            if ((int)(t % shard_count) == shard_index) {
+                tm[k] = tm[t];
+                tf[k] = tf[t];
+                tk[k] = tk[t];
+                ++k;
+            }
+        tm.resize(k);
+        tf.resize(k);
+        tk.resize(k);
+    }
+    const int ntasks = (int)tm.size();
+    int qcap = 1 << 16;
+    while (qcap < 2 * ntasks) qcap <<= 1;
+    P->qcap = qcap;
+    if (P->d_qrec.ensure((size_t)qcap * P->recw) || P->d_qready.ensure(qcap) || P->d_qctl.ensure(8) ||
+        P->d_task_map.ensure(ntasks + 1) || P->d_task_f.ensure(ntasks + 1) || P->d_task_kind.ensure(ntasks + 1) ||
+        P->d_out_ctl.ensure(2) || P->d_per_map.ensure(K))
+        return fail(WPM_EINTERNAL, "device allocation failed (queue)");
+    if (P->has_pins) {
+        if (P->d_pin_in.ensure(P->mw) || P->d_pin_out.ensure(P->mw))
+            return fail(WPM_EINTERNAL, "device allocation failed (pins)");
+        CU(cudaMemcpyAsync(P->d_pin_in.p, P->pin_in.data(), P->mw * 4, cudaMemcpyHostToDevice, P->stream));
+        CU(cudaMemcpyAsync(P->d_pin_out.p, P->pin_out.data(), P->mw * 4, cudaMemcpyHostToDevice, P->stream));
+    }
+    if (P->out_cap == 0) P->out_cap = 1ull << 20;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        if (P->d_out_bits.ensure(P->out_cap * P->w32) || P->d_out_map.ensure(P->out_cap))
+            return fail(WPM_EINTERNAL, "device allocation failed (output)");
+        if (ntasks) {
+            CU(cudaMemcpyAsync(P->d_task_map.p, tm.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
+            CU(cudaMemcpyAsync(P->d_task_f.p, tf.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
+            CU(cudaMemcpyAsync(P->d_task_kind.p, tk.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
+        }
+        unsigned long long ctl[8] = {0, (unsigned long long)ntasks, (unsigned long long)ntasks, 0, 0, 0, 0, 0};
+        CU(cudaMemcpyAsync(P->d_qctl.p, ctl, sizeof(ctl), cudaMemcpyHostToDevice, P->stream));
+        CU(cudaMemsetAsync(P->d_qready.p, 0, (size_t)qcap * 8, P->stream));
+        CU(cudaMemsetAsync(P->d_out_ctl.p, 0, 16, P->stream));
+        CU(cudaMemsetAsync(P->d_per_map.p, 0, K * 8, P->stream));
+        SearchParams sp{};
+        sp.num_maps = K;
+        sp.max_M = P->maxM;
+        sp.max_N = P->maxN;
+        sp.max_n = P->n;
+        sp.max_depth = P->maxDepth;
+        sp.maps = P->d_maps.p;
+        sp.fr = P->d_fr.p;
+        sp.rp = P->d_rp.p;
+        sp.npar = P->d_npar.p;
+        sp.qrec = P->d_qrec.p;
+        sp.qready = P->d_qready.p;
+        sp.qctl = P->d_qctl.p;
+        sp.qcap = qcap;
+        sp.recw = P->recw;
+        sp.mw = P->mw;
+        sp.out_bits = P->d_out_bits.p;
+        sp.out_map = P->d_out_map.p;
+        sp.out_ctl = P->d_out_ctl.p;
+        sp.per_map = P->d_per_map.p;
+        sp.out_cap = P->out_cap;
+        sp.w32 = P->w32;
+        if (launch_seed_tasks(sp, ntasks, P->d_task_map.p, P->d_task_f.p, P->d_task_kind.p,
+                              P->has_pins ? P->d_pin_in.p : nullptr, P->has_pins ? P->d_pin_out.p : nullptr,
+                              P->stream))
+            return fail(WPM_EINTERNAL, "seed launch failed");
+        const int est_warps = P->num_sms * 16;
+        sp.hungry = std::max(64, est_warps / 2);
+        CU(cudaEventRecord(P->ev[0], P->stream));
+        if (ntasks > 0 && !launch_k3_search(sp, P->num_sms, P->stream, &P->warps))
+            return fail(WPM_EINTERNAL, std::string("kernel 3 launch: ") + cudaGetErrorString(cudaGetLastError()));
+        CU(cudaEventRecord(P->ev[1], P->stream));
+        unsigned long long octl[2], qc[8];
+        CU(cudaMemcpyAsync(octl, P->d_out_ctl.p, 16, cudaMemcpyDeviceToHost, P->stream));
+        CU(cudaMemcpyAsync(qc, P->d_qctl.p, sizeof(qc), cudaMemcpyDeviceToHost, P->stream));
+        CU(cudaStreamSynchronize(P->stream));
+        P->total = (long long)octl[0];
+        P->tasks = (long long)qc[3];
+        P->nodes = (long long)qc[4];
+        if (octl[0] <= P->out_cap) break;
+        P->out_cap = octl[0] + octl[0] / 8 + 1024;  // exact count known now: rerun once
+    }
+    P->per_map.assign(K, 0);
+    CU(cudaMemcpyAsync(P->per_map.data(), P->d_per_map.p, K * 8, cudaMemcpyDeviceToHost, P->stream));
+    // canonical sort
+    const long long total = P->total;
+    const size_t tb = canon_sort_temp_bytes(std::max<long long>(total, 1), P->w32);
+    if (P->d_temp.ensure(tb) || P->d_idx_a.ensure(total + 1) || P->d_sorted_bits.ensure((size_t)total * P->w32 + 1) ||
+        P->d_sorted_map.ensure(total + 1))
+        return fail(WPM_EINTERNAL, "device allocation failed (sort)");
+    CU(cudaMemsetAsync(P->d_out_ctl.p + 1, 0, 8, P->stream));
+    CU(cudaEventRecord(P->ev[2], P->stream));
+    if (canon_sort(P->d_out_bits.p, P->d_out_map.p, total, P->w32, P->d_sorted_bits.p, P->d_sorted_map.p,
+                   P->d_temp.p, P->d_temp.n, P->d_idx_a.p, nullptr, P->d_out_ctl.p + 1, P->stream))
+        return fail(WPM_EINTERNAL, std::string("canonical sort: ") + cudaGetErrorString(cudaGetLastError()));
+    CU(cudaEventRecord(P->ev[3], P->stream));
+    unsigned long long dups = 0;
+    CU(cudaMemcpyAsync(&dups, P->d_out_ctl.p + 1, 8, cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaStreamSynchronize(P->stream));
+    P->dups = (long long)dups;
+    CU(cudaEventElapsedTime(&P->ms_search, P->ev[0], P->ev[1]));
+    CU(cudaEventElapsedTime(&P->ms_sort, P->ev[2], P->ev[3]));
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_run(wpm_plan_t* P, int32_t shard_index, int32_t shard_count, int64_t* total_out) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (shard_count < 1) shard_count = 1;
+    if (shard_index < 0 || shard_index >= shard_count) return fail(WPM_EINVAL, "bad shard index");
+    CU(cudaSetDevice(P->device));
+    const int rc = plan_search(P, shard_index, shard_count);
+    if (rc) return rc;
+    if (total_out) *total_out = P->total;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_stats(const wpm_plan_t* P, double* ms_search, double* ms_sort, int64_t* nodes,
+                              int64_t* tasks) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (ms_search) *ms_search = P->ms_search;
+    if (ms_sort) *ms_sort = P->ms_sort;
+    if (nodes) *nodes = P->nodes;
+    if (tasks) *tasks = P->tasks;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_fetch(wpm_plan_t* P, wpm_result_t** out) {
+    *out = nullptr;
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    CU(cudaSetDevice(P->device));
+    const int K = P->num_maps;
+    auto* R = new wpm_result_t();
+    R->num_maps = K;
+    R->words = P->w32 / 2;
+    R->total = P->total;
+    R->counts = new int64_t[K];
+    R->offsets = new int64_t[K + 1];
+    R->offsets[0] = 0;
+    for (int i = 0; i < K; ++i) {
+        R->counts[i] = (int64_t)P->per_map[i];
+        R->offsets[i + 1] = R->offsets[i] + R->counts[i];
+    }
+    R->bits = new uint64_t[(size_t)std::max<long long>(P->total, 1) * R->words];
+    if (P->total > 0) {
+        const cudaError_t e = cudaMemcpyAsync(R->bits, P->d_sorted_bits.p, (size_t)P->total * P->w32 * 4,
+                                              cudaMemcpyDeviceToHost, P->stream);
+        if (e != cudaSuccess || cudaStreamSynchronize(P->stream) != cudaSuccess) {
+            wpm_result_free(R);
+            return fail(WPM_EINTERNAL, "result copy failed");
+        }
+    }
+    R->nodes = P->nodes;
+    R->duplicates = P->dups;
+    R->ms_search = P->ms_search;
+    R->ms_sort = P->ms_sort;
+    R->tasks = P->tasks;
+    *out = R;
+    return WPM_OK;
+}
+
+extern "C" void wpm_plan_destroy(wpm_plan_t* P) {
+    if (!P) return;
+    cudaSetDevice(P->device);
+    if (P->stream) cudaStreamSynchronize(P->stream);
+    for (auto& e : P->ev)
+        if (e) cudaEventDestroy(e);
+    cudaStream_t s = P->stream;
+    delete P;
+    if (s) cudaStreamDestroy(s);
+}
+
+extern "C" void wpm_result_free(wpm_result_t* R) {
+    if (!R) return;
+    delete[] R->counts;
+    delete[] R->offsets;
+    delete[] R->bits;
+    delete R;
+}
+
+extern "C" int wpm_enumerate(const wpm_job_t* job, wpm_result_t** out) {
+    *out = nullptr;
+    if (!job) return fail(WPM_EINVAL, "null job");
+    const int32_t M = job->num_facets;
+    wpm_plan_t* P = nullptr;
+    int rc = wpm_plan_create_universes(job->m, job->n, 1, &M, job->facets, job->facet_cap, job->required,
+                                       job->num_required, job->forbidden, job->num_forbidden, job->device, &P);
+    if (rc) return rc;
+    rc = wpm_plan_run(P, job->shard_count > 1 ? job->shard_index : 0, std::max(1, job->shard_count), nullptr);
+    if (!rc) rc = wpm_plan_fetch(P, out);
+    wpm_plan_destroy(P);
+    return rc;
+}
+
+extern "C" int wpm_enumerate_orbits(int32_t n, int32_t p, int64_t facet_cap, int32_t device, wpm_result_t** out) {
+    *out = nullptr;
+    wpm_plan_t* P = nullptr;
+    int rc = wpm_plan_create_orbits(n, p, facet_cap, device, &P);
+    if (rc) return rc;
+    rc = wpm_plan_run(P, 0, 1, nullptr);
+    if (!rc) rc = wpm_plan_fetch(P, out);
+    wpm_plan_destroy(P);
+    return rc;
+}
+
+// write_complex / write_complexes (complex_io.hpp:21-39)
+extern "C" int64_t wpm_write_cplx(const wpm_result_t* R, int32_t map, int32_t m, int32_t n, const uint64_t* universe,
+                                  char* buf, int64_t buf_len) {
+    if (!R || map < 0 || map >= R->num_maps) return -fail(WPM_EINVAL, "bad map index");
+    int64_t len = 0;
+    char line[512];
+    auto put = [&](const char* s, int k) {
+        if (len + k <= buf_len && buf) std::memcpy(buf + len, s, (size_t)k);
+        len += k;
+    };
+    const int W = R->words;
+    for (int64_t i = R->offsets[map]; i < R->offsets[map + 1]; ++i) {
+        if (i > R->offsets[map]) put("\n", 1);
+        int k = std::snprintf(line, sizeof(line), "%d %d\n", m, n);
+        put(line, k);
+        const uint64_t* K = R->bits + (size_t)i * W;
+        for (int w = 0; w < W; ++w)
+            for (uint64_t x = K[w]; x; x &= x - 1) {
+                const uint64_t f = universe[w * 64 + __builtin_ctzll(x)];
+                k = 0;
+                bool first = true;
+                for (uint64_t y = f; y; y &= y - 1) {
+                    if (!first) line[k++] = ' ';
+                    k += std::snprintf(line + k, sizeof(line) - (size_t)k, "%d", __builtin_ctzll(y));
+                    first = false;
+                }
+                line[k++] = '\n';
+                put(line, k);
+            }
+    }
+    return len;
+}

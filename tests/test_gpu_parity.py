@@ -1,0 +1,198 @@
+"""Parity of the CUDA path (through the C-ABI) against the oracle and the
+reference's golden vectors.  Bit-exact: the same canonical WPM lists, the same
+per-map counts, the same `.cplx` bytes; node counts equal to the CPU
+restatement of the device search."""
+import hashlib
+import random
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _digest_plan(wpm, plan, res, n):
+    h = hashlib.sha256()
+    per = []
+    for i in range(plan.num_maps):
+        b = wpm.write_cplx_bytes(res, i, n + 4, n, plan.universe(i))
+        per.append(hashlib.sha256(b).hexdigest())
+        h.update(b)
+    return h.hexdigest(), per
+
+
+@pytest.mark.parametrize("n", list(range(2, 12)))
+def test_kernel1_universes(wpm, oracle, golden, n):
+    """binary_matroid (charmap.hpp:117-141) on the GPU == the restatement, every map."""
+    rows = golden["orbits"][str(n)]
+    with wpm.Plan.orbits(n) as p:
+        assert p.num_maps == len(rows)
+        for i, r in enumerate(rows):
+            assert p.universe(i) == oracle.matroid_universe(r), (n, i)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 8, 11])
+def test_kernel2_incidence(wpm, oracle, golden, n):
+    """incidence_matrix (incidence.hpp:34-55): ridges, cols and parents."""
+    rows = golden["orbits"][str(n)]
+    with wpm.Plan.orbits(n) as p:
+        for i in range(min(3, len(rows))):
+            uni = p.universe(i)
+            assert p.incidence(i) == oracle.incidence(uni), (n, i)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 6])
+def test_orbit_counts_and_nodes(wpm, golden, n):
+    """Per-map WPM counts == reference (App. A); DFS nodes == CPU restatement."""
+    with wpm.Plan.orbits(n) as p:
+        p.run()
+        res = p.fetch()
+    assert res.duplicates == 0
+    assert res.counts == [m["wpms"] for m in golden["ubt"][str(n)]["maps"]]
+    assert res.nodes == golden["dfs"][str(n)]["nodes"]
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5])
+def test_orbit_digests(wpm, golden, n):
+    """Byte-exact .cplx per map and per n (SURVEY App. C protocol)."""
+    with wpm.Plan.orbits(n) as p:
+        p.run()
+        res = p.fetch()
+        whole, per = _digest_plan(wpm, p, res, n)
+    assert per == golden["ubt"][str(n)]["map_sha256"]
+    assert whole == golden["ubt"][str(n)]["sha256"]
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5])
+def test_nocap_counts(wpm, golden, n):
+    """No property: every WPM (classify_full_universe semantics)."""
+    with wpm.Plan.orbits(n, facet_cap=wpm.WPM_CAP_NONE) as p:
+        p.run()
+        res = p.fetch()
+        whole, _ = _digest_plan(wpm, p, res, n)
+    assert res.counts == golden["nocap"][str(n)]["counts"]
+    assert whole == golden["nocap"][str(n)]["sha256"]
+
+
+def test_small_examples(wpm, oracle):
+    """test_search.cpp:104-121 and :269-274."""
+    u = oracle.all_subsets_universe(4, 2)
+    out = wpm.enumerate_wpm(wpm.SearchJob(4, 2, u))
+    assert len(out) == 7
+    assert sorted(len(k) for k in out) == [3, 3, 3, 3, 4, 4, 4]
+    s3 = oracle.all_subsets_universe(4, 3)
+    out = wpm.enumerate_wpm(wpm.SearchJob(4, 3, s3))
+    assert out == [s3]
+    # two disjoint edges: empty output is valid
+    assert wpm.enumerate_wpm(wpm.SearchJob(4, 2, [0b00110, 0b11000])) == []
+
+
+def _random_universes(seed, count, mlo, mhi, nlo, nhi, Mlo, Mhi, oracle, keep=3):
+    rng = random.Random(seed)
+    out = []
+    while len(out) < count:
+        m = rng.randint(mlo, mhi)
+        n = rng.randint(nlo, nhi)
+        if n >= m:
+            continue
+        u = [f for f in oracle.all_subsets_universe(m, n) if rng.randrange(keep) == 0]
+        if Mlo <= len(u) <= Mhi:
+            out.append((m, n, u))
+    return out
+
+
+def test_full_subset_universes_vs_oracles(wpm, oracle):
+    """acceptance.cpp:259-262 shapes: all n-subsets of [m] vs brute force and
+    the restated reference, bit-exact lists."""
+    for m, n in [(4, 2), (5, 2), (6, 2), (7, 2), (4, 3), (5, 3), (6, 3), (6, 4), (5, 4), (6, 5), (7, 5), (7, 6)]:
+        u = oracle.all_subsets_universe(m, n)
+        res = wpm.enumerate_wpm_bits(wpm.SearchJob(m, n, u))
+        assert res.duplicates == 0
+        if len(u) <= 24:
+            assert res.total == oracle.brute_force_count(u), (m, n)
+        rc, ref = oracle.enumerate_ref(m, n, u)
+        assert rc == 0
+        assert np.array_equal(res.map_bits(0), ref["bits"]), (m, n)
+        cnt, nodes, _ = oracle.dfs(n, u, -1, want_bits=False)
+        assert res.nodes == nodes
+
+
+def test_random_universes_vs_bruteforce(wpm, oracle):
+    """acceptance.cpp:264-279: random universes, M in [8, 24]."""
+    for m, n, u in _random_universes(20240809, 12, 6, 8, 2, 4, 8, 24, oracle):
+        for cap in (-1, 4, 7):
+            job = wpm.SearchJob(m, n, u, properties=[wpm.AffineProperty([-1] * len(u), cap + 1)] if cap >= 0 else [])
+            res = wpm.enumerate_wpm_bits(job)
+            assert res.total == oracle.brute_force_count(u, cap=cap), (m, n, cap)
+            cnt, nodes, bits = oracle.dfs(n, u, cap)
+            assert np.array_equal(res.map_bits(0), bits)
+            assert res.nodes == nodes
+
+
+def test_constrained_vs_bruteforce(wpm, oracle):
+    """acceptance.cpp:281-315: required/forbidden pins vs brute force."""
+    rng = random.Random(20240809)
+    made = 0
+    while made < 10:
+        u = [f for f in oracle.all_subsets_universe(6, 3) if rng.randrange(2) == 0]
+        if not 10 <= len(u) <= 18:
+            continue
+        req, forb = [], []
+        for j in range(len(u)):
+            roll = rng.randrange(10)
+            if roll == 0:
+                req.append(j)
+            elif roll == 1:
+                forb.append(j)
+        made += 1
+        if set(req) & set(forb):
+            continue
+        res = wpm.enumerate_wpm_bits(wpm.SearchJob(6, 3, u, required=req, forbidden=forb))
+        assert res.total == oracle.brute_force_count(u, req, forb), (u, req, forb)
+        cnt, nodes, bits = oracle.dfs(3, u, -1, req, forb)
+        assert np.array_equal(res.map_bits(0), bits)
+        assert res.nodes == nodes
+
+
+def test_octahedron_link_pinning(wpm, oracle):
+    """test_search.cpp:178-220: pinned link of vertex 1 == filtered unconstrained."""
+    u = oracle.all_subsets_universe(6, 3)
+    octa = sorted(sum(1 << (i + 1 + (3 if (c >> i) & 1 else 0)) for i in range(3)) for c in range(8))
+    req = [j for j, f in enumerate(u) if f & 2 and f in octa]
+    forb = [j for j, f in enumerate(u) if f & 2 and f not in octa]
+    pinned = wpm.enumerate_wpm(wpm.SearchJob(6, 3, u, required=req, forbidden=forb))
+    full = wpm.enumerate_wpm(wpm.SearchJob(6, 3, u))
+    filt = [K for K in full if all(u[j] in K for j in req) and not any(u[j] in K for j in forb)]
+    assert pinned == filt and len(pinned) > 0
+
+
+@pytest.mark.parametrize("n", [5, 6])
+def test_shards_partition(wpm, golden, n):
+    """Root-task sharding (the multi-GPU split): shards are disjoint, their
+    union is the full canonical list, node counts add up."""
+    with wpm.Plan.orbits(n) as p:
+        p.run()
+        full = p.fetch()
+        parts = []
+        nodes = 0
+        for s in range(3):
+            p.run(s, 3)
+            r = p.fetch()
+            parts.append(r)
+            nodes += r.nodes
+    assert nodes == full.nodes
+    for i in range(full.num_maps):
+        rows = np.concatenate([r.map_bits(i) for r in parts])
+        assert rows.shape[0] == full.counts[i]
+        got = {tuple(x) for x in rows.tolist()}
+        assert got == {tuple(x) for x in full.map_bits(i).tolist()}
+
+
+def test_deterministic_repeat(wpm):
+    """test_search.cpp:147-157 analogue: identical bytes across runs."""
+    with wpm.Plan.orbits(5) as p:
+        p.run()
+        a = p.fetch()
+        p.run()
+        b = p.fetch()
+    assert np.array_equal(a.bits, b.bits) and a.nodes == b.nodes
