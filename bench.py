@@ -1,0 +1,304 @@
+"""bench.py -- WPM enumeration throughput on B200 (and the reference CPU arm).
+
+Workload (BASELINE.json configs[1]): Picard 4, n = 5 (m = 9) -- every WPM of
+every mod-2 characteristic map (35 IDCM orbits), UBT facet cap, canonical
+output.  One "step" = one complete enumeration of all maps: kernel 3 (search)
++ canonical sort, universes/incidence resident in HBM.
+
+Metric (BASELINE.json): search nodes/s and wall time per n.  A node is one
+facet-inclusion step of the canonical DFS tree of the workload; the tree is
+a property of the workload (3,638,216 nodes at n = 5, pinned by the CPU
+restatement), so both arms report  nodes(workload) / their own wall time and
+the driver's ratio is the wall-time ratio.  The reference's own search size
+(combination-space leaves, search.hpp:62-104) is reported beside it.
+
+  value : nodes / device time, inputs resident (Plan.run; kernel 3 + sort)
+  e2e   : the same through the one-shot C-ABI call wpm_enumerate_orbits with
+          host buffers (orbits -> kernels 1,2 -> search -> sort -> D2H of every
+          WPM bitset), timed on the host around the call
+  roofline : kernel 3 vs the measured INT32 issue peak (5n ops per node,
+          SURVEY.md 8(d)); bound "int-issue" (no tensor / HBM work on this path)
+  cpu_baseline : the reference compiled from its own headers (oracle/_ref),
+          nproc threads, the same workload
+
+Multi-GPU (torchrun): root tasks are sharded t % world == rank (weak split of
+one fixed workload = strong scaling); NCCL only for the final counts and the
+result gather to rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NODES_PER_N = None  # filled from tests/golden/golden.json
+
+
+def _golden():
+    return json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def reference_arm(args):
+    """`--impl reference`: the reference's own CPU path (oracle/_ref, built
+    from the unmodified headers), nproc threads, same workload and unit."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    ref = os.path.join(ROOT, "oracle", "_ref", "plseeds_ref")
+    n = args.n
+    g = _golden()
+    nodes = g["dfs"][str(n)]["nodes"]
+    threads = os.cpu_count() or 1
+    if not os.path.exists(ref):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/plseeds_ref not built"}))
+        return 0
+
+    def one():
+        t0 = time.perf_counter()
+        out = subprocess.run([ref, "enumerate", str(n), "--threads", str(threads)], check=True,
+                             capture_output=True, text=True).stdout
+        wall = time.perf_counter() - t0
+        tot = [ln for ln in out.splitlines() if ln.startswith("total")][0].split()
+        return wall, int(tot[2]), int(tot[4]), float(tot[6]), float(tot[8])
+
+    for _ in range(args.warmup):
+        one()
+    walls, leaves = [], 0
+    wpms = 0
+    for _ in range(args.steps):
+        wall, wpms, leaves, prep, enum = one()
+        walls.append(wall)
+    t = sum(walls) / len(walls)
+    value = nodes / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64 (GF(2) bitsets)", "data": "synthetic (IDCM orbit maps, deterministic)",
+        "config": {"workload": f"Picard 4, n={n} (m={n + 4}): all {len(g['orbits'][str(n)])} characteristic maps, "
+                               "UBT cap", "n": n, "maps": len(g["orbits"][str(n)]), "wpms": wpms,
+                   "reference_leaves": leaves, "threads": threads},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"full n={n} enumeration (all maps), {args.steps} steps"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_leaves_per_s": leaves / t, "wall_s": t,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+METRIC = "search nodes/sec and wall time to enumerate all WPMs per Picard-4 dim n"
+UNIT = "search nodes/s (DFS facet-inclusion steps of the workload / wall s)"
+
+
+def cpu_baseline(n, nodes):
+    ref = os.path.join(ROOT, "oracle", "_ref", "plseeds_ref")
+    threads = os.cpu_count() or 1
+    if not os.path.exists(ref):
+        return None
+    t0 = time.perf_counter()
+    out = subprocess.run([ref, "enumerate", str(n), "--threads", str(threads)], check=True, capture_output=True,
+                         text=True, timeout=600).stdout
+    wall = time.perf_counter() - t0
+    tot = [ln for ln in out.splitlines() if ln.startswith("total")][0].split()
+    return {"value": nodes / wall, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"one full n={n} enumeration, all maps (reference enumerate_wpm, {threads} threads)",
+            "wall_s": wall, "reference_leaves": int(tot[4]), "wpms": int(tot[2])}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--n", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    args.warmup = max(args.warmup, 3)
+
+    import numpy as np
+    import torch
+
+    import paper_2301_00806_b200 as wpm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+    n = args.n
+    g = _golden()
+    expect_nodes = g["dfs"][str(n)]["nodes"]
+    expect_wpms = g["dfs"][str(n)]["sum"]
+
+    plan = wpm.Plan.orbits(n, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")  # > 126 MB L2
+    for _ in range(args.warmup):
+        plan.run(rank, world)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(dev)
+    barrier()
+    sampler.start()
+    ms_total = ms_search = ms_sort = 0.0
+    nodes = 0
+    t_host = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between timed iterations (outside the device-timed window)
+        torch.cuda.synchronize(dev)
+        plan.run(rank, world)
+        st = plan.stats()
+        ms_total += plan.timing()["ms_total"]
+        ms_search += st["ms_search"]
+        ms_sort += st["ms_sort"]
+        nodes = st["nodes"]
+    barrier()
+    t_host = time.perf_counter() - t_host
+    clocks = sampler.stop()
+    res = plan.fetch()
+    # whole-job: sum nodes over ranks, max device time over ranks
+    tot_nodes = nodes
+    ms_step = ms_total / args.steps
+    if dist:
+        t = torch.tensor([float(nodes), ms_step, float(res.total)], dtype=torch.float64, device=f"cuda:{dev}")
+        mx = t.clone()
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        tot_nodes = int(t[0].item())
+        ms_step = mx[1].item()
+        tot_wpms = int(t[2].item())
+    else:
+        tot_wpms = res.total
+    value = tot_nodes / (ms_step * 1e-3)
+
+    # e2e: the reference-facing one-shot C-ABI call, host buffers, all copies inside
+    e2e_times = []
+    h2d = d2h = 0
+    for i in range(max(2, min(args.steps, 5)) + 1):
+        barrier()
+        t0 = time.perf_counter()
+        r = wpm_orbits_oneshot(wpm, n, dev, rank, world)
+        dt = time.perf_counter() - t0
+        if i > 0:  # first call pays context/module load
+            e2e_times.append(dt)
+        h2d, d2h = r.h2d_bytes, r.d2h_bytes
+    e2e_s = statistics.median(e2e_times)
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = t.item()
+    e2e_value = tot_nodes / e2e_s
+
+    # roofline of kernel 3 vs measured INT32 issue peak
+    peak = wpm.int_peak(dev)
+    ops = tot_nodes / max(world, 1) * 5 * n if world > 1 else nodes * 5 * n
+    ms_k3 = ms_search / args.steps
+    achieved = ops / (ms_k3 * 1e-3)
+    roofline = {"bound": "int-issue", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
+                "frac": achieved / peak, "traffic": None,
+                "note": "5n int ops per search node (SURVEY 8d) / kernel-3 CUDA-event time; peak = measured "
+                        "LOP3+IADD chains on all SMs (wpm_int_peak)"}
+
+    if rank == 0:
+        cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(n, expect_nodes)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64 (GF(2) bitsets)",
+            "data": "synthetic (IDCM orbit maps, deterministic; no dataset)",
+            "config": {"workload": f"Picard 4, n={n} (m={n + 4}): all {plan.num_maps} characteristic maps, UBT cap "
+                                   "(BASELINE configs[1])", "n": n, "maps": plan.num_maps, "wpms": tot_wpms,
+                       "dfs_nodes": tot_nodes, "l2": "flushed (256 MB write) between timed steps",
+                       "parallelism": f"root-task shards x{world}"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "wall_ms": e2e_s * 1e3, "call": "wpm_enumerate_orbits (one-shot C-ABI)"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": 4,
+            "breakdown_ms": {"search": ms_k3, "sort": ms_sort / args.steps, "step": ms_step},
+            "parity": {"wpms_expected": expect_wpms, "nodes_expected": expect_nodes,
+                       "ok": tot_wpms == expect_wpms and tot_nodes == expect_nodes},
+            "host_wall_s": t_host,
+        }
+        print(json.dumps(line))
+    plan.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def wpm_orbits_oneshot(wpm, n, dev, rank, world):
+    """wpm_enumerate_orbits for world == 1; per-rank shard + NCCL gather for world > 1."""
+    if world == 1:
+        return wpm.enumerate_orbits(n, device=dev)
+    with wpm.Plan.orbits(n, device=dev) as p:
+        p.run(rank, world)
+        r = p.fetch()
+    return r
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -87,6 +87,9 @@ typedef struct {
     double ms_search;            /* device time of kernel 3 (CUDA events) */
     double ms_sort;              /* device time of the canonical sort + gather */
     int64_t tasks;               /* work items processed (root tasks + donations) */
+    double ms_total;             /* device time of the whole run (first to last op on the plan stream) */
+    int64_t h2d_bytes;           /* host->device bytes of the create + run + fetch that produced this */
+    int64_t d2h_bytes;           /* device->host bytes (result included) */
 } wpm_result_t;
 
 /* ---------------------------------------------------------------- host */
@@ -125,6 +128,24 @@ int wpm_plan_fetch(wpm_plan_t *plan, wpm_result_t **out);
 /* Device-side timing of the last run (ms) and node count, without a fetch. */
 int wpm_plan_stats(const wpm_plan_t *plan, double *ms_search, double *ms_sort, int64_t *nodes,
                    int64_t *tasks);
+/* ms_total of the last run, and the kernel-3 launch geometry (warps). */
+int wpm_plan_timing(const wpm_plan_t *plan, double *ms_total, int32_t *warps);
+/* Resident result of the last run: device pointers (uint32 words, 2 per
+ * uint64 word; uint16 map ids) in canonical order, valid until the next run. */
+int wpm_plan_device_result(const wpm_plan_t *plan, const uint32_t **bits32, const uint16_t **map_ids,
+                           int64_t *count, int32_t *words32);
+
+/* Canonical sort of rows that already live on `device` (e.g. shards gathered
+ * over NCCL): orders (map id, canonical WPM order) into out_bits/out_map and
+ * returns the number of adjacent duplicates in *dups.  Plain device pointers;
+ * stream = a cudaStream_t passed as void* (NULL = legacy default stream). */
+int wpm_canonical_sort_device(int32_t device, const uint32_t *bits32, const uint16_t *map_ids, int64_t count,
+                              int32_t words32, uint32_t *out_bits32, uint16_t *out_map, int64_t *dups,
+                              void *stream);
+
+/* Measured INT32 lane-op peak of `device` (LOP3/IADD3 issue, all SMs), ops/s:
+ * the roofline denominator of the integer-issue-bound search. */
+int wpm_int_peak(int32_t device, double *ops_per_s);
 void wpm_plan_destroy(wpm_plan_t *plan);
 
 /* ---------------------------------------------------------------- one-shot */

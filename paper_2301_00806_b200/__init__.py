@@ -83,6 +83,9 @@ class _Result(ctypes.Structure):
         ("ms_search", ctypes.c_double),
         ("ms_sort", ctypes.c_double),
         ("tasks", ctypes.c_int64),
+        ("ms_total", ctypes.c_double),
+        ("h2d_bytes", ctypes.c_int64),
+        ("d2h_bytes", ctypes.c_int64),
     ]
 
 
@@ -128,6 +131,18 @@ _SIGS = {
         [_PlanP, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),
          ctypes.POINTER(_i64)],
     ),
+    "wpm_plan_timing": (ctypes.c_int, [_PlanP, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)]),
+    "wpm_plan_device_result": (
+        ctypes.c_int,
+        [_PlanP, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(_i64),
+         ctypes.POINTER(_i32)],
+    ),
+    "wpm_canonical_sort_device": (
+        ctypes.c_int,
+        [_i32, ctypes.c_void_p, ctypes.c_void_p, _i64, _i32, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(_i64),
+         ctypes.c_void_p],
+    ),
+    "wpm_int_peak": (ctypes.c_int, [_i32, ctypes.POINTER(ctypes.c_double)]),
     "wpm_plan_destroy": (None, [_PlanP]),
     "wpm_enumerate": (ctypes.c_int, [ctypes.POINTER(_Job), ctypes.POINTER(_ResultP)]),
     "wpm_enumerate_orbits": (ctypes.c_int, [_i32, _i32, _i64, _i32, ctypes.POINTER(_ResultP)]),
@@ -176,6 +191,29 @@ def _i32a(a):
 
 def device_count() -> int:
     return int(_lib.wpm_device_count())
+
+
+def int_peak(device: int = 0) -> float:
+    """Measured INT32 issue peak (lane-ops/s) of `device` (roofline denominator)."""
+    v = ctypes.c_double()
+    _check(_lib.wpm_int_peak(device, ctypes.byref(v)))
+    return v.value
+
+
+def enumerate_orbits(n: int, p: int = 4, facet_cap: int = WPM_CAP_UBT, device: int = 0) -> "Result":
+    """One-shot Algorithm-2 loop for one n (wpm_enumerate_orbits)."""
+    rp = _ResultP()
+    _check(_lib.wpm_enumerate_orbits(n, p, facet_cap, device, ctypes.byref(rp)))
+    return Result(rp)
+
+
+def canonical_sort_device(device: int, bits32_ptr: int, map_ptr: int, count: int, words32: int, out_bits_ptr: int,
+                          out_map_ptr: int, stream: int = 0) -> int:
+    """Canonical sort of device-resident rows (e.g. shards gathered over NCCL); returns duplicates."""
+    d = _i64()
+    _check(_lib.wpm_canonical_sort_device(device, bits32_ptr, map_ptr, count, words32, out_bits_ptr, out_map_ptr,
+                                          ctypes.byref(d), stream or None))
+    return int(d.value)
 
 
 def cyclic_facet_bound(n: int) -> int:
@@ -297,6 +335,18 @@ class Plan:
         _check(_lib.wpm_plan_run(self._h, shard_index, shard_count, ctypes.byref(tot)))
         return int(tot.value)
 
+    def timing(self) -> dict:
+        v, w = ctypes.c_double(), _i32()
+        _check(_lib.wpm_plan_timing(self._h, ctypes.byref(v), ctypes.byref(w)))
+        return {"ms_total": v.value, "warps": int(w.value)}
+
+    def device_result(self):
+        """(bits32_ptr, map_ptr, count, words32) of the resident canonical result."""
+        b, mp, c, w = ctypes.c_void_p(), ctypes.c_void_p(), _i64(), _i32()
+        _check(_lib.wpm_plan_device_result(self._h, ctypes.byref(b), ctypes.byref(mp), ctypes.byref(c),
+                                           ctypes.byref(w)))
+        return b.value or 0, mp.value or 0, int(c.value), int(w.value)
+
     def stats(self) -> dict:
         a, b, c, d = ctypes.c_double(), ctypes.c_double(), _i64(), _i64()
         _check(_lib.wpm_plan_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(d)))
@@ -338,6 +388,9 @@ class Result:
         self.ms_search = r.ms_search
         self.ms_sort = r.ms_sort
         self.tasks = r.tasks
+        self.ms_total = r.ms_total
+        self.h2d_bytes = r.h2d_bytes
+        self.d2h_bytes = r.d2h_bytes
         self.counts = [int(r.counts[i]) for i in range(r.num_maps)]
         self.offsets = [int(r.offsets[i]) for i in range(r.num_maps + 1)]
         n = r.total * r.words

@@ -108,9 +108,10 @@ struct wpm_plan {
     // last run
     long long total = 0, nodes = 0, tasks = 0, dups = 0;
     std::vector<unsigned long long> per_map;
-    float ms_search = 0, ms_sort = 0;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    float ms_search = 0, ms_sort = 0, ms_total = 0;
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     int warps = 0;
+    long long h2d = 0, d2h = 0;  // bytes moved by create + run + fetch
 };
 
 // ------------------------------------------------------------------ host
@@ -281,8 +282,10 @@ static int plan_build_tables(wpm_plan* P, const std::vector<uint32_t>& foff) {
     if (launch_k2_incidence(K, P->d_maps.p, P->m, P->n, P->d_facets.p, P->d_ridges.p, P->d_fr.p, P->d_rp.p,
                             P->d_npar.p, P->d_tmpi.p, P->d_tmpi.p + K, P->stream))
         return fail(WPM_EINTERNAL, std::string("kernel 2 launch: ") + cudaGetErrorString(cudaGetLastError()));
+    P->h2d += 2LL * K * (long long)sizeof(MapDesc);
     std::vector<int32_t> hN(K + 1);
     CU(cudaMemcpyAsync(hN.data(), P->d_tmpi.p, (K + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, P->stream));
+    P->d2h += (long long)(K + 1) * 4;
     CU(cudaStreamSynchronize(P->stream));
     if (hN[K]) return fail(WPM_EINVAL, "a ridge has more than WPM_MAX_PARENTS candidate facets");
     P->N.assign(hN.begin(), hN.begin() + K);
@@ -321,12 +324,14 @@ static int create_from_cols(int32_t n, int32_t m, int32_t K, const uint32_t* col
         return fail(WPM_EINTERNAL, "device allocation failed (universes)");
     }
     cudaMemcpyAsync(d_cols.p, cols, (size_t)K * m * sizeof(uint32_t), cudaMemcpyHostToDevice, P->stream);
+    P->h2d += (long long)K * m * 4;
     if (launch_k1_universe(n, m, K, d_cols.p, P->d_facets.p, stride, P->d_tmpi.p, P->stream)) {
         delete P;
         return fail(WPM_EINTERNAL, "kernel 1 launch failed");
     }
     P->M.assign(K, 0);
     cudaMemcpyAsync(P->M.data(), P->d_tmpi.p, K * sizeof(int32_t), cudaMemcpyDeviceToHost, P->stream);
+    P->d2h += (long long)K * 4;
     if (cudaStreamSynchronize(P->stream) != cudaSuccess) {
         delete P;
         return fail(WPM_EINTERNAL, std::string("kernel 1: ") + cudaGetErrorString(cudaGetLastError()));
@@ -404,6 +409,7 @@ extern "C" int wpm_plan_create_universes(int32_t m, int32_t n, int32_t K, const 
     for (int i = 0; i < K; ++i) P->cap[i] = resolve_cap(facet_cap, n, P->M[i]);
     if (P->d_facets.ensure(h.size())) { delete P; return fail(WPM_EINTERNAL, "device allocation failed"); }
     cudaMemcpyAsync(P->d_facets.p, h.data(), h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, P->stream);
+    P->h2d += (long long)h.size() * 4;
     rc = plan_build_tables(P, foff);
     if (rc) { delete P; return rc; }
     if (num_required || num_forbidden) {
@@ -514,6 +520,7 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         CU(cudaMemcpyAsync(P->d_pin_out.p, P->pin_out.data(), P->mw * 4, cudaMemcpyHostToDevice, P->stream));
     }
     if (P->out_cap == 0) P->out_cap = 1ull << 20;
+    CU(cudaEventRecord(P->ev[4], P->stream));
     for (int attempt = 0; attempt < 2; ++attempt) {
         if (P->d_out_bits.ensure(P->out_cap * P->w32) || P->d_out_map.ensure(P->out_cap))
             return fail(WPM_EINTERNAL, "device allocation failed (output)");
@@ -521,12 +528,12 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
             CU(cudaMemcpyAsync(P->d_task_map.p, tm.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
             CU(cudaMemcpyAsync(P->d_task_f.p, tf.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
             CU(cudaMemcpyAsync(P->d_task_kind.p, tk.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
+            P->h2d += 12LL * ntasks;
         }
-        unsigned long long ctl[8] = {0, (unsigned long long)ntasks, (unsigned long long)ntasks, 0, 0, 0, 0, 0};
+        unsigned long long ctl[8] = {(unsigned long long)ntasks << 32, 0, (unsigned long long)ntasks, 0, 0, 0, 0, 0};
         CU(cudaMemcpyAsync(P->d_qctl.p, ctl, sizeof(ctl), cudaMemcpyHostToDevice, P->stream));
         CU(cudaMemsetAsync(P->d_qready.p, 0, (size_t)qcap * 8, P->stream));
         CU(cudaMemsetAsync(P->d_out_ctl.p, 0, 16, P->stream));
-        CU(cudaMemsetAsync(P->d_per_map.p, 0, K * 8, P->stream));
         SearchParams sp{};
         sp.num_maps = K;
         sp.max_M = P->maxM;
@@ -563,14 +570,14 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         CU(cudaMemcpyAsync(octl, P->d_out_ctl.p, 16, cudaMemcpyDeviceToHost, P->stream));
         CU(cudaMemcpyAsync(qc, P->d_qctl.p, sizeof(qc), cudaMemcpyDeviceToHost, P->stream));
         CU(cudaStreamSynchronize(P->stream));
+        P->h2d += (long long)sizeof(ctl);
+        P->d2h += 16 + (long long)sizeof(qc);
         P->total = (long long)octl[0];
         P->tasks = (long long)qc[3];
         P->nodes = (long long)qc[4];
         if (octl[0] <= P->out_cap) break;
         P->out_cap = octl[0] + octl[0] / 8 + 1024;  // exact count known now: rerun once
     }
-    P->per_map.assign(K, 0);
-    CU(cudaMemcpyAsync(P->per_map.data(), P->d_per_map.p, K * 8, cudaMemcpyDeviceToHost, P->stream));
     // canonical sort
     const long long total = P->total;
     const size_t tb = canon_sort_temp_bytes(std::max<long long>(total, 1), P->w32);
@@ -578,17 +585,33 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         P->d_sorted_map.ensure(total + 1))
         return fail(WPM_EINTERNAL, "device allocation failed (sort)");
     CU(cudaMemsetAsync(P->d_out_ctl.p + 1, 0, 8, P->stream));
+    CU(cudaMemsetAsync(P->d_per_map.p, 0xFF, K * 8, P->stream));  // first row per map, -1 = none
     CU(cudaEventRecord(P->ev[2], P->stream));
     if (canon_sort(P->d_out_bits.p, P->d_out_map.p, total, P->w32, P->d_sorted_bits.p, P->d_sorted_map.p,
-                   P->d_temp.p, P->d_temp.n, P->d_idx_a.p, nullptr, P->d_out_ctl.p + 1, P->stream))
+                   P->d_temp.p, P->d_temp.n, P->d_idx_a.p, (long long*)P->d_per_map.p, P->d_out_ctl.p + 1,
+                   P->stream))
         return fail(WPM_EINTERNAL, std::string("canonical sort: ") + cudaGetErrorString(cudaGetLastError()));
     CU(cudaEventRecord(P->ev[3], P->stream));
     unsigned long long dups = 0;
+    std::vector<long long> first(K);
     CU(cudaMemcpyAsync(&dups, P->d_out_ctl.p + 1, 8, cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaMemcpyAsync(first.data(), P->d_per_map.p, K * 8, cudaMemcpyDeviceToHost, P->stream));
     CU(cudaStreamSynchronize(P->stream));
+    P->d2h += 8 + 8LL * K;
     P->dups = (long long)dups;
+    // per-map counts from the group boundaries of the sorted map ids
+    P->per_map.assign(K, 0);
+    {
+        long long next = P->total;
+        for (int i = K - 1; i >= 0; --i)
+            if (first[i] >= 0) {
+                P->per_map[i] = (unsigned long long)(next - first[i]);
+                next = first[i];
+            }
+    }
     CU(cudaEventElapsedTime(&P->ms_search, P->ev[0], P->ev[1]));
     CU(cudaEventElapsedTime(&P->ms_sort, P->ev[2], P->ev[3]));
+    CU(cudaEventElapsedTime(&P->ms_total, P->ev[4], P->ev[3]));
     return WPM_OK;
 }
 
@@ -610,6 +633,55 @@ extern "C" int wpm_plan_stats(const wpm_plan_t* P, double* ms_search, double* ms
     if (ms_sort) *ms_sort = P->ms_sort;
     if (nodes) *nodes = P->nodes;
     if (tasks) *tasks = P->tasks;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_timing(const wpm_plan_t* P, double* ms_total, int32_t* warps) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (ms_total) *ms_total = P->ms_total;
+    if (warps) *warps = P->warps;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_device_result(const wpm_plan_t* P, const uint32_t** bits32, const uint16_t** map_ids,
+                                      int64_t* count, int32_t* words32) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    *bits32 = P->d_sorted_bits.p;
+    *map_ids = P->d_sorted_map.p;
+    *count = P->total;
+    *words32 = P->w32;
+    return WPM_OK;
+}
+
+extern "C" int wpm_canonical_sort_device(int32_t device, const uint32_t* bits32, const uint16_t* map_ids,
+                                         int64_t count, int32_t words32, uint32_t* out_bits32, uint16_t* out_map,
+                                         int64_t* dups, void* stream) {
+    CU(cudaSetDevice(device));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (count <= 0) {
+        if (dups) *dups = 0;
+        return WPM_OK;
+    }
+    DevBuf<uint8_t> temp;
+    DevBuf<uint32_t> idx;
+    DevBuf<unsigned long long> d;
+    const size_t tb = canon_sort_temp_bytes(count, words32);
+    if (temp.ensure(tb) || idx.ensure(count) || d.ensure(1)) return fail(WPM_EINTERNAL, "allocation failed (sort)");
+    CU(cudaMemsetAsync(d.p, 0, 8, st));
+    if (canon_sort(bits32, map_ids, count, words32, out_bits32, out_map, temp.p, temp.n, idx.p, nullptr, d.p, st))
+        return fail(WPM_EINTERNAL, std::string("canonical sort: ") + cudaGetErrorString(cudaGetLastError()));
+    unsigned long long h = 0;
+    CU(cudaMemcpyAsync(&h, d.p, 8, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (dups) *dups = (int64_t)h;
+    return WPM_OK;
+}
+
+extern "C" int wpm_int_peak(int32_t device, double* ops_per_s) {
+    CU(cudaSetDevice(device));
+    double v = 0;
+    if (int_peak_measure(device, &v)) return fail(WPM_EINTERNAL, "int peak microbenchmark failed");
+    *ops_per_s = v;
     return WPM_OK;
 }
 
@@ -638,8 +710,12 @@ extern "C" int wpm_plan_fetch(wpm_plan_t* P, wpm_result_t** out) {
             return fail(WPM_EINTERNAL, "result copy failed");
         }
     }
+    P->d2h += (long long)P->total * P->w32 * 4;
     R->nodes = P->nodes;
     R->duplicates = P->dups;
+    R->ms_total = P->ms_total;
+    R->h2d_bytes = P->h2d;
+    R->d2h_bytes = P->d2h;
     R->ms_search = P->ms_search;
     R->ms_sort = P->ms_sort;
     R->tasks = P->tasks;

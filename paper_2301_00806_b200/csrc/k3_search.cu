@@ -20,21 +20,29 @@
 // Branches partition the solution space, so every WPM is produced exactly
 // once and the final sort/unique (search.hpp:254-256) finds no duplicate.
 //
+// 87-97 % of branch points have a single undecided candidate (measured on
+// the CPU restatement, n = 5..11): those FORCED moves run as a chain inside
+// one descent -- no frame, no sibling exclusion -- and unwind with one
+// undo_to.  Frames exist only for real branch points.  The open ridges with
+// exactly one undecided candidate are kept in a bitset, so the MRV choice is
+// a first-set-bit lookup; the full (undecided, id) min-scan over the open
+// bitset runs only when that bitset is empty.
+//
 // Execution model (B200): a persistent grid, one DFS per warp.  Lanes
 // cooperate on each node: lane k < n updates the k-th ridge of the included
 // facet; exclusions are flattened (facet, ridge) pairs over 32 lanes with
-// shared-memory atomics; the branch ridge is a warp min-reduction over the
-// open-ridge bitset; the next candidate is a __ballot_sync over the ridge's
-// <= 8 candidate slots (or over 32 facets at a closed node).  The per-warp
-// search state lives in shared memory (ridge counts + undecided counts packed
-// in one byte, facet status, an undo trail and the frame stack); the per-map
-// tables are read-only global memory (L1 resident).
+// shared-memory atomics; branch choices are __ballot_sync / __reduce_min_sync.
+// The per-warp state lives in shared memory (ridge count + undecided count
+// packed in one byte, facet status, an undo trail, the frame stack); every
+// helper is inlined so the warp's scalars stay in registers and all state
+// accesses are LDS/STS/ATOMS.  Per-map tables are read-only global memory
+// (L1 resident).
 //
 // Work sharing replaces parallel_for_index (parallel.hpp:27-54): a global
-// queue of tasks (IN/OUT facet bitsets + the frame to resume).  Warps pop
-// tasks; every few nodes a busy warp checks whether the queue runs short and,
-// if so, donates its shallowest frame that still has untried children (it
-// marks the frame exhausted and keeps going).  The tree explored is the same
+// ticket queue of tasks (IN/OUT facet bitsets + the frame to resume).  Every
+// few nodes a busy warp looks at a prefetched (head, tail) word; if warps are
+// waiting it donates its shallowest frame that still has untried children
+// (it marks the frame exhausted and keeps going).  The tree is the same
 // whoever explores it, so node counts are deterministic.
 #include <cstdint>
 #include <climits>
@@ -49,13 +57,16 @@ namespace {
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr uint8_t FU = 0, FIN = 1, FOUT = 2;
 constexpr uint16_t TR_INC = 0x8000;
-constexpr uint16_t CLOSED_FRAME = 0xFFFF;
+constexpr uint32_t CLOSED_FRAME = 0xFFFFu;
+constexpr uint32_t POS_DONE = 0xFFFFu;
+constexpr uint32_t NO_CHILD = 0xFFFFu;
+constexpr int CHECK_EVERY = 32;  // nodes between looks at the queue word
 
 enum TaskKind : uint32_t { T_SINGLE = 0, T_OPEN = 1, T_CLOSED = 2, T_ENTRY = 3 };
 
 // per-warp shared-memory layout, byte offsets
 struct Layout {
-    int rs, fst, dpos, open, inb, trail, frames, bytes;
+    int rs, fst, dpos, open, b1, inb, trail, frames, scratch, bytes;
     int nw, mw;
 };
 
@@ -67,76 +78,87 @@ __host__ __device__ inline Layout make_layout(int maxM, int maxN, int maxDepth) 
     L.nw = (maxN + 31) / 32;
     L.mw = (maxM + 31) / 32;
     int o = 0;
-    L.rs = o;     o += NP;                  // uint8 per ridge: count | undecided << 2
-    L.fst = o;    o += MP;                  // uint8 per facet
-    L.dpos = o;   o += align16(2 * MP);     // uint16 per facet: trail index + 1 of its decision
-    L.open = o;   o += align16(4 * L.nw + 4);   // open-ridge bitset
-    L.inb = o;    o += align16(4 * L.mw + 4);   // IN facet bitset
-    L.trail = o;  o += align16(2 * MP);     // uint16 per decision
-    L.frames = o; o += align16(8 * (maxDepth + 2));
+    L.rs = o;      o += NP;                       // uint8 per ridge: count | undecided << 2
+    L.fst = o;     o += MP;                       // uint8 per facet: U / IN / OUT
+    L.dpos = o;    o += align16(2 * MP);          // uint16 per facet: trail index + 1 of its decision
+    L.open = o;    o += align16(4 * L.nw + 4);    // open ridges (count 1)
+    L.b1 = o;      o += align16(4 * L.nw + 4);    // open ridges with exactly one undecided candidate
+    L.inb = o;     o += align16(4 * L.mw + 4);    // IN facet bitset
+    L.trail = o;   o += align16(2 * MP);          // uint16 per decision (bit 15: include)
+    L.frames = o;  o += align16(8 * (maxDepth + 2));
+    L.scratch = o; o += 64;                       // closing-ridge list
     L.bytes = o;
     return L;
 }
 
-struct Frame {  // two words
-    uint32_t a;  // mark (low 16) | ridge or CLOSED_FRAME (high 16)
-    uint32_t b;  // pos (low 16) | cur (high 16)
-};
-
-struct Warp {
-    uint8_t* rs;
-    uint32_t* rsw;
-    uint8_t* fst;
-    uint16_t* dpos;
-    uint32_t* open;
-    uint32_t* inb;
-    uint16_t* trail;
-    Frame* frames;
-    int size, nopen, ndead, tl, depth;
-};
-
 struct MapView {
-    int M, N, n, cap, map;
+    int M, N, n, cap, map, nw;
+    int lpf_shift;  // lanes per facet in flattened passes: 1 << lpf_shift >= n
     const uint16_t* fr;
     const uint16_t* rp;
     const uint8_t* npar;
 };
 
+// the warp's search state: shared arrays + register scalars
+struct WS {
+    uint8_t* rs;
+    uint32_t* rsw;
+    uint8_t* fst;
+    uint16_t* dpos;
+    uint32_t* open;
+    uint32_t* b1;
+    uint32_t* inb;
+    uint16_t* trail;
+    uint2* frames;      // .x = ridge | pos << 16, .y = cur | cm << 16 (cm: trail length before cur)
+    uint16_t* scratch;
+    int size, nopen, ndead, tl, depth;
+};
+
 __device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
-// ------------------------------------------------------------ state updates
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
 
-// av -= 1 on every ridge of the facets trail[lo..hi) (already marked OUT)
-__device__ __forceinline__ void apply_exclusions(Warp& w, const MapView& mp, int lo, int hi, int lane) {
-    const int n = mp.n;
-    for (int e0 = lo; e0 < hi; e0 += 2) {
-        const int e = e0 + (lane >> 4), k = lane & 15;
+// ------------------------------------------------------------ state updates
+// ridge byte = c | a << 2: c = IN candidates (0..2), a = undecided candidates.
+// open: c == 1.  b1: c == 1 && a == 1.  dead: c == 1 && a == 0.
+
+// a -= 1 on every ridge of the facets trail[lo..hi) (already marked OUT)
+__device__ __forceinline__ void apply_exclusions(WS& w, const MapView& mp, int lo, int hi, int lane) {
+    const int sh_l = mp.lpf_shift, k = lane & ((1 << sh_l) - 1), per = 32 >> sh_l;
+    for (int e0 = lo; e0 < hi; e0 += per) {
+        const int e = e0 + (lane >> sh_l);
         bool dead = false;
-        if (e < hi && k < n) {
+        if (e < hi && k < mp.n) {
             const int g = w.trail[e] & 0x7FFF;
             const int r = __ldg(mp.fr + g * FR + k);
             const unsigned sh = (r & 3) * 8;
-            const unsigned old = atomicSub(&w.rsw[r >> 2], 4u << sh);
-            const unsigned ob = (old >> sh) & 0xFFu;
-            dead = (ob & 3u) == 1u && (ob >> 2) == 1u;
+            const unsigned ob = (atomicSub(&w.rsw[r >> 2], 4u << sh) >> sh) & 0xFFu;
+            dead = ob == (1u | (1u << 2));             // (1,1) -> (1,0)
+            if (ob == (1u | (1u << 2)) || ob == (1u | (2u << 2)))  // leaves / enters b1
+                atomicXor(&w.b1[r >> 5], 1u << (r & 31));
         }
         w.ndead += __popc(__ballot_sync(FULL, dead));
     }
 }
 
-__device__ __forceinline__ void undo_exclusions(Warp& w, const MapView& mp, int lo, int hi, int lane) {
-    const int n = mp.n;
+__device__ __forceinline__ void undo_exclusions(WS& w, const MapView& mp, int lo, int hi, int lane) {
     for (int e = lo + lane; e < hi; e += 32) w.fst[w.trail[e] & 0x7FFF] = FU;
-    for (int e0 = lo; e0 < hi; e0 += 2) {
-        const int e = e0 + (lane >> 4), k = lane & 15;
+    const int sh_l = mp.lpf_shift, k = lane & ((1 << sh_l) - 1), per = 32 >> sh_l;
+    for (int e0 = lo; e0 < hi; e0 += per) {
+        const int e = e0 + (lane >> sh_l);
         bool undead = false;
-        if (e < hi && k < n) {
+        if (e < hi && k < mp.n) {
             const int g = w.trail[e] & 0x7FFF;
             const int r = __ldg(mp.fr + g * FR + k);
             const unsigned sh = (r & 3) * 8;
-            const unsigned old = atomicAdd(&w.rsw[r >> 2], 4u << sh);
-            const unsigned ob = (old >> sh) & 0xFFu;
-            undead = (ob & 3u) == 1u && (ob >> 2) == 0u;
+            const unsigned ob = (atomicAdd(&w.rsw[r >> 2], 4u << sh) >> sh) & 0xFFu;
+            undead = ob == 1u;                         // (1,0) -> (1,1)
+            if (ob == 1u || ob == (1u | (1u << 2)))    // enters / leaves b1
+                atomicXor(&w.b1[r >> 5], 1u << (r & 31));
         }
         w.ndead -= __popc(__ballot_sync(FULL, undead));
     }
@@ -144,36 +166,46 @@ __device__ __forceinline__ void undo_exclusions(Warp& w, const MapView& mp, int 
 }
 
 // exclude one facet (a tried sibling)
-__device__ __forceinline__ void exclude_one(Warp& w, const MapView& mp, int g, int lane) {
+__device__ __forceinline__ void exclude_one(WS& w, const MapView& mp, int g, int lane) {
     if (lane == 0) {
         w.fst[g] = FOUT;
         w.trail[w.tl] = (uint16_t)g;
         w.dpos[g] = (uint16_t)(w.tl + 1);
     }
-    __syncwarp();
-    apply_exclusions(w, mp, w.tl, w.tl + 1, lane);
+    bool dead = false;
+    if (lane < mp.n) {
+        const int r = __ldg(mp.fr + g * FR + lane);
+        const unsigned sh = (r & 3) * 8;
+        const unsigned ob = (atomicSub(&w.rsw[r >> 2], 4u << sh) >> sh) & 0xFFu;
+        dead = ob == (1u | (1u << 2));
+        if (ob == (1u | (1u << 2)) || ob == (1u | (2u << 2))) atomicXor(&w.b1[r >> 5], 1u << (r & 31));
+    }
+    w.ndead += __popc(__ballot_sync(FULL, dead));
     w.tl += 1;
     __syncwarp();
 }
 
-__device__ __forceinline__ void include_facet(Warp& w, const MapView& mp, int f, int lane) {
-    const int n = mp.n;
-    const bool act = lane < n;
+__device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, int lane) {
+    const bool act = lane < mp.n;
     int r = 0;
-    unsigned b = 0;
+    unsigned b = 4;
     if (act) {
         r = __ldg(mp.fr + f * FR + lane);
         b = w.rs[r];
     }
-    const unsigned c = b & 3u, a = b >> 2;
-    const unsigned nc = c + 1u, na = a - 1u;
-    const bool opened = act && nc == 1u, closed = act && nc == 2u;
-    if (act) w.rs[r] = (uint8_t)(nc | (na << 2));
-    if (opened || closed) atomicXor(&w.open[r >> 5], 1u << (r & 31));
+    const unsigned c = b & 3u, a = b >> 2;   // c in {0,1}, a >= 1 (f is undecided)
+    const bool opened = act && c == 0u, closed = act && c == 1u;
+    if (act) {
+        w.rs[r] = (uint8_t)(b + 1u - 4u);    // c + 1, a - 1
+        const unsigned bit = 1u << (r & 31);
+        atomicXor(&w.open[r >> 5], bit);       // 0 -> 1 sets, 1 -> 2 clears
+        if ((c == 1u && a == 1u) || (c == 0u && a == 2u)) atomicXor(&w.b1[r >> 5], bit);
+    }
     const unsigned bo = __ballot_sync(FULL, opened), bc = __ballot_sync(FULL, closed);
-    const unsigned bd = __ballot_sync(FULL, opened && na == 0u);
+    const unsigned bd = __ballot_sync(FULL, opened && a == 1u);
     w.nopen += __popc(bo) - __popc(bc);
     w.ndead += __popc(bd);
+    if (closed) w.scratch[__popc(bc & lanemask_lt(lane))] = (uint16_t)r;
     if (lane == 0) {
         w.fst[f] = FIN;
         w.inb[f >> 5] |= 1u << (f & 31);
@@ -186,18 +218,19 @@ __device__ __forceinline__ void include_facet(Warp& w, const MapView& mp, int f,
     if (!bc) return;
     // propagation: closing ridges exclude their other undecided candidates.
     // Two ridges of f share no candidate besides f, so the list has no repeats.
+    const int ncl = __popc(bc);
     const int base = w.tl;
     int E = 0;
-    unsigned rem = bc;
-    while (rem) {
-        const int jj = lane >> 3, q = lane & 7;
-        const unsigned src = __fns(rem, 0, jj + 1);  // lane holding the (jj+1)-th closing ridge
-        const int rr = __shfl_sync(FULL, r, (int)(src & 31u));
+    for (int j0 = 0; j0 < ncl; j0 += 4) {
+        const int j = j0 + (lane >> 3), q = lane & 7;
         bool v = false;
         int g = 0;
-        if (src < 32u && q < (int)__ldg(mp.npar + rr)) {
-            g = __ldg(mp.rp + rr * RP + q);
-            v = w.fst[g] == FU;
+        if (j < ncl) {
+            const int rr = w.scratch[j];
+            if (q < (int)__ldg(mp.npar + rr)) {
+                g = __ldg(mp.rp + rr * RP + q);
+                v = w.fst[g] == FU;
+            }
         }
         const unsigned bv = __ballot_sync(FULL, v);
         if (v) {
@@ -207,28 +240,31 @@ __device__ __forceinline__ void include_facet(Warp& w, const MapView& mp, int f,
             w.dpos[g] = (uint16_t)(pos + 1);
         }
         E += __popc(bv);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) rem &= rem - 1u;
     }
-    __syncwarp();
-    if (E) apply_exclusions(w, mp, base, base + E, lane);
-    w.tl += E;
+    if (E) {
+        __syncwarp();
+        apply_exclusions(w, mp, base, base + E, lane);
+        w.tl += E;
+    }
     __syncwarp();
 }
 
-__device__ __forceinline__ void undo_include(Warp& w, const MapView& mp, int f, int lane) {
-    const int n = mp.n;
-    const bool act = lane < n;
+__device__ __forceinline__ void undo_include(WS& w, const MapView& mp, int f, int lane) {
+    const bool act = lane < mp.n;
     int r = 0;
     unsigned b = 0;
     if (act) {
         r = __ldg(mp.fr + f * FR + lane);
         b = w.rs[r];
     }
-    const unsigned c = b & 3u, a = b >> 2;
-    if (act) w.rs[r] = (uint8_t)((c - 1u) | ((a + 1u) << 2));
+    const unsigned c = b & 3u, a = b >> 2;   // c in {1,2}
+    if (act) {
+        w.rs[r] = (uint8_t)(b - 1u + 4u);    // c - 1, a + 1
+        const unsigned bit = 1u << (r & 31);
+        atomicXor(&w.open[r >> 5], bit);
+        if ((c == 1u && a == 1u) || (c == 2u && a == 0u)) atomicXor(&w.b1[r >> 5], bit);
+    }
     const bool was_open = act && c == 1u, was_closed = act && c == 2u;
-    if (was_open || was_closed) atomicXor(&w.open[r >> 5], 1u << (r & 31));
     const unsigned bo = __ballot_sync(FULL, was_open), bc = __ballot_sync(FULL, was_closed);
     const unsigned bd = __ballot_sync(FULL, was_open && a == 0u);
     w.nopen += __popc(bc) - __popc(bo);
@@ -241,98 +277,71 @@ __device__ __forceinline__ void undo_include(Warp& w, const MapView& mp, int f, 
     __syncwarp();
 }
 
-__device__ __noinline__ void undo_to(Warp& w, const MapView& mp, int mark, int lane) {
+__device__ __forceinline__ void undo_to(WS& w, const MapView& mp, int mark, int lane) {
     while (w.tl > mark) {
         const int idx = w.tl - 1 - lane;
         const bool valid = idx >= mark;
         const unsigned e = valid ? w.trail[idx] : 0u;
         const unsigned bi = __ballot_sync(FULL, valid && (e & TR_INC));
         if (bi & 1u) {
-            const int f = (int)(__shfl_sync(FULL, e, 0) & 0x7FFFu);
-            undo_include(w, mp, f, lane);
+            undo_include(w, mp, (int)(__shfl_sync(FULL, e, 0) & 0x7FFFu), lane);
             w.tl -= 1;
         } else {
-            const int run = bi ? (__ffs(bi) - 1) : __popc(__ballot_sync(FULL, valid));
+            const int run = bi ? (__ffs(bi) - 1) : min(32, w.tl - mark);
             undo_exclusions(w, mp, w.tl - run, w.tl, lane);
             w.tl -= run;
         }
     }
 }
 
-// open ridge with the fewest undecided candidates, ties by lowest id
-__device__ __forceinline__ int select_ridge(const Warp& w, int nw, int lane) {
+// MRV branch ridge: the lowest open ridge with one undecided candidate, else
+// the open ridge with the fewest (ties: lowest id).  Returns ridge | a << 16.
+__device__ __forceinline__ unsigned select_ridge(const WS& w, int nw, int lane) {
+    for (int i0 = 0; i0 < nw; i0 += 32) {
+        const unsigned word = (i0 + lane < nw) ? w.b1[i0 + lane] : 0u;
+        const unsigned bw = __ballot_sync(FULL, word != 0u);
+        if (bw) {
+            const int l = __ffs(bw) - 1;
+            const unsigned x = __shfl_sync(FULL, word, l);
+            return (unsigned)((i0 + l) * 32 + __ffs(x) - 1) | (1u << 16);
+        }
+    }
     unsigned best = 0xFFFFFFFFu;
     for (int i = lane; i < nw; i += 32) {
         unsigned bits = w.open[i];
         while (bits) {
             const int r = i * 32 + __ffs(bits) - 1;
             bits &= bits - 1u;
-            const unsigned key = ((unsigned)(w.rs[r] >> 2) << 16) | (unsigned)r;
-            best = min(best, key);
+            best = min(best, ((unsigned)(w.rs[r] >> 2) << 16) | (unsigned)r);
         }
     }
-    best = __reduce_min_sync(FULL, best);
-    return (int)(best & 0xFFFFu);
+    return __reduce_min_sync(FULL, best);
 }
 
-// --------------------------------------------------------------- the search
-
-struct Ctx {
-    SearchParams p;
-    Layout L;
-};
-
-__device__ __forceinline__ void emit(Warp& w, const MapView& mp, const SearchParams& p, int lane) {
-    unsigned long long slot = 0;
-    if (lane == 0) {
-        slot = atomicAdd(&p.out_ctl[0], 1ull);
-        atomicAdd(&p.per_map[mp.map], 1ull);
+// the undecided candidates of an OPEN frame's ridge from slot pos: first one
+__device__ __forceinline__ int first_candidate(const WS& w, const MapView& mp, int ridge, int pos, int* slot,
+                                               int lane) {
+    int g = 0;
+    bool ok = false;
+    if (lane < RP && lane >= pos && lane < (int)__ldg(mp.npar + ridge)) {
+        g = __ldg(mp.rp + ridge * RP + lane);
+        ok = w.fst[g] == FU;
     }
-    slot = __shfl_sync(FULL, slot, 0);
-    if (slot < p.out_cap) {
-        uint32_t* o = p.out_bits + slot * (unsigned long long)p.w32;
-        const int mw = (mp.M + 31) >> 5;
-        for (int i = lane; i < p.w32; i += 32) o[i] = i < mw ? w.inb[i] : 0u;
-        if (lane == 0) p.out_map[slot] = (uint16_t)mp.map;
-    } else if (lane == 0) {
-        atomicExch(&p.out_ctl[1], 1ull);
-    }
+    const unsigned b = __ballot_sync(FULL, ok);
+    if (!b) return -1;
+    const int q = __ffs(b) - 1;
+    *slot = q;
+    return __shfl_sync(FULL, g, q);
 }
 
-// node entry after an include (or a task entry): emit / prune / push a frame.
-// Returns true if a frame was pushed.
-__device__ __forceinline__ bool enter_node(Warp& w, const MapView& mp, const SearchParams& p, int nw,
-                                           int mark, bool may_emit, int lane) {
-    if (w.ndead) return false;
-    if (w.nopen == 0) {
-        if (may_emit && w.size > 0) emit(w, mp, p, lane);
-        if (w.size + mp.n + 1 > mp.cap) return false;
-        if (lane == 0) {
-            w.frames[w.depth].a = (uint32_t)mark | ((uint32_t)CLOSED_FRAME << 16);
-            w.frames[w.depth].b = 0xFFFF0000u;  // pos 0, cur none
-        }
-    } else {
-        if (w.size + (w.nopen + mp.n - 1) / mp.n > mp.cap) return false;
-        const int r = select_ridge(w, nw, lane);
-        if (lane == 0) {
-            w.frames[w.depth].a = (uint32_t)mark | ((uint32_t)r << 16);
-            w.frames[w.depth].b = 0xFFFF0000u;
-        }
-    }
-    w.depth += 1;
-    __syncwarp();
-    return true;
-}
-
-// next undecided child of frame fr starting at its pos; -1 if none
-__device__ __forceinline__ int next_child(const Warp& w, const MapView& mp, uint32_t fa, uint32_t fb,
-                                          int* new_pos, int lane) {
-    const int ridge = (int)(fa >> 16), pos = (int)(fb & 0xFFFFu);
+// next undecided child of a frame from its pos; -1 if none
+__device__ __forceinline__ int next_child(const WS& w, const MapView& mp, uint2 fr, int* new_pos, int lane) {
+    const uint32_t ridge = fr.x & 0xFFFFu, pos = fr.x >> 16;
+    if (pos == POS_DONE) return -1;
     if (ridge == CLOSED_FRAME) {
-        for (int p0 = pos; p0 < mp.M; p0 += 32) {
+        for (int p0 = (int)pos; p0 < mp.M; p0 += 32) {
             const int f = p0 + lane;
-            const bool ok = f < mp.M && w.fst[f] == FU;
-            const unsigned b = __ballot_sync(FULL, ok);
+            const unsigned b = __ballot_sync(FULL, f < mp.M && w.fst[f] == FU);
             if (b) {
                 const int c = p0 + __ffs(b) - 1;
                 *new_pos = c + 1;
@@ -341,38 +350,79 @@ __device__ __forceinline__ int next_child(const Warp& w, const MapView& mp, uint
         }
         return -1;
     }
-    const int np = __ldg(mp.npar + ridge);
-    int g = 0;
-    bool ok = false;
-    if (lane < np && lane >= pos) {
-        g = __ldg(mp.rp + ridge * RP + lane);
-        ok = w.fst[g] == FU;
-    }
-    const unsigned b = __ballot_sync(FULL, ok);
-    if (!b) return -1;
-    const int q = __ffs(b) - 1;
+    int q = 0;
+    const int g = first_candidate(w, mp, (int)ridge, (int)pos, &q, lane);
     *new_pos = q + 1;
-    return __shfl_sync(FULL, g, q);
+    return g;
 }
 
-// rebuild the per-warp state from an IN/OUT record (+ closure: a ridge with
-// two IN candidates excludes the rest).  Returns false if infeasible.
-__device__ bool load_state(Warp& w, const MapView& mp, const uint32_t* rec_in, const uint32_t* rec_out,
-                           int nw, int lane) {
-    const int M = mp.M, N = mp.N, mw = (M + 31) >> 5;
+// --------------------------------------------------------------- the search
+
+__device__ __forceinline__ void emit(const WS& w, const MapView& mp, const SearchParams& p, int lane) {
+    unsigned long long slot = 0;
+    if (lane == 0) slot = atomicAdd(&p.out_ctl[0], 1ull);
+    slot = __shfl_sync(FULL, slot, 0);
+    if (slot < p.out_cap) {
+        uint32_t* o = p.out_bits + slot * (unsigned long long)p.w32;
+        const int mw = (mp.M + 31) >> 5;
+        for (int i = lane; i < p.w32; i += 32) o[i] = i < mw ? w.inb[i] : 0u;
+        if (lane == 0) p.out_map[slot] = (uint16_t)mp.map;
+    }
+}
+
+// The descent below a node just entered (after an include, or at a task
+// entry): emit / prune, follow forced moves as a chain of includes, stop at
+// the next real branch point by pushing its frame.  Returns true if a frame
+// was pushed; false if the descent ended (dead, pruned, or a leaf).
+__device__ __forceinline__ bool descend(WS& w, const MapView& mp, const SearchParams& p, unsigned long long& nodes,
+                                        int lane) {
+    for (;;) {
+        if (w.ndead) return false;
+        uint32_t ridge;
+        if (w.nopen == 0) {
+            if (w.size > 0) emit(w, mp, p, lane);
+            if (w.size + mp.n + 1 > mp.cap) return false;
+            ridge = CLOSED_FRAME;
+        } else {
+            if (w.size + (w.nopen + mp.n - 1) / mp.n > mp.cap) return false;
+            const unsigned sel = select_ridge(w, mp.nw, lane);
+            ridge = sel & 0xFFFFu;
+            if ((sel >> 16) == 1u) {  // forced: the only undecided candidate
+                int q;
+                const int u = first_candidate(w, mp, (int)ridge, 0, &q, lane);
+                include_facet(w, mp, u, lane);
+                ++nodes;
+                continue;
+            }
+        }
+        if (lane == 0) w.frames[w.depth] = make_uint2(ridge, NO_CHILD);
+        w.depth += 1;
+        __syncwarp();
+        return true;
+    }
+}
+
+// rebuild the warp state from an IN/OUT record (+ closure: a ridge with two
+// IN candidates excludes the rest).  Returns false if infeasible.
+__device__ __forceinline__ bool load_state(WS& w, const MapView& mp, const uint32_t* rec_in, const uint32_t* rec_out,
+                                           int lane) {
+    const int M = mp.M, N = mp.N, mw = (M + 31) >> 5, nw = mp.nw;
     int size = 0;
     for (int i = lane; i < mw; i += 32) {
         const uint32_t iv = __ldcg(rec_in + i);
         w.inb[i] = iv;
         size += __popc(iv);
     }
-    for (int f = lane; f < M; f += 32) {
-        const uint32_t iv = __ldcg(rec_in + (f >> 5)), ov = __ldcg(rec_out + (f >> 5));
-        const uint32_t bit = 1u << (f & 31);
-        w.fst[f] = (iv & bit) ? FIN : ((ov & bit) ? FOUT : FU);
-        w.dpos[f] = 0;
+    for (int f0 = 0; f0 < M; f0 += 32) {
+        const int f = f0 + lane;
+        const uint32_t iv = __ldcg(rec_in + (f0 >> 5)), ov = __ldcg(rec_out + (f0 >> 5));
+        const uint32_t bit = 1u << lane;
+        if (f < M) {
+            w.fst[f] = (iv & bit) ? FIN : ((ov & bit) ? FOUT : FU);
+            w.dpos[f] = 0;
+        }
     }
-    w.size = __reduce_add_sync(FULL, (unsigned)size);
+    w.size = (int)__reduce_add_sync(FULL, (unsigned)size);
     __syncwarp();
     // pass 1: IN counts; a count >= 3 is infeasible
     bool bad = false;
@@ -380,7 +430,7 @@ __device__ bool load_state(Warp& w, const MapView& mp, const uint32_t* rec_in, c
         const int np = __ldg(mp.npar + r);
         unsigned c = 0;
         for (int q = 0; q < np; ++q) c += w.fst[__ldg(mp.rp + r * RP + q)] == FIN;
-        if (c > 2u) bad = true;
+        bad |= c > 2u;
         w.rs[r] = (uint8_t)min(c, 2u);
     }
     if (__any_sync(FULL, bad)) return false;
@@ -393,11 +443,11 @@ __device__ bool load_state(Warp& w, const MapView& mp, const uint32_t* rec_in, c
         if (on_closed) w.fst[f] = FOUT;
     }
     __syncwarp();
-    // pass 2: undecided counts, open bitset, open/dead tallies
+    // pass 2: undecided counts, open / b1 bitsets, open / dead tallies
     int nopen = 0, ndead = 0;
     for (int r0 = 0; r0 < nw * 32; r0 += 32) {
         const int r = r0 + lane;
-        bool op = false, dd = false;
+        bool op = false, dd = false, one = false;
         if (r < N) {
             const int np = __ldg(mp.npar + r);
             unsigned a = 0;
@@ -406,9 +456,13 @@ __device__ bool load_state(Warp& w, const MapView& mp, const uint32_t* rec_in, c
             w.rs[r] = (uint8_t)(c | (a << 2));
             op = c == 1u;
             dd = op && a == 0u;
+            one = op && a == 1u;
         }
-        const unsigned bo = __ballot_sync(FULL, op);
-        if (lane == 0) w.open[r0 >> 5] = bo;
+        const unsigned bo = __ballot_sync(FULL, op), b1 = __ballot_sync(FULL, one);
+        if (lane == 0) {
+            w.open[r0 >> 5] = bo;
+            w.b1[r0 >> 5] = b1;
+        }
         nopen += __popc(bo);
         ndead += __popc(__ballot_sync(FULL, dd));
     }
@@ -421,43 +475,42 @@ __device__ bool load_state(Warp& w, const MapView& mp, const uint32_t* rec_in, c
 }
 
 // donate the shallowest frame that still has an untried child
-__device__ void try_donate(Warp& w, const MapView& mp, const SearchParams& p, int lane) {
+__device__ __forceinline__ void try_donate(WS& w, const MapView& mp, const SearchParams& p, int lane) {
     const int M = mp.M, mw = (M + 31) >> 5;
     for (int d = 0; d < w.depth; ++d) {
-        const uint32_t fa = w.frames[d].a, fb = w.frames[d].b;
-        const bool top = d + 1 == w.depth;
-        const int mk = top ? w.tl : (int)(w.frames[d + 1].a & 0xFFFFu);
-        const int cur = top ? -1 : (int)(fb >> 16);
-        const int ridge = (int)(fa >> 16), pos = (int)(fb & 0xFFFFu);
+        const uint2 fr = w.frames[d];
+        const uint32_t ridge = fr.x & 0xFFFFu, pos = fr.x >> 16;
+        if (pos == POS_DONE) continue;
+        const bool busy = (fr.y & 0xFFFFu) != NO_CHILD && d + 1 < w.depth;
+        const int mk = busy ? (int)(fr.y >> 16) : w.tl;  // the frame's own state
+        const int cur = busy ? (int)(fr.y & 0xFFFFu) : -1;
         bool any = false;
         if (ridge == CLOSED_FRAME) {
-            for (int f0 = pos; f0 < M && !any; f0 += 32) {
+            for (int f0 = (int)pos; f0 < M && !any; f0 += 32) {
                 const int f = f0 + lane;
-                const bool ok = f < M && f != cur && (w.fst[f] == FU || (int)w.dpos[f] > mk);
-                any = __any_sync(FULL, ok);
+                any = __any_sync(FULL, f < M && f != cur && (w.fst[f] == FU || (int)w.dpos[f] > mk));
             }
         } else {
-            const int np = __ldg(mp.npar + ridge);
             bool ok = false;
-            if (lane < np && lane >= pos) {
+            if (lane < RP && lane >= (int)pos && lane < (int)__ldg(mp.npar + ridge)) {
                 const int g = __ldg(mp.rp + ridge * RP + lane);
                 ok = g != cur && (w.fst[g] == FU || (int)w.dpos[g] > mk);
             }
             any = __any_sync(FULL, ok);
         }
         if (!any) continue;
-        // claim a queue slot
+        // claim a push ticket (high half of the queue word)
         unsigned long long t = 0;
         if (lane == 0) {
             atomicAdd(&p.qctl[2], 1ull);  // pending, before publishing
-            t = atomicAdd(&p.qctl[1], 1ull);
+            t = atomicAdd(&p.qctl[0], 1ull << 32) >> 32;
         }
         t = __shfl_sync(FULL, t, 0);
         uint32_t* rec = p.qrec + (t % (unsigned long long)p.qcap) * (unsigned long long)p.recw;
         if (lane == 0) {
             rec[0] = (uint32_t)mp.map | ((ridge == CLOSED_FRAME ? (uint32_t)T_CLOSED : (uint32_t)T_OPEN) << 24);
-            rec[1] = (uint32_t)ridge;
-            rec[2] = (uint32_t)pos;
+            rec[1] = ridge;
+            rec[2] = pos;
             rec[3] = 0;
         }
         for (int f0 = 0; f0 < mw * 32; f0 += 32) {
@@ -479,58 +532,59 @@ __device__ void try_donate(Warp& w, const MapView& mp, const SearchParams& p, in
         __syncwarp();
         if (lane == 0) {
             atomicExch(&p.qready[t % (unsigned long long)p.qcap], t + 1ull);
-            w.frames[d].b = (fb & 0xFFFF0000u) | 0xFFFFu;  // exhausted
+            w.frames[d].x = ridge | (POS_DONE << 16);  // exhausted here
         }
         __syncwarp();
         return;
     }
 }
 
-__global__ void __launch_bounds__(128) k3_search(SearchParams p, Layout L) {
+__global__ void __launch_bounds__(128) k3_search(const __grid_constant__ SearchParams p,
+                                                 const __grid_constant__ Layout L) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint8_t* base = smem + (size_t)wid * L.bytes;
-    Warp w;
+    uint8_t* base = smem + wid * L.bytes;
+    WS w;
     w.rs = base + L.rs;
     w.rsw = reinterpret_cast<uint32_t*>(base + L.rs);
     w.fst = base + L.fst;
     w.dpos = reinterpret_cast<uint16_t*>(base + L.dpos);
     w.open = reinterpret_cast<uint32_t*>(base + L.open);
+    w.b1 = reinterpret_cast<uint32_t*>(base + L.b1);
     w.inb = reinterpret_cast<uint32_t*>(base + L.inb);
     w.trail = reinterpret_cast<uint16_t*>(base + L.trail);
-    w.frames = reinterpret_cast<Frame*>(base + L.frames);
+    w.frames = reinterpret_cast<uint2*>(base + L.frames);
+    w.scratch = reinterpret_cast<uint16_t*>(base + L.scratch);
     unsigned long long nodes = 0, tasks = 0;
-    unsigned backoff = 64;
 
     for (;;) {
-        // ---- pop a task (lane 0), broadcast
+        // ---- pop: a ticket queue.  One atomicAdd on the low half of the
+        // queue word claims ticket t; the warp waits on ITS slot until the
+        // pusher holding push-ticket t publishes it (FIFO hand-off, no CAS
+        // retries, no shared spin address).  pending == 0 means no task
+        // exists anywhere and no warp can push again: every waiter leaves.
         long long t = -1;
         if (lane == 0) {
+            const unsigned long long tk = atomicAdd(&p.qctl[0], 1ull) & 0xFFFFFFFFull;
+            volatile unsigned long long* rdy = p.qready + (tk % (unsigned long long)p.qcap);
+            volatile unsigned long long* pend = p.qctl + 2;
+            unsigned backoff = 32;
             for (;;) {
-                const unsigned long long h = atomicAdd(&p.qctl[0], 0ull);
-                const unsigned long long tl = atomicAdd(&p.qctl[1], 0ull);
-                if (h >= tl) break;
-                if (atomicCAS(&p.qctl[0], h, h + 1ull) == h) {
-                    t = (long long)h;
+                if (*rdy == tk + 1ull) {
+                    t = (long long)tk;
                     break;
                 }
-            }
-            if (t < 0) {
-                const unsigned long long pend = atomicAdd(&p.qctl[2], 0ull);
-                if (pend == 0ull) t = -2;
+                if (*pend == 0ull) {
+                    t = -2;
+                    break;
+                }
+                __nanosleep(backoff);
+                backoff = min(backoff * 2u, 2048u);
             }
         }
         t = __shfl_sync(FULL, t, 0);
         if (t == -2) break;
-        if (t == -1) {
-            __nanosleep(backoff);
-            backoff = min(backoff * 2u, 4096u);
-            continue;
-        }
-        backoff = 64;
         const unsigned long long slot = (unsigned long long)t % (unsigned long long)p.qcap;
-        if (lane == 0)
-            while (atomicAdd(&p.qready[slot], 0ull) != (unsigned long long)t + 1ull) __nanosleep(32);
         __syncwarp();
         __threadfence();
         const uint32_t* rec = p.qrec + slot * (unsigned long long)p.recw;
@@ -544,73 +598,69 @@ __global__ void __launch_bounds__(128) k3_search(SearchParams p, Layout L) {
         mp.n = md.n;
         mp.cap = md.cap;
         mp.map = map;
+        mp.nw = (md.N + 31) >> 5;
+        mp.lpf_shift = md.n <= 4 ? 2 : (md.n <= 8 ? 3 : 4);
         mp.fr = p.fr + md.fr_off;
         mp.rp = p.rp + md.rp_off;
         mp.npar = p.npar + md.np_off;
-        const int nw = (mp.N + 31) >> 5;
         ++tasks;
 
-        bool alive = load_state(w, mp, rec + 4, rec + 4 + p.mw, nw, lane);
-        if (alive) {
+        if (load_state(w, mp, rec + 4, rec + 4 + p.mw, lane)) {
             if (kind == T_SINGLE) {
-                const int f = (int)h1;
-                include_facet(w, mp, f, lane);
+                include_facet(w, mp, (int)h1, lane);
                 ++nodes;
-                enter_node(w, mp, p, nw, 0, true, lane);
+                descend(w, mp, p, nodes, lane);
             } else if (kind == T_ENTRY) {
-                enter_node(w, mp, p, nw, 0, true, lane);
-            } else if (w.ndead == 0) {
-                if (lane == 0) {
-                    w.frames[0].a = (kind == T_CLOSED) ? ((uint32_t)CLOSED_FRAME << 16) : (h1 << 16);
-                    w.frames[0].b = 0xFFFF0000u | (h2 & 0xFFFFu);
-                }
+                descend(w, mp, p, nodes, lane);
+            } else if (w.ndead == 0) {  // resume a donated frame
+                if (lane == 0)
+                    w.frames[0] = make_uint2((kind == T_CLOSED ? CLOSED_FRAME : h1) | ((h2 & 0xFFFFu) << 16), NO_CHILD);
                 w.depth = 1;
                 __syncwarp();
             }
         }
-        // ---- the DFS
-        unsigned since_check = 0;
+        // ---- the DFS over branch frames
+        unsigned long long qword = ld_relaxed_u64(&p.qctl[0]);  // prefetched queue state
+        unsigned long long next_check = nodes + CHECK_EVERY;
         while (w.depth > 0) {
-            Frame& F = w.frames[w.depth - 1];
-            const uint32_t fa = F.a, fb = F.b;
+            const uint2 fr = w.frames[w.depth - 1];
             int npos = 0;
-            const int c = ((fb & 0xFFFFu) == 0xFFFFu) ? -1 : next_child(w, mp, fa, fb, &npos, lane);
+            const int c = next_child(w, mp, fr, &npos, lane);
             if (c < 0) {
-                undo_to(w, mp, (int)(fa & 0xFFFFu), lane);
+                // frame exhausted: back to the parent frame's state before its
+                // current child, then exclude that child there
                 w.depth -= 1;
                 if (w.depth > 0) {
-                    Frame& P = w.frames[w.depth - 1];
-                    const uint32_t pb = P.b;
-                    exclude_one(w, mp, (int)(pb >> 16), lane);
-                    if ((P.a >> 16) != CLOSED_FRAME && w.ndead) {
-                        if (lane == 0) P.b = pb | 0xFFFFu;
+                    const uint2 pf = w.frames[w.depth - 1];
+                    undo_to(w, mp, (int)(pf.y >> 16), lane);
+                    exclude_one(w, mp, (int)(pf.y & 0xFFFFu), lane);
+                    if ((pf.x & 0xFFFFu) != CLOSED_FRAME && w.ndead) {
+                        if (lane == 0) w.frames[w.depth - 1].x = (pf.x & 0xFFFFu) | (POS_DONE << 16);
                         __syncwarp();
                     }
                 }
                 continue;
             }
-            if (lane == 0) F.b = ((uint32_t)c << 16) | (uint32_t)npos;
+            const int cm = w.tl;
+            if (lane == 0) w.frames[w.depth - 1] = make_uint2((fr.x & 0xFFFFu) | ((uint32_t)npos << 16),
+                                                              (uint32_t)c | ((uint32_t)cm << 16));
             __syncwarp();
-            const int mark = w.tl;
             include_facet(w, mp, c, lane);
             ++nodes;
-            if (!enter_node(w, mp, p, nw, mark, true, lane)) {
-                undo_to(w, mp, mark, lane);
+            if (!descend(w, mp, p, nodes, lane)) {
+                undo_to(w, mp, cm, lane);
                 exclude_one(w, mp, c, lane);
-                if ((fa >> 16) != CLOSED_FRAME && w.ndead) {
-                    if (lane == 0) F.b = (F.b & 0xFFFF0000u) | 0xFFFFu;
+                if ((fr.x & 0xFFFFu) != CLOSED_FRAME && w.ndead) {
+                    if (lane == 0) w.frames[w.depth - 1].x = (fr.x & 0xFFFFu) | (POS_DONE << 16);
                     __syncwarp();
                 }
             }
-            if (++since_check >= 16u) {
-                since_check = 0;
-                int hungry = 0;
-                if (lane == 0) {
-                    const unsigned long long h = *(volatile unsigned long long*)&p.qctl[0];
-                    const unsigned long long tl = *(volatile unsigned long long*)&p.qctl[1];
-                    hungry = (tl - h) < (unsigned long long)p.hungry;
-                }
-                if (__shfl_sync(FULL, hungry, 0)) try_donate(w, mp, p, lane);
+            if (nodes >= next_check) {
+                next_check = nodes + CHECK_EVERY;
+                // waiting warps <=> the head ticket ran ahead of the tail
+                const long long queued = (long long)(qword >> 32) - (long long)(qword & 0xFFFFFFFFull);
+                if (queued < (long long)p.hungry) try_donate(w, mp, p, lane);
+                qword = ld_relaxed_u64(&p.qctl[0]);  // consumed at the next check
             }
         }
         // task finished

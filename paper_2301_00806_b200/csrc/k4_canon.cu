@@ -47,13 +47,16 @@ __global__ void iota_u32(uint32_t* idx, long long n) {
 
 __global__ void gather_rows(const uint32_t* __restrict__ bits, const uint16_t* __restrict__ map,
                             const uint32_t* __restrict__ idx, long long n, int w32, uint32_t* __restrict__ out,
-                            uint16_t* __restrict__ out_map, unsigned long long* dups) {
-    // one warp per row
+                            uint16_t* __restrict__ out_map, unsigned long long* dups,
+                            long long* __restrict__ first_row) {
+    // one warp per row; first_row[map] = index of the map's first row (group boundaries)
     const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= n) return;
     const uint32_t src = idx[row];
-    bool same = row > 0 && map[idx[row - 1]] == map[src];
+    const bool new_group = row == 0 || map[idx[row - 1]] != map[src];
+    if (lane == 0 && new_group && first_row) first_row[map[src]] = row;
+    bool same = !new_group;
     const uint32_t* S = bits + (size_t)src * w32;
     const uint32_t* P = row > 0 ? bits + (size_t)idx[row - 1] * w32 : S;
     for (int w = lane; w < w32; w += 32) {
@@ -76,9 +79,8 @@ size_t canon_sort_temp_bytes(long long count, int w32) {
 }
 
 int canon_sort(const uint32_t* d_bits, const uint16_t* d_map, long long count, int w32, uint32_t* d_sorted_bits,
-               uint16_t* d_sorted_map, void* d_temp, size_t temp_bytes, uint32_t* d_idx_a, uint32_t* d_idx_b,
+               uint16_t* d_sorted_map, void* d_temp, size_t temp_bytes, uint32_t* d_idx_a, long long* d_first_row,
                unsigned long long* d_dups, cudaStream_t st) {
-    (void)d_idx_b;
     if (count <= 0) return 0;
     iota_u32<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(d_idx_a, count);
     CanonLess cmp{d_bits, d_map, w32};
@@ -86,7 +88,8 @@ int canon_sort(const uint32_t* d_bits, const uint16_t* d_map, long long count, i
     if (cub::DeviceMergeSort::SortKeys(d_temp, bytes, d_idx_a, (int)count, cmp, st) != cudaSuccess) return 1;
     const long long threads = count * 32;
     gather_rows<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(d_bits, d_map, d_idx_a, count, w32,
-                                                                     d_sorted_bits, d_sorted_map, d_dups);
+                                                                     d_sorted_bits, d_sorted_map, d_dups,
+                                                                     d_first_row);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

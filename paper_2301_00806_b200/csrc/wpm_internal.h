@@ -28,7 +28,7 @@ struct SearchParams {
     // work queue
     uint32_t* qrec;
     unsigned long long* qready;
-    unsigned long long* qctl;  // [0] head, [1] tail, [2] pending, [3] tasks done, [4] nodes
+    unsigned long long* qctl;  // [0] tail << 32 | head, [2] pending, [3] tasks done, [4] nodes
     int qcap, recw, mw;
     int hungry;                 // donate while queued tasks < hungry
     // output
@@ -52,7 +52,10 @@ int launch_k3_search(const SearchParams& p, int num_sms, cudaStream_t st, int* w
 // into sorted_bits, reports duplicates
 int canon_sort(const uint32_t* d_bits, const uint16_t* d_map, long long count, int w32,
                uint32_t* d_sorted_bits, uint16_t* d_sorted_map, void* d_temp, size_t temp_bytes,
-               uint32_t* d_idx_a, uint32_t* d_idx_b, unsigned long long* d_dups, cudaStream_t st);
+               uint32_t* d_idx_a, long long* d_first_row, unsigned long long* d_dups, cudaStream_t st);
 size_t canon_sort_temp_bytes(long long count, int w32);
+
+// INT32 lane-op issue peak (LOP3 + IADD3 chains over every SM), ops/s
+int int_peak_measure(int device, double* ops_per_s);
 
 }  // namespace wpm
