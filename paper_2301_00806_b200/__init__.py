@@ -394,9 +394,18 @@ class Result:
         self.counts = [int(r.counts[i]) for i in range(r.num_maps)]
         self.offsets = [int(r.offsets[i]) for i in range(r.num_maps + 1)]
         n = r.total * r.words
-        self.bits = (np.ctypeslib.as_array(r.bits, shape=(max(n, 1),))[:n].copy().reshape(r.total, r.words)
+        # zero-copy view of the library's (page-locked) result rows; the
+        # block goes back to the library cache when this object dies
+        self._rp = rp
+        self.bits = (np.ctypeslib.as_array(r.bits, shape=(max(n, 1),))[:n].reshape(r.total, r.words)
                      if n else np.zeros((0, r.words), dtype=np.uint64))
-        _lib.wpm_result_free(rp)
+
+    def __del__(self):
+        rp = getattr(self, "_rp", None)
+        if rp is not None:
+            self._rp = None
+            self.bits = None
+            _lib.wpm_result_free(rp)
 
     def map_bits(self, i: int) -> np.ndarray:
         return self.bits[self.offsets[i]:self.offsets[i + 1]]

@@ -10,6 +10,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
+#include <chrono>
+#include <cstdlib>
 #include <climits>
 #include <cstdio>
 #include <cstring>
@@ -44,21 +48,92 @@ int fail(int code, const std::string& msg) {
             return fail(WPM_EINTERNAL, std::string(#call) + ": " + cudaGetErrorString(e_));       \
     } while (0)
 
+// Device buffers come from the stream-ordered caching allocator (the
+// device's default memory pool with an unbounded release threshold), so
+// repeated plans / one-shot calls reuse memory instead of paying
+// cudaMalloc / cudaFree each time.
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
+void init_pool(int device) {
+    static bool done[64] = {false};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[device] = true;
+}
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    cudaStream_t s = nullptr;
     int ensure(size_t count) {
         if (count <= n && p) return 0;
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s);
         p = nullptr;
         n = 0;
-        if (cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)) != cudaSuccess) return 1;
-        n = std::max<size_t>(count, 1);
+        s = g_alloc_stream;
+        const size_t c = std::max<size_t>(count, 1);
+        if (cudaMallocAsync(reinterpret_cast<void**>(&p), c * sizeof(T), s) != cudaSuccess) {
+            p = nullptr;
+            return 1;
+        }
+        n = c;
         return 0;
     }
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+// Result rows live in page-locked host memory from a grow-only cache, so the
+// D2H of the canonical list runs at full PCIe/C2C speed without paying the
+// pinning cost on every call; wpm_result_free returns the block.
+struct PinnedCache {
+    std::mutex mu;
+    std::vector<std::pair<void*, size_t>> free_blocks;
+    void* get(size_t bytes, size_t* got) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            size_t best = (size_t)-1;
+            for (size_t i = 0; i < free_blocks.size(); ++i)
+                if (free_blocks[i].second >= bytes && (best == (size_t)-1 || free_blocks[i].second < free_blocks[best].second))
+                    best = i;
+            if (best != (size_t)-1) {
+                auto b = free_blocks[best];
+                free_blocks.erase(free_blocks.begin() + (long)best);
+                *got = b.second;
+                return b.first;
+            }
+        }
+        void* p = nullptr;
+        const size_t sz = std::max<size_t>(bytes, 1 << 20);
+        if (cudaHostAlloc(&p, sz, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+        *got = sz;
+        return p;
+    }
+    void put(void* p, size_t bytes) {
+        std::lock_guard<std::mutex> lk(mu);
+        free_blocks.emplace_back(p, bytes);
+    }
+};
+PinnedCache g_pinned;
+std::mutex g_block_mu;
+std::unordered_map<void*, size_t> g_block_size;
+
+// WPM_TRACE=1: host-side phase timings on stderr
+struct Trace {
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    Trace() : on(std::getenv("WPM_TRACE") != nullptr), t0(std::chrono::steady_clock::now()) {}
+    void mark(const char* what) {
+        if (!on) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[wpm] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
     }
 };
 
@@ -225,19 +300,54 @@ extern "C" int32_t wpm_charmap_of_dcm(int32_t m, int32_t p, const uint32_t* rows
 
 // ------------------------------------------------------------------ plans
 
+// Per-device context, created once: attributes, and a free list of
+// (stream, events) bundles that plans borrow and return.
+struct DevCtx {
+    bool init = false;
+    int major = 0, num_sms = 0;
+    std::mutex mu;
+    struct Bundle {
+        cudaStream_t s;
+        cudaEvent_t ev[5];
+    };
+    std::vector<Bundle> free_bundles;
+};
+DevCtx g_dev[64];
+std::mutex g_dev_mu;
+
 static int plan_init(wpm_plan* P, int device) {
-    int count = 0;
-    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
-        return fail(WPM_EINTERNAL, "no CUDA device: the B200 path has no CPU fallback");
-    if (device < 0 || device >= count) return fail(WPM_EINVAL, "device ordinal out of range");
+    static int count = -1;
+    if (count < 0 && cudaGetDeviceCount(&count) != cudaSuccess) count = 0;
+    if (count == 0) return fail(WPM_EINTERNAL, "no CUDA device: the B200 path has no CPU fallback");
+    if (device < 0 || device >= count || device >= 64) return fail(WPM_EINVAL, "device ordinal out of range");
     P->device = device;
     CU(cudaSetDevice(device));
-    cudaDeviceProp prop;
-    CU(cudaGetDeviceProperties(&prop, device));
-    if (prop.major < 10) return fail(WPM_EINTERNAL, "device is not sm_100 (Blackwell); this build targets sm_100a");
-    P->num_sms = prop.multiProcessorCount;
-    CU(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
-    for (auto& e : P->ev) CU(cudaEventCreate(&e));
+    DevCtx& dc = g_dev[device];
+    {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        if (!dc.init) {
+            CU(cudaDeviceGetAttribute(&dc.major, cudaDevAttrComputeCapabilityMajor, device));
+            CU(cudaDeviceGetAttribute(&dc.num_sms, cudaDevAttrMultiProcessorCount, device));
+            init_pool(device);
+            dc.init = true;
+        }
+    }
+    if (dc.major < 10) return fail(WPM_EINTERNAL, "device is not sm_100 (Blackwell); this build targets sm_100a");
+    P->num_sms = dc.num_sms;
+    {
+        std::lock_guard<std::mutex> lk(dc.mu);
+        if (!dc.free_bundles.empty()) {
+            const auto b = dc.free_bundles.back();
+            dc.free_bundles.pop_back();
+            P->stream = b.s;
+            for (int i = 0; i < 5; ++i) P->ev[i] = b.ev[i];
+        }
+    }
+    if (!P->stream) {
+        CU(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+        for (auto& e : P->ev) CU(cudaEventCreate(&e));
+    }
+    g_alloc_stream = P->stream;
     return WPM_OK;
 }
 
@@ -265,17 +375,19 @@ static int plan_build_tables(wpm_plan* P, const std::vector<uint32_t>& foff) {
         d.m = P->m;
         d.cap = P->cap[i];
         d.facet_off = foff[i];
-        d.fr_off = (uint32_t)(fr_tot * FR);
+        d.fr_stride = P->n;
+        d.rp_stride = std::min(WPM_MAX_PARENTS, P->m - P->n + 1);
+        d.fr_off = (uint32_t)(fr_tot * P->n);
         const size_t rcap = std::min<size_t>(binom_small(P->m, P->n - 1), (size_t)M * P->n);
         d.ridge_off = (uint32_t)r_tot;
-        d.rp_off = (uint32_t)(r_tot * RP);
+        d.rp_off = (uint32_t)(r_tot * d.rp_stride);
         d.np_off = (uint32_t)r_tot;
         fr_tot += (size_t)M;
         r_tot += rcap;
         P->maxM = std::max(P->maxM, M);
     }
-    if (P->d_maps.ensure(K) || P->d_ridges.ensure(r_tot) || P->d_fr.ensure(fr_tot * FR) ||
-        P->d_rp.ensure(r_tot * RP) || P->d_npar.ensure(r_tot) || P->d_tmpi.ensure(K + 1))
+    if (P->d_maps.ensure(K) || P->d_ridges.ensure(r_tot) || P->d_fr.ensure(fr_tot * P->n) ||
+        P->d_rp.ensure(r_tot * WPM_MAX_PARENTS) || P->d_npar.ensure(r_tot) || P->d_tmpi.ensure(K + 1))
         return fail(WPM_EINTERNAL, "device allocation failed (tables)");
     CU(cudaMemcpyAsync(P->d_maps.p, P->desc.data(), K * sizeof(MapDesc), cudaMemcpyHostToDevice, P->stream));
     CU(cudaMemsetAsync(P->d_tmpi.p, 0, (K + 1) * sizeof(int32_t), P->stream));
@@ -310,9 +422,11 @@ static int create_from_cols(int32_t n, int32_t m, int32_t K, const uint32_t* col
     *out = nullptr;
     if (n < 1 || m < n || m > WPM_MAX_M) return fail(WPM_EINVAL, "unsupported (m, n): need 1 <= n <= m <= 16");
     if (K < 1) return fail(WPM_EINVAL, "no characteristic maps");
+    Trace tr;
     auto* P = new wpm_plan();
     int rc = plan_init(P, device);
     if (rc) { delete P; return rc; }
+    tr.mark("plan init (stream, events)");
     P->n = n;
     P->m = m;
     P->num_maps = K;
@@ -341,6 +455,7 @@ static int create_from_cols(int32_t n, int32_t m, int32_t K, const uint32_t* col
             delete P;
             return fail(WPM_EINVAL, "matrix is rank deficient");
         }
+    tr.mark("kernel 1 + sync");
     P->cap.resize(K);
     std::vector<uint32_t> foff(K);
     for (int i = 0; i < K; ++i) {
@@ -348,6 +463,7 @@ static int create_from_cols(int32_t n, int32_t m, int32_t K, const uint32_t* col
         foff[i] = (uint32_t)((size_t)i * stride);
     }
     rc = plan_build_tables(P, foff);
+    tr.mark("kernel 2 + sync");
     if (rc) { delete P; return rc; }
     *out = P;
     return WPM_OK;
@@ -360,14 +476,17 @@ extern "C" int wpm_plan_create_charmaps(int32_t n, int32_t m, int32_t num_maps, 
 
 extern "C" int wpm_plan_create_orbits(int32_t n, int32_t p, int64_t facet_cap, int32_t device, wpm_plan_t** out) {
     *out = nullptr;
-    const int32_t K = wpm_idcm_orbits(n, p, nullptr, 0);
-    if (K < 0) return -K;
+    Trace tr;
     const int m = n + p;
-    std::vector<uint32_t> rows((size_t)K * m), cols((size_t)K * m);
-    wpm_idcm_orbits(n, p, rows.data(), K);
+    std::vector<uint32_t> rows((size_t)4096 * m);
+    const int32_t K = wpm_idcm_orbits(n, p, rows.data(), 4096);
+    if (K < 0) return -K;
+    if (K > 4096) return fail(WPM_EINVAL, "too many orbits");
+    std::vector<uint32_t> cols((size_t)K * m);
     for (int i = 0; i < K; ++i)
         if (wpm_charmap_of_dcm(m, p, rows.data() + (size_t)i * m, cols.data() + (size_t)i * m) < 0)
             return WPM_EINVAL;
+    tr.mark("orbits + charmaps (host)");
     return create_from_cols(n, m, K, cols.data(), facet_cap, device, out);
 }
 
@@ -454,7 +573,8 @@ extern "C" int32_t wpm_plan_incidence(wpm_plan_t* P, int32_t map, uint64_t* ridg
     const int M = d.M, N = d.N, n = d.n;
     if (ridges_cap < N) return N;
     std::vector<uint32_t> r(N);
-    std::vector<uint16_t> fr((size_t)M * FR), rp((size_t)N * RP);
+    const int RS = d.rp_stride;
+    std::vector<uint16_t> fr((size_t)M * n), rp((size_t)N * RS);
     if (cudaMemcpy(r.data(), P->d_ridges.p + d.ridge_off, N * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
         cudaMemcpy(fr.data(), P->d_fr.p + d.fr_off, fr.size() * 2, cudaMemcpyDeviceToHost) != cudaSuccess ||
         cudaMemcpy(rp.data(), P->d_rp.p + d.rp_off, rp.size() * 2, cudaMemcpyDeviceToHost) != cudaSuccess)
@@ -462,12 +582,12 @@ extern "C" int32_t wpm_plan_incidence(wpm_plan_t* P, int32_t map, uint64_t* ridg
     for (int i = 0; i < N; ++i) ridges_out[i] = r[i];
     if (cols_out)
         for (int j = 0; j < M; ++j)
-            for (int k = 0; k < n; ++k) cols_out[j * n + k] = fr[(size_t)j * FR + k];
+            for (int k = 0; k < n; ++k) cols_out[j * n + k] = fr[(size_t)j * n + k];
     if (par_out)
         for (int i = 0; i < N; ++i)
-            for (int q = 0; q < RP; ++q) {
-                const uint16_t g = rp[(size_t)i * RP + q];
-                par_out[i * RP + q] = g == NONE16 ? -1 : (int32_t)g;
+            for (int q = 0; q < WPM_MAX_PARENTS; ++q) {
+                const uint16_t g = q < RS ? rp[(size_t)i * RS + q] : NONE16;
+                par_out[i * WPM_MAX_PARENTS + q] = g == NONE16 ? -1 : (int32_t)g;
             }
     return N;
 }
@@ -482,11 +602,11 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         tf.push_back(0);
         tk.push_back(3);
     } else {
-        int maxM = 0;
-        for (int i = 0; i < K; ++i) maxM = std::max(maxM, P->M[i]);
-        for (int f = 0; f < maxM; ++f)
-            for (int i = 0; i < K; ++i)
-                if (f < P->M[i] && P->n + 1 <= P->cap[i]) {
+        // map-major: at any moment the warps of an SM share few maps, so the
+        // per-map tables stay L1 resident; donations balance the load
+        for (int i = 0; i < K; ++i)
+            for (int f = 0; f < P->M[i]; ++f)
+                if (P->n + 1 <= P->cap[i]) {
                     tm.push_back(i);
                     tf.push_back(f);
                     tk.push_back(0);
@@ -519,7 +639,14 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         CU(cudaMemcpyAsync(P->d_pin_in.p, P->pin_in.data(), P->mw * 4, cudaMemcpyHostToDevice, P->stream));
         CU(cudaMemcpyAsync(P->d_pin_out.p, P->pin_out.data(), P->mw * 4, cudaMemcpyHostToDevice, P->stream));
     }
-    if (P->out_cap == 0) P->out_cap = 1ull << 20;
+    if (P->out_cap == 0) {
+        // first run: size the row buffer from free memory (a rerun is only
+        // needed if the WPM count exceeds it; the count is then known)
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const unsigned long long row = (unsigned long long)P->w32 * 4 + 2;
+        P->out_cap = std::min<unsigned long long>(std::max<unsigned long long>(fr / 16 / row, 1ull << 20), 1ull << 26);
+    }
     CU(cudaEventRecord(P->ev[4], P->stream));
     for (int attempt = 0; attempt < 2; ++attempt) {
         if (P->d_out_bits.ensure(P->out_cap * P->w32) || P->d_out_map.ensure(P->out_cap))
@@ -620,6 +747,7 @@ extern "C" int wpm_plan_run(wpm_plan_t* P, int32_t shard_index, int32_t shard_co
     if (shard_count < 1) shard_count = 1;
     if (shard_index < 0 || shard_index >= shard_count) return fail(WPM_EINVAL, "bad shard index");
     CU(cudaSetDevice(P->device));
+    g_alloc_stream = P->stream;
     const int rc = plan_search(P, shard_index, shard_count);
     if (rc) return rc;
     if (total_out) *total_out = P->total;
@@ -657,7 +785,9 @@ extern "C" int wpm_canonical_sort_device(int32_t device, const uint32_t* bits32,
                                          int64_t count, int32_t words32, uint32_t* out_bits32, uint16_t* out_map,
                                          int64_t* dups, void* stream) {
     CU(cudaSetDevice(device));
+    init_pool(device);
     cudaStream_t st = (cudaStream_t)stream;
+    g_alloc_stream = st;
     if (count <= 0) {
         if (dups) *dups = 0;
         return WPM_OK;
@@ -701,7 +831,18 @@ extern "C" int wpm_plan_fetch(wpm_plan_t* P, wpm_result_t** out) {
         R->counts[i] = (int64_t)P->per_map[i];
         R->offsets[i + 1] = R->offsets[i] + R->counts[i];
     }
-    R->bits = new uint64_t[(size_t)std::max<long long>(P->total, 1) * R->words];
+    size_t got = 0;
+    R->bits = static_cast<uint64_t*>(g_pinned.get((size_t)std::max<long long>(P->total, 1) * R->words * 8, &got));
+    if (!R->bits) {
+        delete[] R->counts;
+        delete[] R->offsets;
+        delete R;
+        return fail(WPM_EINTERNAL, "pinned host allocation failed");
+    }
+    {
+        std::lock_guard<std::mutex> lk(g_block_mu);
+        g_block_size[R->bits] = got;
+    }
     if (P->total > 0) {
         const cudaError_t e = cudaMemcpyAsync(R->bits, P->d_sorted_bits.p, (size_t)P->total * P->w32 * 4,
                                               cudaMemcpyDeviceToHost, P->stream);
@@ -726,19 +867,33 @@ extern "C" int wpm_plan_fetch(wpm_plan_t* P, wpm_result_t** out) {
 extern "C" void wpm_plan_destroy(wpm_plan_t* P) {
     if (!P) return;
     cudaSetDevice(P->device);
-    if (P->stream) cudaStreamSynchronize(P->stream);
-    for (auto& e : P->ev)
-        if (e) cudaEventDestroy(e);
-    cudaStream_t s = P->stream;
-    delete P;
-    if (s) cudaStreamDestroy(s);
+    DevCtx::Bundle b;
+    b.s = P->stream;
+    for (int i = 0; i < 5; ++i) b.ev[i] = P->ev[i];
+    const int dev = P->device;
+    delete P;  // buffers go back to the pool, ordered on the stream
+    if (b.s) {
+        std::lock_guard<std::mutex> lk(g_dev[dev].mu);
+        g_dev[dev].free_bundles.push_back(b);
+    }
 }
 
 extern "C" void wpm_result_free(wpm_result_t* R) {
     if (!R) return;
     delete[] R->counts;
     delete[] R->offsets;
-    delete[] R->bits;
+    if (R->bits) {
+        size_t sz = 0;
+        {
+            std::lock_guard<std::mutex> lk(g_block_mu);
+            auto it = g_block_size.find(R->bits);
+            if (it != g_block_size.end()) {
+                sz = it->second;
+                g_block_size.erase(it);
+            }
+        }
+        if (sz) g_pinned.put(R->bits, sz);
+    }
     delete R;
 }
 
@@ -758,12 +913,17 @@ extern "C" int wpm_enumerate(const wpm_job_t* job, wpm_result_t** out) {
 
 extern "C" int wpm_enumerate_orbits(int32_t n, int32_t p, int64_t facet_cap, int32_t device, wpm_result_t** out) {
     *out = nullptr;
+    Trace tr;
     wpm_plan_t* P = nullptr;
     int rc = wpm_plan_create_orbits(n, p, facet_cap, device, &P);
+    tr.mark("create (orbits, k1, k2)");
     if (rc) return rc;
     rc = wpm_plan_run(P, 0, 1, nullptr);
+    tr.mark("run (k3 + sort)");
     if (!rc) rc = wpm_plan_fetch(P, out);
+    tr.mark("fetch (D2H)");
     wpm_plan_destroy(P);
+    tr.mark("destroy");
     return rc;
 }
 

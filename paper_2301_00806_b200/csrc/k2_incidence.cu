@@ -103,8 +103,7 @@ __global__ void __launch_bounds__(256) k2_incidence(Binom bn, const MapDesc* __r
         const uint32_t f0 = F[j] >> 1;
         int k = 0;
         for (int v = m - 1; v >= 0; --v)
-            if ((f0 >> v) & 1u) FRm[j * FR + k++] = (uint16_t)rflag[colex_rank(cb, f0 & ~(1u << v))];
-        for (; k < FR; ++k) FRm[j * FR + k] = NONE16;
+            if ((f0 >> v) & 1u) FRm[j * d.fr_stride + k++] = (uint16_t)rflag[colex_rank(cb, f0 & ~(1u << v))];
     }
     // ridge -> candidate facets (ascending)
     uint16_t* RPm = rp + d.rp_off;
@@ -118,12 +117,12 @@ __global__ void __launch_bounds__(256) k2_incidence(Binom bn, const MapDesc* __r
             if ((r0 >> v) & 1u) continue;
             const uint16_t g = fidx[colex_rank(cb, r0 | (1u << v))];
             if (g == NONE16) continue;
-            if (c < RP) RPm[ri * RP + c] = g;
+            if (c < d.rp_stride) RPm[ri * d.rp_stride + c] = g;
             ++c;
         }
-        if (c > RP) s_bad = 1;
-        NPm[ri] = (uint8_t)min(c, RP);
-        for (int q = c; q < RP; ++q) RPm[ri * RP + q] = NONE16;
+        if (c > d.rp_stride) s_bad = 1;
+        NPm[ri] = (uint8_t)min(c, d.rp_stride);
+        for (int q = c; q < d.rp_stride; ++q) RPm[ri * d.rp_stride + q] = NONE16;
     }
     __syncthreads();
     if (tid == 0) {

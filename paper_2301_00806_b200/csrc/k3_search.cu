@@ -66,7 +66,7 @@ enum TaskKind : uint32_t { T_SINGLE = 0, T_OPEN = 1, T_CLOSED = 2, T_ENTRY = 3 }
 
 // per-warp shared-memory layout, byte offsets
 struct Layout {
-    int rs, fst, dpos, open, b1, inb, trail, frames, scratch, bytes;
+    int rs, fst, open, b1, inb, late, trail, frames, scratch, bytes;
     int nw, mw;
 };
 
@@ -80,10 +80,10 @@ __host__ __device__ inline Layout make_layout(int maxM, int maxN, int maxDepth) 
     int o = 0;
     L.rs = o;      o += NP;                       // uint8 per ridge: count | undecided << 2
     L.fst = o;     o += MP;                       // uint8 per facet: U / IN / OUT
-    L.dpos = o;    o += align16(2 * MP);          // uint16 per facet: trail index + 1 of its decision
     L.open = o;    o += align16(4 * L.nw + 4);    // open ridges (count 1)
     L.b1 = o;      o += align16(4 * L.nw + 4);    // open ridges with exactly one undecided candidate
     L.inb = o;     o += align16(4 * L.mw + 4);    // IN facet bitset
+    L.late = o;    o += align16(4 * L.mw + 4);    // donation scratch: facets decided after a frame
     L.trail = o;   o += align16(2 * MP);          // uint16 per decision (bit 15: include)
     L.frames = o;  o += align16(8 * (maxDepth + 2));
     L.scratch = o; o += 64;                       // closing-ridge list
@@ -96,7 +96,7 @@ struct MapView {
     int lpf_shift;  // lanes per facet in flattened passes: 1 << lpf_shift >= n
     const uint16_t* fr;
     const uint16_t* rp;
-    const uint8_t* npar;
+    int fs, ps;     // strides of fr (= n) and rp (<= 8, 0xFFFF padded)
 };
 
 // the warp's search state: shared arrays + register scalars
@@ -104,10 +104,10 @@ struct WS {
     uint8_t* rs;
     uint32_t* rsw;
     uint8_t* fst;
-    uint16_t* dpos;
     uint32_t* open;
     uint32_t* b1;
     uint32_t* inb;
+    uint32_t* late;
     uint16_t* trail;
     uint2* frames;      // .x = ridge | pos << 16, .y = cur | cm << 16 (cm: trail length before cur)
     uint16_t* scratch;
@@ -134,7 +134,7 @@ __device__ __forceinline__ void apply_exclusions(WS& w, const MapView& mp, int l
         bool dead = false;
         if (e < hi && k < mp.n) {
             const int g = w.trail[e] & 0x7FFF;
-            const int r = __ldg(mp.fr + g * FR + k);
+            const int r = __ldg(mp.fr + g * mp.fs + k);
             const unsigned sh = (r & 3) * 8;
             const unsigned ob = (atomicSub(&w.rsw[r >> 2], 4u << sh) >> sh) & 0xFFu;
             dead = ob == (1u | (1u << 2));             // (1,1) -> (1,0)
@@ -153,7 +153,7 @@ __device__ __forceinline__ void undo_exclusions(WS& w, const MapView& mp, int lo
         bool undead = false;
         if (e < hi && k < mp.n) {
             const int g = w.trail[e] & 0x7FFF;
-            const int r = __ldg(mp.fr + g * FR + k);
+            const int r = __ldg(mp.fr + g * mp.fs + k);
             const unsigned sh = (r & 3) * 8;
             const unsigned ob = (atomicAdd(&w.rsw[r >> 2], 4u << sh) >> sh) & 0xFFu;
             undead = ob == 1u;                         // (1,0) -> (1,1)
@@ -170,11 +170,10 @@ __device__ __forceinline__ void exclude_one(WS& w, const MapView& mp, int g, int
     if (lane == 0) {
         w.fst[g] = FOUT;
         w.trail[w.tl] = (uint16_t)g;
-        w.dpos[g] = (uint16_t)(w.tl + 1);
     }
     bool dead = false;
     if (lane < mp.n) {
-        const int r = __ldg(mp.fr + g * FR + lane);
+        const int r = __ldg(mp.fr + g * mp.fs + lane);
         const unsigned sh = (r & 3) * 8;
         const unsigned ob = (atomicSub(&w.rsw[r >> 2], 4u << sh) >> sh) & 0xFFu;
         dead = ob == (1u | (1u << 2));
@@ -190,7 +189,7 @@ __device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, i
     int r = 0;
     unsigned b = 4;
     if (act) {
-        r = __ldg(mp.fr + f * FR + lane);
+        r = __ldg(mp.fr + f * mp.fs + lane);
         b = w.rs[r];
     }
     const unsigned c = b & 3u, a = b >> 2;   // c in {0,1}, a >= 1 (f is undecided)
@@ -210,7 +209,6 @@ __device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, i
         w.fst[f] = FIN;
         w.inb[f >> 5] |= 1u << (f & 31);
         w.trail[w.tl] = (uint16_t)(f | TR_INC);
-        w.dpos[f] = (uint16_t)(w.tl + 1);
     }
     w.tl += 1;
     w.size += 1;
@@ -227,9 +225,9 @@ __device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, i
         int g = 0;
         if (j < ncl) {
             const int rr = w.scratch[j];
-            if (q < (int)__ldg(mp.npar + rr)) {
-                g = __ldg(mp.rp + rr * RP + q);
-                v = w.fst[g] == FU;
+            if (q < mp.ps) {
+                g = __ldg(mp.rp + rr * mp.ps + q);
+                v = g != NONE16 && w.fst[g] == FU;
             }
         }
         const unsigned bv = __ballot_sync(FULL, v);
@@ -237,7 +235,6 @@ __device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, i
             const int pos = base + E + __popc(bv & lanemask_lt(lane));
             w.trail[pos] = (uint16_t)g;
             w.fst[g] = FOUT;
-            w.dpos[g] = (uint16_t)(pos + 1);
         }
         E += __popc(bv);
     }
@@ -254,7 +251,7 @@ __device__ __forceinline__ void undo_include(WS& w, const MapView& mp, int f, in
     int r = 0;
     unsigned b = 0;
     if (act) {
-        r = __ldg(mp.fr + f * FR + lane);
+        r = __ldg(mp.fr + f * mp.fs + lane);
         b = w.rs[r];
     }
     const unsigned c = b & 3u, a = b >> 2;   // c in {1,2}
@@ -323,9 +320,9 @@ __device__ __forceinline__ int first_candidate(const WS& w, const MapView& mp, i
                                                int lane) {
     int g = 0;
     bool ok = false;
-    if (lane < RP && lane >= pos && lane < (int)__ldg(mp.npar + ridge)) {
-        g = __ldg(mp.rp + ridge * RP + lane);
-        ok = w.fst[g] == FU;
+    if (lane >= pos && lane < mp.ps) {
+        g = __ldg(mp.rp + ridge * mp.ps + lane);
+        ok = g != NONE16 && w.fst[g] == FU;
     }
     const unsigned b = __ballot_sync(FULL, ok);
     if (!b) return -1;
@@ -384,7 +381,8 @@ __device__ __forceinline__ bool descend(WS& w, const MapView& mp, const SearchPa
             if (w.size + mp.n + 1 > mp.cap) return false;
             ridge = CLOSED_FRAME;
         } else {
-            if (w.size + (w.nopen + mp.n - 1) / mp.n > mp.cap) return false;
+            // |S| + ceil(open / n) > cap  <=>  open > (cap - |S|) * n
+            if ((long long)(mp.cap - w.size) * mp.n < (long long)w.nopen) return false;
             const unsigned sel = select_ridge(w, mp.nw, lane);
             ridge = sel & 0xFFFFu;
             if ((sel >> 16) == 1u) {  // forced: the only undecided candidate
@@ -419,7 +417,6 @@ __device__ __forceinline__ bool load_state(WS& w, const MapView& mp, const uint3
         const uint32_t bit = 1u << lane;
         if (f < M) {
             w.fst[f] = (iv & bit) ? FIN : ((ov & bit) ? FOUT : FU);
-            w.dpos[f] = 0;
         }
     }
     w.size = (int)__reduce_add_sync(FULL, (unsigned)size);
@@ -427,9 +424,11 @@ __device__ __forceinline__ bool load_state(WS& w, const MapView& mp, const uint3
     // pass 1: IN counts; a count >= 3 is infeasible
     bool bad = false;
     for (int r = lane; r < N; r += 32) {
-        const int np = __ldg(mp.npar + r);
         unsigned c = 0;
-        for (int q = 0; q < np; ++q) c += w.fst[__ldg(mp.rp + r * RP + q)] == FIN;
+        for (int q = 0; q < mp.ps; ++q) {
+            const int g = __ldg(mp.rp + r * mp.ps + q);
+            c += g != NONE16 && w.fst[g] == FIN;
+        }
         bad |= c > 2u;
         w.rs[r] = (uint8_t)min(c, 2u);
     }
@@ -439,7 +438,7 @@ __device__ __forceinline__ bool load_state(WS& w, const MapView& mp, const uint3
     for (int f = lane; f < M; f += 32) {
         if (w.fst[f] != FU) continue;
         bool on_closed = false;
-        for (int k = 0; k < mp.n; ++k) on_closed |= w.rs[__ldg(mp.fr + f * FR + k)] == 2u;
+        for (int k = 0; k < mp.n; ++k) on_closed |= w.rs[__ldg(mp.fr + f * mp.fs + k)] == 2u;
         if (on_closed) w.fst[f] = FOUT;
     }
     __syncwarp();
@@ -449,9 +448,11 @@ __device__ __forceinline__ bool load_state(WS& w, const MapView& mp, const uint3
         const int r = r0 + lane;
         bool op = false, dd = false, one = false;
         if (r < N) {
-            const int np = __ldg(mp.npar + r);
             unsigned a = 0;
-            for (int q = 0; q < np; ++q) a += w.fst[__ldg(mp.rp + r * RP + q)] == FU;
+            for (int q = 0; q < mp.ps; ++q) {
+                const int g = __ldg(mp.rp + r * mp.ps + q);
+                a += g != NONE16 && w.fst[g] == FU;
+            }
             const unsigned c = w.rs[r];
             w.rs[r] = (uint8_t)(c | (a << 2));
             op = c == 1u;
@@ -474,7 +475,9 @@ __device__ __forceinline__ bool load_state(WS& w, const MapView& mp, const uint3
     return true;
 }
 
-// donate the shallowest frame that still has an untried child
+// donate the shallowest frame that still has an untried child.  The
+// frame's state = the current state minus every decision on the trail at or
+// after mk (`late`), with its in-progress child excluded.
 __device__ __forceinline__ void try_donate(WS& w, const MapView& mp, const SearchParams& p, int lane) {
     const int M = mp.M, mw = (M + 31) >> 5;
     for (int d = 0; d < w.depth; ++d) {
@@ -484,17 +487,25 @@ __device__ __forceinline__ void try_donate(WS& w, const MapView& mp, const Searc
         const bool busy = (fr.y & 0xFFFFu) != NO_CHILD && d + 1 < w.depth;
         const int mk = busy ? (int)(fr.y >> 16) : w.tl;  // the frame's own state
         const int cur = busy ? (int)(fr.y & 0xFFFFu) : -1;
+        for (int i = lane; i < mw; i += 32) w.late[i] = 0u;
+        __syncwarp();
+        for (int e = mk + lane; e < w.tl; e += 32) {
+            const int g = w.trail[e] & 0x7FFF;
+            atomicOr(&w.late[g >> 5], 1u << (g & 31));
+        }
+        __syncwarp();
         bool any = false;
         if (ridge == CLOSED_FRAME) {
             for (int f0 = (int)pos; f0 < M && !any; f0 += 32) {
                 const int f = f0 + lane;
-                any = __any_sync(FULL, f < M && f != cur && (w.fst[f] == FU || (int)w.dpos[f] > mk));
+                any = __any_sync(FULL, f < M && f != cur &&
+                                           (w.fst[f] == FU || ((w.late[f >> 5] >> (f & 31)) & 1u)));
             }
         } else {
             bool ok = false;
-            if (lane < RP && lane >= (int)pos && lane < (int)__ldg(mp.npar + ridge)) {
-                const int g = __ldg(mp.rp + ridge * RP + lane);
-                ok = g != cur && (w.fst[g] == FU || (int)w.dpos[g] > mk);
+            if (lane >= (int)pos && lane < mp.ps) {
+                const int g = __ldg(mp.rp + ridge * mp.ps + lane);
+                ok = g != NONE16 && g != cur && (w.fst[g] == FU || ((w.late[g >> 5] >> (g & 31)) & 1u));
             }
             any = __any_sync(FULL, ok);
         }
@@ -518,7 +529,7 @@ __device__ __forceinline__ void try_donate(WS& w, const MapView& mp, const Searc
             bool in = false, out = false;
             if (f < M) {
                 const uint8_t s = w.fst[f];
-                const bool before = (int)w.dpos[f] <= mk;
+                const bool before = !((w.late[f >> 5] >> (f & 31)) & 1u);
                 in = s == FIN && before;
                 out = (s == FOUT && before) || f == cur;
             }
@@ -548,7 +559,7 @@ __global__ void __launch_bounds__(128) k3_search(const __grid_constant__ SearchP
     w.rs = base + L.rs;
     w.rsw = reinterpret_cast<uint32_t*>(base + L.rs);
     w.fst = base + L.fst;
-    w.dpos = reinterpret_cast<uint16_t*>(base + L.dpos);
+    w.late = reinterpret_cast<uint32_t*>(base + L.late);
     w.open = reinterpret_cast<uint32_t*>(base + L.open);
     w.b1 = reinterpret_cast<uint32_t*>(base + L.b1);
     w.inb = reinterpret_cast<uint32_t*>(base + L.inb);
@@ -602,7 +613,8 @@ __global__ void __launch_bounds__(128) k3_search(const __grid_constant__ SearchP
         mp.lpf_shift = md.n <= 4 ? 2 : (md.n <= 8 ? 3 : 4);
         mp.fr = p.fr + md.fr_off;
         mp.rp = p.rp + md.rp_off;
-        mp.npar = p.npar + md.np_off;
+        mp.fs = md.fr_stride;
+        mp.ps = md.rp_stride;
         ++tasks;
 
         if (load_state(w, mp, rec + 4, rec + 4 + p.mw, lane)) {

@@ -24,10 +24,12 @@ constexpr uint16_t NONE16 = 0xFFFF;
 struct MapDesc {
     int32_t M, N, n, m;
     int32_t cap;        // facet cap (INT32_MAX = none)
+    int32_t fr_stride;  // = n
+    int32_t rp_stride;  // = min(8, m - n + 1); 0xFFFF padded
     int32_t pad0;
     uint32_t facet_off; // into facets (uint32)
     uint32_t ridge_off; // into ridges (uint32)
-    uint32_t fr_off;    // into fr (uint16), = map_slot * MAXF * FR
+    uint32_t fr_off;    // into fr (uint16)
     uint32_t rp_off;    // into rp (uint16)
     uint32_t np_off;    // into npar (uint8)
     uint32_t pad1;

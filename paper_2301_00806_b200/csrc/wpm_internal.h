@@ -24,7 +24,7 @@ struct SearchParams {
     const MapDesc* maps;
     const uint16_t* fr;
     const uint16_t* rp;
-    const uint8_t* npar;
+    const uint8_t* npar;  // host-side parity hook only
     // work queue
     uint32_t* qrec;
     unsigned long long* qready;
