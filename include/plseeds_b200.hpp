@@ -1,0 +1,366 @@
+// plseeds_b200.hpp -- header-only C++ drop-in for the reference's enumeration
+// path, over the C-ABI of libwpm_b200.so (include/wpm_b200.h).
+//
+// Two ways to use it:
+//
+// 1. Standalone, namespace plseeds_b200: the same names, argument meaning and
+//    error types as the reference (/root/reference/proj/include/plseeds):
+//      VertexSet            vertex_set.hpp:20-68
+//      PureComplex          complex.hpp:23-104
+//      DualCharMatrix       charmap.hpp:64-87      CharMatrixZ2  charmap.hpp:20-26
+//      idcm_orbits          charmap.hpp:212-281    charmap_of_dcm charmap.hpp:155-204
+//      binary_matroid       charmap.hpp:117-141 (kernel 1 on the GPU)
+//      matroid_universe     pipeline.hpp:33-35
+//      AffineProperty, ubt_property, cyclic_facet_bound   affine_property.hpp:16-54
+//      SearchJob            search.hpp:46-55 (+ required/forbidden pins, device)
+//      enumerate_wpm        search.hpp:141-258 (kernels 2-3 + canonical sort)
+//      enumerate_orbits     the per-orbit loop of pipeline.hpp:383-397, one launch
+//      write_complex(es)    complex_io.hpp:21-39
+//      purity_error, cap_exceeded_error, format_error   errors.hpp:10-32
+//
+// 2. Inside a program that already includes the reference headers
+//    (plseeds/search.hpp first): plseeds::b200::enumerate_wpm(const
+//    plseeds::SearchJob&) takes the reference's own job type -- universe,
+//    properties, the (possibly link-pinned) KernelBasis and candidate_cap --
+//    and returns the reference's std::vector<plseeds::PureComplex>, identical
+//    to plseeds::enumerate_wpm(job).
+#ifndef PLSEEDS_B200_HPP
+#define PLSEEDS_B200_HPP
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <functional>
+#include <initializer_list>
+#include <ostream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "wpm_b200.h"
+
+namespace plseeds_b200 {
+
+struct purity_error : std::runtime_error {
+    explicit purity_error(const std::string& w) : std::runtime_error(w) {}
+};
+struct format_error : std::runtime_error {
+    explicit format_error(const std::string& w) : std::runtime_error(w) {}
+};
+struct cap_exceeded_error : std::runtime_error {
+    explicit cap_exceeded_error(const std::string& w) : std::runtime_error(w) {}
+};
+// status 1: CUDA / no device (there is no CPU fallback)
+struct device_error : std::runtime_error {
+    explicit device_error(const std::string& w) : std::runtime_error(w) {}
+};
+
+inline void check(int rc) {
+    if (rc == WPM_OK) return;
+    const std::string msg = wpm_last_error();
+    if (rc == WPM_ECAP) throw cap_exceeded_error(msg);
+    if (rc == WPM_EINVAL) {
+        if (msg.find("purity") != std::string::npos || msg.find("empty facet set") != std::string::npos)
+            throw purity_error(msg);
+        throw std::invalid_argument(msg);
+    }
+    if (rc == WPM_EINFEASIBLE) throw std::invalid_argument(msg);
+    throw device_error(msg);
+}
+
+struct VertexSet {
+    std::uint64_t bits = 0;
+    constexpr VertexSet() = default;
+    constexpr explicit VertexSet(std::uint64_t raw) : bits(raw) {}
+    VertexSet(std::initializer_list<int> labels) {
+        for (int v : labels) bits |= std::uint64_t{1} << v;
+    }
+    constexpr bool contains(int v) const { return (bits >> v) & 1u; }
+    int count() const { return __builtin_popcountll(bits); }
+    bool operator==(const VertexSet& o) const { return bits == o.bits; }
+    bool operator!=(const VertexSet& o) const { return bits != o.bits; }
+    bool operator<(const VertexSet& o) const { return bits < o.bits; }  // canonical order
+};
+
+struct PureComplex {
+    int m = 0;
+    int n = 0;
+    std::vector<VertexSet> facets;  // canonical (ascending) order
+    bool embedded = false;
+    bool operator==(const PureComplex& o) const { return m == o.m && n == o.n && facets == o.facets; }
+    int facet_count() const { return static_cast<int>(facets.size()); }
+};
+
+struct DualCharMatrix {
+    int m = 0;
+    int p = 0;
+    std::vector<std::uint32_t> rows;
+};
+
+struct CharMatrixZ2 {
+    int n = 0;
+    int m = 0;
+    std::vector<std::uint32_t> cols;
+};
+
+struct AffineProperty {
+    std::vector<std::int64_t> weights;
+    std::int64_t constant = 0;
+    bool is_count_cap() const {
+        for (auto w : weights)
+            if (w != -1) return false;
+        return true;
+    }
+};
+
+inline std::int64_t cyclic_facet_bound(int n) { return wpm_cyclic_facet_bound(n); }
+
+inline AffineProperty ubt_property(int n, int universe_size) {
+    AffineProperty g;
+    g.weights.assign(static_cast<std::size_t>(universe_size), -1);
+    g.constant = cyclic_facet_bound(n) + 1;
+    return g;
+}
+
+struct SearchJob {
+    int m = 0;
+    int n = 0;
+    std::vector<VertexSet> facets;  // the universe, canonical order
+    std::vector<AffineProperty> properties;
+    std::vector<int> required;      // link pins (apply_link_constraints semantics)
+    std::vector<int> forbidden;
+    int threads = 1;                // accepted; the device search has its own parallelism
+    std::uint64_t candidate_cap = std::uint64_t{1} << 48;  // no combination space on the device
+    std::function<void(long long, long long)> progress;
+    int device = 0;
+};
+
+inline std::vector<DualCharMatrix> idcm_orbits(int n, int p) {
+    const int m = n + p;
+    std::vector<std::uint32_t> rows(static_cast<std::size_t>(4096) * m);
+    const int k = wpm_idcm_orbits(n, p, rows.data(), 4096);
+    if (k < 0) check(-k);
+    std::vector<DualCharMatrix> out(static_cast<std::size_t>(k));
+    for (int i = 0; i < k; ++i) {
+        out[i].m = m;
+        out[i].p = p;
+        out[i].rows.assign(rows.begin() + static_cast<long>(i) * m, rows.begin() + static_cast<long>(i + 1) * m);
+    }
+    return out;
+}
+
+inline CharMatrixZ2 charmap_of_dcm(const DualCharMatrix& d) {
+    CharMatrixZ2 lam;
+    lam.m = d.m;
+    lam.cols.assign(static_cast<std::size_t>(d.m), 0);
+    const int n = wpm_charmap_of_dcm(d.m, d.p, d.rows.data(), lam.cols.data());
+    if (n < 0) check(-n);
+    lam.n = n;
+    return lam;
+}
+
+namespace detail {
+struct Plan {
+    wpm_plan_t* p = nullptr;
+    ~Plan() { wpm_plan_destroy(p); }
+};
+struct Result {
+    wpm_result_t* r = nullptr;
+    ~Result() { wpm_result_free(r); }
+};
+
+inline std::vector<VertexSet> universe_of(wpm_plan_t* p, int map) {
+    std::vector<std::uint64_t> f(WPM_MAX_FACETS);
+    const int M = wpm_plan_universe(p, map, f.data(), WPM_MAX_FACETS);
+    if (M < 0) check(-M);
+    std::vector<VertexSet> out;
+    out.reserve(static_cast<std::size_t>(M));
+    for (int j = 0; j < M; ++j) out.emplace_back(f[static_cast<std::size_t>(j)]);
+    return out;
+}
+
+inline std::vector<PureComplex> complexes_of(const wpm_result_t* r, int map, int m, int n,
+                                             const std::vector<VertexSet>& u) {
+    std::vector<PureComplex> out;
+    out.reserve(static_cast<std::size_t>(r->counts[map]));
+    for (std::int64_t i = r->offsets[map]; i < r->offsets[map + 1]; ++i) {
+        PureComplex K;
+        K.m = m;
+        K.n = n;
+        K.embedded = true;
+        const std::uint64_t* row = r->bits + static_cast<std::size_t>(i) * r->words;
+        for (int w = 0; w < r->words; ++w)
+            for (std::uint64_t x = row[w]; x; x &= x - 1) K.facets.push_back(u[static_cast<std::size_t>(w * 64 + __builtin_ctzll(x))]);
+        out.push_back(std::move(K));
+    }
+    return out;
+}
+
+inline std::int64_t facet_cap_of(const std::vector<AffineProperty>& props) {
+    std::int64_t cap = WPM_CAP_NONE;
+    for (const auto& g : props) {
+        if (!g.is_count_cap())
+            throw std::invalid_argument("general affine properties are not supported by the B200 path (count caps only)");
+        const std::int64_t c = g.constant - 1;
+        cap = cap < 0 ? c : std::min(cap, c);
+    }
+    return cap;
+}
+}  // namespace detail
+
+// binary_matroid (charmap.hpp:117-141): kernel 1 on device 0
+inline PureComplex binary_matroid(const CharMatrixZ2& lam, int device = 0) {
+    detail::Plan P;
+    check(wpm_plan_create_charmaps(lam.n, lam.m, 1, lam.cols.data(), WPM_CAP_UBT, device, &P.p));
+    PureComplex K;
+    K.m = lam.m;
+    K.n = lam.n;
+    K.embedded = true;
+    K.facets = detail::universe_of(P.p, 0);
+    return K;
+}
+
+inline std::vector<VertexSet> matroid_universe(const DualCharMatrix& d, int device = 0) {
+    return binary_matroid(charmap_of_dcm(d), device).facets;
+}
+
+// enumerate_wpm (search.hpp:141-258)
+inline std::vector<PureComplex> enumerate_wpm(const SearchJob& job) {
+    if (job.facets.empty()) throw purity_error("incidence of an empty facet set");
+    std::vector<std::uint64_t> f;
+    f.reserve(job.facets.size());
+    for (const auto& v : job.facets) f.push_back(v.bits);
+    wpm_job_t j{};
+    j.m = job.m;
+    j.n = job.n;
+    j.num_facets = static_cast<std::int32_t>(f.size());
+    j.facets = f.data();
+    j.facet_cap = detail::facet_cap_of(job.properties);
+    j.required = job.required.data();
+    j.num_required = static_cast<std::int32_t>(job.required.size());
+    j.forbidden = job.forbidden.data();
+    j.num_forbidden = static_cast<std::int32_t>(job.forbidden.size());
+    j.device = job.device;
+    detail::Result R;
+    check(wpm_enumerate(&j, &R.r));
+    if (job.progress) job.progress(1, 1);
+    return detail::complexes_of(R.r, 0, job.m, job.n, job.facets);
+}
+
+// the Algorithm-2 per-orbit loop (pipeline.hpp:383-397) for one n in one launch:
+// element i = enumerate_wpm over matroid_universe(idcm_orbits(n, p)[i]) with the UBT cap
+inline std::vector<std::vector<PureComplex>> enumerate_orbits(int n, int p = 4, int device = 0,
+                                                              std::int64_t facet_cap = WPM_CAP_UBT) {
+    detail::Plan P;
+    check(wpm_plan_create_orbits(n, p, facet_cap, device, &P.p));
+    std::int64_t total = 0;
+    check(wpm_plan_run(P.p, 0, 1, &total));
+    detail::Result R;
+    check(wpm_plan_fetch(P.p, &R.r));
+    std::vector<std::vector<PureComplex>> out;
+    for (int i = 0; i < R.r->num_maps; ++i)
+        out.push_back(detail::complexes_of(R.r, i, n + p, n, detail::universe_of(P.p, i)));
+    return out;
+}
+
+// complex_io.hpp:21-39
+inline void write_complex(std::ostream& os, const PureComplex& K) {
+    os << K.m << ' ' << K.n << '\n';
+    for (const VertexSet& f : K.facets) {
+        bool first = true;
+        for (std::uint64_t b = f.bits; b; b &= b - 1) {
+            if (!first) os << ' ';
+            os << __builtin_ctzll(b);
+            first = false;
+        }
+        os << '\n';
+    }
+}
+
+inline void write_complexes(std::ostream& os, const std::vector<PureComplex>& list) {
+    for (std::size_t i = 0; i < list.size(); ++i) {
+        if (i > 0) os << '\n';
+        write_complex(os, list[i]);
+    }
+}
+
+}  // namespace plseeds_b200
+
+// ---------------------------------------------------------------------------
+// Adapter for programs that include the reference headers first.
+#ifdef PLSEEDS_SEARCH_HPP
+namespace plseeds {
+namespace b200 {
+
+// Drop-in for plseeds::enumerate_wpm(job).  Honours job.basis exactly: the
+// reference enumerates base + span(free generators) (search.hpp:152-153,
+// combination_space :81-104).  A facet on which every free generator vanishes
+// is fixed to its base bit; those pins go to the device search, and each
+// result is kept iff K xor base lies in the span of the free generators (a
+// no-op for bases produced by apply_link_constraints, whose solution set is
+// exactly the pinned WPMs).  The candidate cap throws cap_exceeded_error like
+// the reference (search.hpp:147-150).
+inline std::vector<PureComplex> enumerate_wpm(const SearchJob& job) {
+    const KernelBasis& kb = job.basis;
+    const std::uint64_t space = combination_space(kb).size_saturated();
+    if (space > job.candidate_cap)
+        throw cap_exceeded_error("combination space of " + std::to_string(space) + " candidates exceeds cap " +
+                                 std::to_string(job.candidate_cap));
+    const int M = static_cast<int>(job.facets.size());
+    const int first_free = kb.pinned_ones + kb.pinned_zeros;
+    BitVec base(M);
+    for (int g = 0; g < kb.pinned_ones; ++g) base ^= kb.gens[static_cast<std::size_t>(g)];
+    std::vector<int> req, forb;
+    if (first_free > 0) {
+        BitVec any_free(M);
+        for (int g = first_free; g < kb.s(); ++g)
+            for (std::size_t w = 0; w < any_free.words.size(); ++w)
+                any_free.words[w] |= kb.gens[static_cast<std::size_t>(g)].words[w];
+        for (int j = 0; j < M; ++j)
+            if (!any_free.test(j)) (base.test(j) ? req : forb).push_back(j);
+    }
+    plseeds_b200::SearchJob j;
+    j.m = job.m;
+    j.n = job.n;
+    for (const auto& f : job.facets) j.facets.emplace_back(f.bits);
+    for (const auto& g : job.properties) j.properties.push_back({g.weights, g.constant});
+    j.required = req;
+    j.forbidden = forb;
+    // echelon of the free generators for the affine-span filter
+    std::vector<BitVec> ech;
+    std::vector<int> lead;
+    for (int g = first_free; g < kb.s(); ++g) {
+        BitVec v = kb.gens[static_cast<std::size_t>(g)];
+        for (std::size_t i = 0; i < ech.size(); ++i)
+            if (v.test(lead[i])) v ^= ech[i];
+        int l = -1;
+        for (int b = 0; b < M && l < 0; ++b)
+            if (v.test(b)) l = b;
+        if (l < 0) continue;
+        for (std::size_t i = 0; i < ech.size(); ++i)
+            if (ech[i].test(l)) ech[i] ^= v;
+        ech.push_back(v);
+        lead.push_back(l);
+    }
+    std::vector<PureComplex> out;
+    for (auto& K : plseeds_b200::enumerate_wpm(j)) {
+        BitVec x = base;
+        for (const auto& f : K.facets) {
+            const auto it = std::lower_bound(job.facets.begin(), job.facets.end(), VertexSet(f.bits));
+            x.flip(static_cast<int>(it - job.facets.begin()));
+        }
+        for (std::size_t i = 0; i < ech.size(); ++i)
+            if (x.test(lead[i])) x ^= ech[i];
+        if (x.any()) continue;
+        std::vector<VertexSet> fs;
+        for (const auto& f : K.facets) fs.emplace_back(f.bits);
+        out.emplace_back(job.m, job.n, std::move(fs), /*embedded=*/true);
+    }
+    return out;
+}
+
+}  // namespace b200
+}  // namespace plseeds
+#endif
+
+#endif

@@ -173,6 +173,20 @@ static int cmp_bits(const void *a, const void *b) {
     return po_bits_cmp((const uint64_t *)a, (const uint64_t *)b, g_words);
 }
 
+static int g_shard_index = 0, g_shard_count = 1;
+
+/* dfs_enumerate restricted to the root branches f with f % count == index
+ * (the single-map case of the device root-task split, api.cu plan_search) */
+int dfs_enumerate_shard(int n, const uint64_t *facets, int M, int64_t cap, int want_bits,
+                        int shard_index, int shard_count, dfs_result *out) {
+    g_shard_index = shard_index;
+    g_shard_count = shard_count;
+    const int rc = dfs_enumerate(n, facets, M, cap, 0, 0, 0, 0, want_bits, 0, M - 1 < 0 ? 0 : M, out);
+    g_shard_index = 0;
+    g_shard_count = 1;
+    return rc;
+}
+
 int dfs_enumerate(int n, const uint64_t *facets, int M, int64_t cap, const int32_t *required,
                   int nreq, const int32_t *forbidden, int nforb, int want_bits, int root_lo,
                   int root_hi, dfs_result *out) {
@@ -209,14 +223,15 @@ int dfs_enumerate(int n, const uint64_t *facets, int M, int64_t cap, const int32
     }
     if (ok && c.ndead) ok = 0;
     if (ok) {
-        if (nreq > 0 || root_lo > 0 || root_hi < M) {
+        if (nreq > 0 || root_lo > 0 || root_hi < M || g_shard_count > 1) {
             if (nreq > 0) {
                 search(&c);
             } else {
                 /* root branches [root_lo, root_hi): minimum facet f */
                 for (int f = 0; f < root_hi; ++f) {
                     if (c.st[f] != ST_U) continue;
-                    if (f >= root_lo && (cap < 0 || n + 1 <= cap)) child(&c, f);
+                    if (f >= root_lo && f % g_shard_count == g_shard_index && (cap < 0 || n + 1 <= cap))
+                        child(&c, f);
                     do_exclude(&c, f);
                 }
             }

@@ -34,6 +34,8 @@ typedef struct {
 int dfs_enumerate(int n, const uint64_t *facets, int M, int64_t cap, const int32_t *required,
                   int nreq, const int32_t *forbidden, int nforb, int want_bits, int root_lo,
                   int root_hi, dfs_result *out);
+int dfs_enumerate_shard(int n, const uint64_t *facets, int M, int64_t cap, int want_bits,
+                        int shard_index, int shard_count, dfs_result *out);
 void dfs_result_free(dfs_result *r);
 
 #ifdef __cplusplus

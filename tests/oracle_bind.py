@@ -71,6 +71,8 @@ class Oracle:
                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     ctypes.POINTER(_DfsResult)]
         L.dfs_result_free.argtypes = [ctypes.POINTER(_DfsResult)]
+        L.dfs_enumerate_shard.argtypes = [ctypes.c_int, _u64p, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
+                                          ctypes.c_int, ctypes.c_int, ctypes.POINTER(_DfsResult)]
 
     # -- characteristic maps
     def idcm_orbits(self, n: int, p: int = 4) -> List[List[int]]:
@@ -158,6 +160,20 @@ class Oracle:
             raise ValueError("bad universe")
         cnt, w = res.count, res.words
         bits = (np.ctypeslib.as_array(res.bits, shape=(cnt * w,)).copy().reshape(cnt, w) if cnt and want_bits
+                else np.zeros((0, w), dtype=np.uint64))
+        nodes = res.nodes
+        self.lib.dfs_result_free(ctypes.byref(res))
+        return cnt, nodes, bits
+
+    def dfs_shard(self, n: int, facets: Sequence[int], cap: int, shard_index: int, shard_count: int):
+        f = _arr(facets, np.uint64)
+        res = _DfsResult()
+        rc = self.lib.dfs_enumerate_shard(n, f.ctypes.data_as(_u64p), len(facets), cap, 1, shard_index, shard_count,
+                                          ctypes.byref(res))
+        if rc != 0:
+            raise ValueError("bad universe")
+        cnt, w = res.count, res.words
+        bits = (np.ctypeslib.as_array(res.bits, shape=(cnt * w,)).copy().reshape(cnt, w) if cnt
                 else np.zeros((0, w), dtype=np.uint64))
         nodes = res.nodes
         self.lib.dfs_result_free(ctypes.byref(res))

@@ -1,0 +1,111 @@
+"""CPU tests of the drop-in boundary: the C-ABI library loads, exports every
+symbol include/wpm_b200.h declares, the C++ drop-in header compiles and
+links against it, and compute entry points fail loudly without a GPU (no
+CPU fallback)."""
+import ctypes
+import os
+import re
+import shutil
+import subprocess
+import tempfile
+
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "wpm_b200.h")
+LIB = os.path.join(ROOT, "paper_2301_00806_b200", "libwpm_b200.so")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b(wpm_\w+)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("wpm_enumerate", "wpm_result_free", "wpm_device_count", "wpm_last_error", "wpm_plan_run",
+                 "wpm_idcm_orbits", "wpm_write_cplx"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(LIB)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    nm = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True).stdout
+    for n in declared_functions():
+        assert re.search(rf"\bT {n}$", nm, flags=re.M), n
+
+
+def test_python_mirror_binds_every_symbol(wpm):
+    assert set(wpm.EXPORTED_SYMBOLS) == set(declared_functions())
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.skipif(shutil.which("g++") is None, reason="no g++")
+def test_cpp_dropin_compiles_and_links():
+    """include/plseeds_b200.hpp: the reference-named C++ API over the C-ABI."""
+    src = r'''
+#include "plseeds_b200.hpp"
+#include <sstream>
+int main() {
+    using namespace plseeds_b200;
+    auto orbits = idcm_orbits(5, 4);
+    SearchJob job;
+    job.m = 9; job.n = 5;
+    job.facets = matroid_universe(orbits.at(0));
+    job.properties = {ubt_property(5, (int)job.facets.size())};
+    std::ostringstream os;
+    if (std::getenv("WPM_RUN")) write_complexes(os, enumerate_wpm(job));
+    return orbits.size() == 35 ? 0 : 1;
+}
+'''
+    with tempfile.TemporaryDirectory() as td:
+        p = os.path.join(td, "t.cpp")
+        open(p, "w").write(src)
+        exe = os.path.join(td, "t")
+        r = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), p, "-o", exe,
+                            LIB, f"-Wl,-rpath,{os.path.dirname(LIB)}"], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        # host-only path runs without a GPU (idcm_orbits is host C++); matroid_universe needs the device
+        env = dict(os.environ)
+        r = subprocess.run([exe], capture_output=True, text=True, env=env)
+        if not _has_gpu():
+            assert r.returncode != 0 and "no CUDA device" in (r.stderr + r.stdout)
+
+
+def _has_gpu():
+    import paper_2301_00806_b200 as w
+
+    return w.device_count() > 0
+
+
+def test_no_cpu_fallback(wpm, oracle):
+    """Without a B200 every compute call raises instead of computing on the CPU."""
+    if _has_gpu():
+        pytest.skip("GPU present")
+    u = oracle.all_subsets_universe(4, 2)
+    with pytest.raises(wpm.WpmError, match="no CPU fallback"):
+        wpm.enumerate_wpm(wpm.SearchJob(4, 2, u))
+    with pytest.raises(wpm.WpmError):
+        wpm.enumerate_orbits(2)
+    with pytest.raises(wpm.WpmError):
+        wpm.Plan.orbits(2)
+
+
+def test_job_validation_errors(wpm):
+    """PureComplex::validate / incidence_matrix error behaviour (complex.hpp:37-55,
+    incidence.hpp:35) is checked on the host before any device work."""
+    with pytest.raises(wpm.PurityError):
+        wpm.enumerate_wpm(wpm.SearchJob(4, 2, []))
+    with pytest.raises(ValueError):
+        wpm.enumerate_wpm(wpm.SearchJob(4, 2, [0b1100, 0b0110]))  # not canonical order
+    with pytest.raises(ValueError):
+        wpm.enumerate_wpm(wpm.SearchJob(4, 2, [0b0110], properties=[wpm.AffineProperty([2], 3)]))
