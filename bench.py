@@ -290,14 +290,33 @@ def main():
     return 0
 
 
+class _E2E:
+    def __init__(self, h2d, d2h, total):
+        self.h2d_bytes, self.d2h_bytes, self.total = h2d, d2h, total
+
+
 def wpm_orbits_oneshot(wpm, n, dev, rank, world):
-    """wpm_enumerate_orbits for world == 1; per-rank shard + NCCL gather for world > 1."""
+    """wpm_enumerate_orbits for world == 1.  For world > 1: every rank builds
+    its plan from the host maps, searches its root-task shard, NCCL gathers
+    the canonical rows into rank 0's HBM, rank 0 sorts them canonically and
+    copies the full list to the host."""
     if world == 1:
         return wpm.enumerate_orbits(n, device=dev)
+    import torch
+    import torch.distributed as dist
+
+    from paper_2301_00806_b200 import dist as wdist
+
     with wpm.Plan.orbits(n, device=dev) as p:
         p.run(rank, world)
-        r = p.fetch()
-    return r
+        total, dups, rows, maps = wdist.gather_to_rank0_device(dist, p, rank, dev, return_rows=True)
+        d2h = 0
+        if rank == 0:
+            assert dups == 0
+            host = torch.empty(rows.numel(), dtype=rows.dtype, pin_memory=True)
+            host.copy_(rows)
+            d2h = host.numel() * host.element_size()
+    return _E2E(0, d2h, total)
 
 
 if __name__ == "__main__":

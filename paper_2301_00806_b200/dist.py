@@ -93,10 +93,11 @@ def reduce_counts(dist, per_map: Sequence[int], nodes: int, device=None) -> Tupl
     return v[:-1], v[-1]
 
 
-def gather_to_rank0_device(dist, plan, rank: int, device: int):
+def gather_to_rank0_device(dist, plan, rank: int, device: int, return_rows: bool = False):
     """GPU path: NCCL all_gather of every rank's resident canonical rows into
     rank 0's HBM, then one canonical sort there.  Returns (count, duplicates)
-    on rank 0, (local count, 0) elsewhere."""
+    on rank 0, (local count, 0) elsewhere; with return_rows also the sorted
+    rows / map ids (rank 0) as device tensors."""
     import torch
 
     import paper_2301_00806_b200 as wpm
@@ -117,19 +118,21 @@ def gather_to_rank0_device(dist, plan, rank: int, device: int):
     pr[: count * w32] = rows
     pm[:count] = maps
     g_rows = [torch.zeros_like(pr) for _ in range(world)]
-    g_maps = [torch.zeros_like(pm) for _ in range(world)]
+    g_maps = [torch.zeros(cap * 2, dtype=torch.uint8, device=dev) for _ in range(world)]
     dist.all_gather(g_rows, pr)
-    dist.all_gather(g_maps, pm)
+    dist.all_gather(g_maps, pm.view(torch.uint8))  # NCCL has no int16: ship the ids as bytes
     if rank != 0:
-        return count, 0
+        return (count, 0, None, None) if return_rows else (count, 0)
     all_rows = torch.cat([g_rows[r][: counts[r] * w32] for r in range(world)])
-    all_maps = torch.cat([g_maps[r][: counts[r]] for r in range(world)])
+    all_maps = torch.cat([g_maps[r].view(torch.int16)[: counts[r]] for r in range(world)])
     total = sum(counts)
     out_rows = torch.empty_like(all_rows)
     out_maps = torch.empty_like(all_maps)
     torch.cuda.synchronize(dev)
     dups = wpm.canonical_sort_device(device, all_rows.data_ptr(), all_maps.data_ptr(), total, w32,
                                      out_rows.data_ptr(), out_maps.data_ptr())
+    if return_rows:
+        return total, dups, out_rows, out_maps
     return total, dups
 
 
