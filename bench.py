@@ -137,6 +137,34 @@ def reference_arm(args):
 
 
 METRIC = "search nodes/sec and wall time to enumerate all WPMs per Picard-4 dim n"
+# per step, from the ncu launch list of this command (profiles/r01_bench_n5_launches.txt):
+# seed_tasks + k3_search + iota_u32 + 13 CUB merge-sort kernels + gather_rows
+LAUNCHES_PER_STEP = 17
+
+
+def _profile_summary(n):
+    """traffic / instructions-per-node of kernel 3 from the committed ncu capture."""
+    out = {}
+    path = os.path.join(ROOT, "profiles", f"r01_k3_n{n}_ncu.txt")
+    if not os.path.exists(path):
+        return out
+    rd = wr = None
+    for ln in open(path):
+        t = ln.split()
+        if not t:
+            continue
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        if t[0] == "dram__bytes_read.sum":
+            rd = float(t[1]) * scale.get(t[2], 1)
+        elif t[0] == "dram__bytes_write.sum":
+            wr = float(t[1]) * scale.get(t[2], 1)
+        elif ln.startswith("warp instructions per node"):
+            out["inst_per_node"] = float(t[-1])
+        elif t[0] == "smsp__issue_active.avg.pct_of_peak_sustained_active":
+            out["issue_pct"] = float(t[1])
+    if rd is not None and wr is not None:
+        out["traffic"] = rd + wr
+    return out
 UNIT = "search nodes/s (DFS facet-inclusion steps of the workload / wall s)"
 
 
@@ -158,7 +186,7 @@ def cpu_baseline(n, nodes):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--n", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -256,10 +284,17 @@ def main():
     ops = tot_nodes / max(world, 1) * 5 * n if world > 1 else nodes * 5 * n
     ms_k3 = ms_search / args.steps
     achieved = ops / (ms_k3 * 1e-3)
+    prof = _profile_summary(n)
     roofline = {"bound": "int-issue", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
-                "frac": achieved / peak, "traffic": None,
-                "note": "5n int ops per search node (SURVEY 8d) / kernel-3 CUDA-event time; peak = measured "
-                        "LOP3+IADD chains on all SMs (wpm_int_peak)"}
+                "frac": achieved / peak, "traffic": prof.get("traffic"),
+                "note": "achieved = 5n int lane-ops per search node (SURVEY 8d) / kernel-3 CUDA-event time; peak = "
+                        "measured LOP3+IADD chains on all SMs (wpm_int_peak, live). traffic = dram read+write bytes "
+                        "of one kernel-3 launch from the committed ncu --set full capture",
+                "issue": {"warp_inst_per_node": prof.get("inst_per_node"),
+                          "issue_active_pct": prof.get("issue_pct"),
+                          "warp_inst_peak_per_s": 4 * 148 * 1.965e9,
+                          "note": "the kernel is issue-bound: one DFS per warp has O(n) lanes of work per node; "
+                                  "see profiles/r01_k3_n5_ncu.txt"}}
 
     if rank == 0:
         cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(n, expect_nodes)
@@ -277,7 +312,9 @@ def main():
             "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clocks,
-            "gpu_launches": 4,
+            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "gpu_launches_per_step": {"seed_tasks": 1, "k3_search": 1, "iota_u32": 1, "cub_merge_sort": 13,
+                                      "gather_rows": 1},
             "breakdown_ms": {"search": ms_k3, "sort": ms_sort / args.steps, "step": ms_step},
             "parity": {"wpms_expected": expect_wpms, "nodes_expected": expect_nodes,
                        "ok": tot_wpms == expect_wpms and tot_nodes == expect_nodes},
