@@ -1,0 +1,104 @@
+// tests/cpp/adapter_check.cpp -- TEST INFRASTRUCTURE.
+//
+// Runs the UNMODIFIED reference enumerate_wpm (compiled in from
+// /root/reference/proj/include at build time) and the drop-in
+// plseeds::b200::enumerate_wpm (include/plseeds_b200.hpp -> libwpm_b200.so)
+// on the same reference SearchJob and compares the outputs complex by
+// complex: every orbit map for n = 2..5 (UBT cap), full-subset universes, the
+// test_search.cpp:178-220 link-pinned octahedron basis, random pinned bases
+// from apply_link_constraints, and the candidate_cap error.  Built by
+// oracle/Makefile (target `ref`) into oracle/_ref/; run by tests/test_gpu_parity.py.
+#include <cstdio>
+#include <random>
+
+#include "plseeds/catalog.hpp"
+#include "plseeds/pipeline.hpp"
+#include "plseeds/search.hpp"
+#include "plseeds_b200.hpp"
+
+using namespace plseeds;
+
+static int failures = 0;
+
+static void check(const SearchJob& job, const char* what) {
+    const auto ref = enumerate_wpm(job);
+    const auto got = b200::enumerate_wpm(job);
+    if (!(ref == got)) {
+        std::printf("MISMATCH %s: reference %zu, b200 %zu\n", what, ref.size(), got.size());
+        ++failures;
+    }
+}
+
+static SearchJob make_job(const std::vector<VertexSet>& u, int m, int n) {
+    SearchJob job;
+    job.m = m;
+    job.n = n;
+    job.facets = u;
+    const auto A = incidence_matrix(u);
+    job.basis = convenient_basis(kernel_basis(A), A);
+    job.candidate_cap = ~0ull;
+    return job;
+}
+
+int main() {
+    int jobs = 0;
+    for (int n = 2; n <= 5; ++n)
+        for (const auto& d : idcm_orbits(n, 4)) {
+            auto job = make_job(matroid_universe(d), n + 4, n);
+            job.properties = {ubt_property(n, static_cast<int>(job.facets.size()))};
+            check(job, "orbit map");
+            ++jobs;
+        }
+    for (auto [m, n] : {std::pair{5, 2}, {6, 2}, {6, 3}, {7, 3}, {6, 4}})
+        check(make_job(all_subsets_universe(m, n), m, n), "full subsets"), ++jobs;
+    {  // octahedron link pinning, test_search.cpp:178-220
+        const auto u = all_subsets_universe(6, 3);
+        auto job = make_job(u, 6, 3);
+        const auto oct = octahedron();
+        std::vector<int> req, forb;
+        for (std::size_t j = 0; j < u.size(); ++j) {
+            if (!u[j].contains(1)) continue;
+            (std::binary_search(oct.facets.begin(), oct.facets.end(), u[j]) ? req : forb).push_back((int)j);
+        }
+        job.basis = *apply_link_constraints(job.basis, req, forb);
+        check(job, "octahedron pin");
+        ++jobs;
+    }
+    std::mt19937 rng(20240809);
+    int made = 0;
+    while (made < 20) {
+        std::vector<VertexSet> u;
+        for (VertexSet f : all_subsets_universe(6, 3))
+            if (rng() % 2 == 0) u.push_back(f);
+        if (u.size() < 10 || u.size() > 18) continue;
+        std::vector<int> req, forb;
+        for (std::size_t j = 0; j < u.size(); ++j) {
+            const auto roll = rng() % 10;
+            if (roll == 0) req.push_back((int)j);
+            else if (roll == 1) forb.push_back((int)j);
+        }
+        auto job = make_job(u, 6, 3);
+        const auto pinned = apply_link_constraints(job.basis, req, forb);
+        ++made;
+        if (!pinned) continue;
+        job.basis = *pinned;
+        check(job, "random pin");
+        ++jobs;
+    }
+    {  // candidate_cap: same exception type
+        auto job = make_job(all_subsets_universe(6, 2), 6, 2);
+        job.candidate_cap = 16;
+        bool threw = false;
+        try {
+            b200::enumerate_wpm(job);
+        } catch (const cap_exceeded_error&) {
+            threw = true;
+        }
+        if (!threw) {
+            std::printf("MISMATCH cap_exceeded_error not thrown\n");
+            ++failures;
+        }
+    }
+    std::printf("adapter_check: %d jobs, %d mismatches\n", jobs, failures);
+    return failures ? 1 : 0;
+}

@@ -81,6 +81,34 @@ int main() {
             assert r.returncode != 0 and "no CUDA device" in (r.stderr + r.stdout)
 
 
+@pytest.mark.skipif(not os.path.isdir("/root/reference/proj/include") or shutil.which("g++") is None,
+                    reason="reference headers not present (dev container only)")
+def test_cpp_adapter_compiles_with_reference_headers():
+    """plseeds::b200::enumerate_wpm(const plseeds::SearchJob&) type-checks
+    against the unmodified reference headers."""
+    src = r'''
+#include "plseeds/pipeline.hpp"
+#include "plseeds_b200.hpp"
+int main() {
+    using namespace plseeds;
+    SearchJob job;
+    job.m = 6; job.n = 2;
+    job.facets = matroid_universe(idcm_orbits(2, 4)[0]);
+    const auto A = incidence_matrix(job.facets);
+    job.basis = convenient_basis(kernel_basis(A), A);
+    job.properties = {ubt_property(2, (int)job.facets.size())};
+    auto out = std::getenv("WPM_RUN") ? b200::enumerate_wpm(job) : std::vector<PureComplex>{};
+    return (int)out.size() * 0;
+}
+'''
+    with tempfile.TemporaryDirectory() as td:
+        p = os.path.join(td, "a.cpp")
+        open(p, "w").write(src)
+        r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I/root/reference/proj/include", "-I",
+                            os.path.join(ROOT, "include"), p], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+
+
 def _has_gpu():
     import paper_2301_00806_b200 as w
 

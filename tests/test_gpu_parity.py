@@ -295,3 +295,21 @@ def test_nccl_gather_world1(wpm, golden):
         assert total == golden["ubt"]["5"]["sum"] and dups == 0
     finally:
         dist.destroy_process_group()
+
+
+def test_cpp_adapter_vs_reference():
+    """plseeds::b200::enumerate_wpm(const plseeds::SearchJob&) against the
+    reference's own enumerate_wpm in one binary (tests/cpp/adapter_check.cpp,
+    reference headers compiled in): orbit maps n = 2..5, full-subset
+    universes, link-pinned bases (apply_link_constraints), candidate_cap."""
+    import os
+    import subprocess
+
+    from conftest import ROOT
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "adapter_check")
+    if not os.path.exists(exe):
+        pytest.skip("adapter_check not built (needs the reference headers at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 mismatches" in r.stdout
