@@ -29,7 +29,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwpm_b200.so")
+LIB_PATH = os.path.join(_HERE, {"debug": "libwpm_b200_dbg.so", "traps": "libwpm_b200_trap.so"}.get(
+    os.environ.get("WPM_DEBUG_LIB", ""), "libwpm_b200.so"))
 
 WPM_OK = 0
 WPM_EINTERNAL = 1

@@ -46,6 +46,7 @@
 // whoever explores it, so node counts are deterministic.
 #include <cstdint>
 #include <climits>
+#include <cstdio>
 
 #include "wpm_dev.cuh"
 #include "wpm_internal.h"
@@ -145,26 +146,6 @@ __device__ __forceinline__ void apply_exclusions(WS& w, const MapView& mp, int l
     }
 }
 
-__device__ __forceinline__ void undo_exclusions(WS& w, const MapView& mp, int lo, int hi, int lane) {
-    for (int e = lo + lane; e < hi; e += 32) w.fst[w.trail[e] & 0x7FFF] = FU;
-    const int sh_l = mp.lpf_shift, k = lane & ((1 << sh_l) - 1), per = 32 >> sh_l;
-    for (int e0 = lo; e0 < hi; e0 += per) {
-        const int e = e0 + (lane >> sh_l);
-        bool undead = false;
-        if (e < hi && k < mp.n) {
-            const int g = w.trail[e] & 0x7FFF;
-            const int r = __ldg(mp.fr + g * mp.fs + k);
-            const unsigned sh = (r & 3) * 8;
-            const unsigned ob = (atomicAdd(&w.rsw[r >> 2], 4u << sh) >> sh) & 0xFFu;
-            undead = ob == 1u;                         // (1,0) -> (1,1)
-            if (ob == 1u || ob == (1u | (1u << 2)))    // enters / leaves b1
-                atomicXor(&w.b1[r >> 5], 1u << (r & 31));
-        }
-        w.ndead -= __popc(__ballot_sync(FULL, undead));
-    }
-    __syncwarp();
-}
-
 // exclude one facet (a tried sibling)
 __device__ __forceinline__ void exclude_one(WS& w, const MapView& mp, int g, int lane) {
     if (lane == 0) {
@@ -184,14 +165,39 @@ __device__ __forceinline__ void exclude_one(WS& w, const MapView& mp, int g, int
     __syncwarp();
 }
 
-__device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, int lane) {
-    const bool act = lane < mp.n;
-    int r = 0;
-    unsigned b = 4;
-    if (act) {
-        r = __ldg(mp.fr + f * mp.fs + lane);
-        b = w.rs[r];
+// The facet's ridges and their current bytes (lane k < n: k-th ridge), and
+// whether including it is dead on arrival: one of its ridges has it as the
+// sole undecided candidate (c = 0, a = 1) and would open with a = 0.  On the
+// CPU restatement 92-97 % of dead includes are of this kind; they are counted
+// as nodes but never applied (no include, no undo).
+struct Probe {
+    int r;
+    unsigned b;
+    bool dead;
+};
+
+__device__ __forceinline__ Probe probe_facet(const WS& w, const MapView& mp, int f, int lane) {
+    Probe pr{0, 4u, false};
+#ifdef WPM_TRAPS
+    if (f < 0 || f >= mp.M) {
+        if (lane == 0)
+            printf("WPM_TRAP probe f=%d M=%d nopen=%d ndead=%d size=%d tl=%d depth=%d\n", f, mp.M, w.nopen, w.ndead,
+                   w.size, w.tl, w.depth);
+        __trap();
     }
+#endif
+    if (lane < mp.n) {
+        pr.r = __ldg(mp.fr + f * mp.fs + lane);
+        pr.b = w.rs[pr.r];
+    }
+    pr.dead = __any_sync(FULL, pr.b == (1u << 2) && lane < mp.n);
+    return pr;
+}
+
+__device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, const Probe& pr, int lane) {
+    const bool act = lane < mp.n;
+    const int r = pr.r;
+    const unsigned b = pr.b;
     const unsigned c = b & 3u, a = b >> 2;   // c in {0,1}, a >= 1 (f is undecided)
     const bool opened = act && c == 0u, closed = act && c == 1u;
     if (act) {
@@ -246,50 +252,107 @@ __device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, i
     __syncwarp();
 }
 
-__device__ __forceinline__ void undo_include(WS& w, const MapView& mp, int f, int lane) {
-    const bool act = lane < mp.n;
-    int r = 0;
-    unsigned b = 0;
-    if (act) {
-        r = __ldg(mp.fr + f * mp.fs + lane);
-        b = w.rs[r];
+// Undo every decision on trail[mark..tl) at once.  Each decision is an
+// additive delta on the packed ridge bytes (include: c+1, a-1; exclusion:
+// a-1), so the final bytes do not depend on the order the inverse deltas are
+// applied in.  All (decision, ridge) pairs are flattened over the 32 lanes and
+// applied with shared atomics; each atomic returns the exact old byte, so the
+// open / forced / dead transitions it reports are exact and their sum
+// telescopes to the right totals and bitsets whatever the interleaving.
+__device__ __forceinline__ void undo_to(WS& w, const MapView& mp, int mark, int lane) {
+    const int lo = mark, hi = w.tl;
+    if (hi <= lo) return;
+#ifdef WPM_V_SYNC
+    __syncwarp();
+#endif
+    for (int e0 = lo; e0 < hi; e0 += 32) {
+        const int e = e0 + lane;
+        bool inc = false;
+        if (e < hi) {
+            const unsigned t = w.trail[e];
+            const int g = (int)(t & 0x7FFFu);
+            w.fst[g] = FU;
+            inc = (t & TR_INC) != 0u;
+            if (inc) atomicAnd(&w.inb[g >> 5], ~(1u << (g & 31)));
+        }
+        w.size -= __popc(__ballot_sync(FULL, inc));
     }
-    const unsigned c = b & 3u, a = b >> 2;   // c in {1,2}
-    if (act) {
-        w.rs[r] = (uint8_t)(b - 1u + 4u);    // c - 1, a + 1
-        const unsigned bit = 1u << (r & 31);
-        atomicXor(&w.open[r >> 5], bit);
-        if ((c == 1u && a == 1u) || (c == 2u && a == 0u)) atomicXor(&w.b1[r >> 5], bit);
+#ifdef WPM_V_SYNC
+    __syncwarp();
+#endif
+    const int sh_l = mp.lpf_shift, k = lane & ((1 << sh_l) - 1), per = 32 >> sh_l;
+    for (int e0 = lo; e0 < hi; e0 += per) {
+        const int e = e0 + (lane >> sh_l);
+        bool o0 = false, o1 = false, z0 = false, z1 = false;
+        if (e < hi && k < mp.n) {
+            const unsigned t = w.trail[e];
+            const int g = (int)(t & 0x7FFFu);
+            const int r = __ldg(mp.fr + g * mp.fs + k);
+            const unsigned delta = (t & TR_INC) ? 3u : 4u;  // (c-1, a+1) or (a+1)
+            const unsigned sh = (r & 3) * 8;
+            const unsigned ob = (atomicAdd(&w.rsw[r >> 2], delta << sh) >> sh) & 0xFFu;
+            const unsigned nb = ob + delta;
+            o0 = (ob & 3u) == 1u;
+            o1 = (nb & 3u) == 1u;
+            const bool f0 = ob == 5u, f1 = nb == 5u;  // (1,1): forced
+            z0 = ob == 1u;                            // (1,0): dead
+            z1 = nb == 1u;
+            const unsigned bit = 1u << (r & 31);
+            if (o0 != o1) atomicXor(&w.open[r >> 5], bit);
+            if (f0 != f1) atomicXor(&w.b1[r >> 5], bit);
+        }
+        w.nopen += __popc(__ballot_sync(FULL, o1 && !o0)) - __popc(__ballot_sync(FULL, o0 && !o1));
+        w.ndead += __popc(__ballot_sync(FULL, z1 && !z0)) - __popc(__ballot_sync(FULL, z0 && !z1));
     }
-    const bool was_open = act && c == 1u, was_closed = act && c == 2u;
-    const unsigned bo = __ballot_sync(FULL, was_open), bc = __ballot_sync(FULL, was_closed);
-    const unsigned bd = __ballot_sync(FULL, was_open && a == 0u);
-    w.nopen += __popc(bc) - __popc(bo);
-    w.ndead -= __popc(bd);
-    if (lane == 0) {
-        w.fst[f] = FU;
-        w.inb[f >> 5] &= ~(1u << (f & 31));
-    }
-    w.size -= 1;
+    w.tl = mark;
     __syncwarp();
 }
 
-__device__ __forceinline__ void undo_to(WS& w, const MapView& mp, int mark, int lane) {
-    while (w.tl > mark) {
-        const int idx = w.tl - 1 - lane;
-        const bool valid = idx >= mark;
-        const unsigned e = valid ? w.trail[idx] : 0u;
-        const unsigned bi = __ballot_sync(FULL, valid && (e & TR_INC));
-        if (bi & 1u) {
-            undo_include(w, mp, (int)(__shfl_sync(FULL, e, 0) & 0x7FFFu), lane);
-            w.tl -= 1;
-        } else {
-            const int run = bi ? (__ffs(bi) - 1) : min(32, w.tl - mark);
-            undo_exclusions(w, mp, w.tl - run, w.tl, lane);
-            w.tl -= run;
+#ifdef WPM_DEBUG
+// Debug builds: recompute every derived quantity from the facet statuses and
+// trap on the first mismatch (counts, open / forced bitsets, open / dead
+// tallies, IN bitset, size).
+__device__ void debug_check(const WS& w, const MapView& mp, int lane, int where) {
+    __syncwarp();
+    int bad = 0, nopen = 0, ndead = 0, size = 0;
+    for (int r = lane; r < mp.N; r += 32) {
+        unsigned c = 0, a = 0;
+        for (int q = 0; q < mp.ps; ++q) {
+            const int g = __ldg(mp.rp + r * mp.ps + q);
+            if (g == NONE16) continue;
+            c += w.fst[g] == FIN;
+            a += w.fst[g] == FU;
         }
+        const unsigned b = w.rs[r];
+        if (b != (c | (a << 2))) bad |= 1;
+        const bool op = c == 1, f1 = c == 1 && a == 1;
+        if (((w.open[r >> 5] >> (r & 31)) & 1u) != (unsigned)op) bad |= 2;
+        if (((w.b1[r >> 5] >> (r & 31)) & 1u) != (unsigned)f1) bad |= 4;
+        nopen += op;
+        ndead += op && a == 0;
+    }
+    for (int f = lane; f < mp.M; f += 32) {
+        size += w.fst[f] == FIN;
+        if (((w.inb[f >> 5] >> (f & 31)) & 1u) != (unsigned)(w.fst[f] == FIN)) bad |= 8;
+    }
+    nopen = (int)__reduce_add_sync(FULL, (unsigned)nopen);
+    ndead = (int)__reduce_add_sync(FULL, (unsigned)ndead);
+    size = (int)__reduce_add_sync(FULL, (unsigned)size);
+    bad = (int)__reduce_or_sync(FULL, (unsigned)bad);
+    if (nopen != w.nopen) bad |= 16;
+    if (ndead != w.ndead) bad |= 32;
+    if (size != w.size) bad |= 64;
+    if (bad) {
+        if (lane == 0)
+            printf("WPM_DEBUG mismatch %d at site %d: nopen %d/%d ndead %d/%d size %d/%d tl %d depth %d\n", bad, where,
+                   w.nopen, nopen, w.ndead, ndead, w.size, size, w.tl, w.depth);
+        __trap();
     }
 }
+#define DEBUG_CHECK(w, mp, lane, where) debug_check(w, mp, lane, where)
+#else
+#define DEBUG_CHECK(w, mp, lane, where) ((void)0)
+#endif
 
 // MRV branch ridge: the lowest open ridge with one undecided candidate, else
 // the open ridge with the fewest (ties: lowest id).  Returns ridge | a << 16.
@@ -312,6 +375,7 @@ __device__ __forceinline__ unsigned select_ridge(const WS& w, int nw, int lane) 
             best = min(best, ((unsigned)(w.rs[r] >> 2) << 16) | (unsigned)r);
         }
     }
+    __syncwarp();  // reconverge after the divergent scan before the CREDUX
     return __reduce_min_sync(FULL, best);
 }
 
@@ -388,8 +452,11 @@ __device__ __forceinline__ bool descend(WS& w, const MapView& mp, const SearchPa
             if ((sel >> 16) == 1u) {  // forced: the only undecided candidate
                 int q;
                 const int u = first_candidate(w, mp, (int)ridge, 0, &q, lane);
-                include_facet(w, mp, u, lane);
+                const Probe pr = probe_facet(w, mp, u, lane);
                 ++nodes;
+                if (pr.dead) return false;
+                include_facet(w, mp, u, pr, lane);
+                DEBUG_CHECK(w, mp, lane, 1);
                 continue;
             }
         }
@@ -419,6 +486,7 @@ __device__ __forceinline__ bool load_state(WS& w, const MapView& mp, const uint3
             w.fst[f] = (iv & bit) ? FIN : ((ov & bit) ? FOUT : FU);
         }
     }
+    __syncwarp();  // reconverge after the divergent loops before the CREDUX
     w.size = (int)__reduce_add_sync(FULL, (unsigned)size);
     __syncwarp();
     // pass 1: IN counts; a count >= 3 is infeasible
@@ -619,9 +687,13 @@ __global__ void __launch_bounds__(128) k3_search(const __grid_constant__ SearchP
 
         if (load_state(w, mp, rec + 4, rec + 4 + p.mw, lane)) {
             if (kind == T_SINGLE) {
-                include_facet(w, mp, (int)h1, lane);
+                const Probe pr = probe_facet(w, mp, (int)h1, lane);
                 ++nodes;
-                descend(w, mp, p, nodes, lane);
+                if (!pr.dead) {
+                    include_facet(w, mp, (int)h1, pr, lane);
+                    DEBUG_CHECK(w, mp, lane, 2);
+                    descend(w, mp, p, nodes, lane);
+                }
             } else if (kind == T_ENTRY) {
                 descend(w, mp, p, nodes, lane);
             } else if (w.ndead == 0) {  // resume a donated frame
@@ -645,7 +717,9 @@ __global__ void __launch_bounds__(128) k3_search(const __grid_constant__ SearchP
                 if (w.depth > 0) {
                     const uint2 pf = w.frames[w.depth - 1];
                     undo_to(w, mp, (int)(pf.y >> 16), lane);
+                    DEBUG_CHECK(w, mp, lane, 3);
                     exclude_one(w, mp, (int)(pf.y & 0xFFFFu), lane);
+                    DEBUG_CHECK(w, mp, lane, 4);
                     if ((pf.x & 0xFFFFu) != CLOSED_FRAME && w.ndead) {
                         if (lane == 0) w.frames[w.depth - 1].x = (pf.x & 0xFFFFu) | (POS_DONE << 16);
                         __syncwarp();
@@ -657,11 +731,19 @@ __global__ void __launch_bounds__(128) k3_search(const __grid_constant__ SearchP
             if (lane == 0) w.frames[w.depth - 1] = make_uint2((fr.x & 0xFFFFu) | ((uint32_t)npos << 16),
                                                               (uint32_t)c | ((uint32_t)cm << 16));
             __syncwarp();
-            include_facet(w, mp, c, lane);
+            const Probe pr = probe_facet(w, mp, c, lane);
             ++nodes;
-            if (!descend(w, mp, p, nodes, lane)) {
+            bool pushed = false;
+            if (!pr.dead) {
+                include_facet(w, mp, c, pr, lane);
+                DEBUG_CHECK(w, mp, lane, 5);
+                pushed = descend(w, mp, p, nodes, lane);
+            }
+            if (!pushed) {
                 undo_to(w, mp, cm, lane);
+                DEBUG_CHECK(w, mp, lane, 6);
                 exclude_one(w, mp, c, lane);
+                DEBUG_CHECK(w, mp, lane, 7);
                 if ((fr.x & 0xFFFFu) != CLOSED_FRAME && w.ndead) {
                     if (lane == 0) w.frames[w.depth - 1].x = (fr.x & 0xFFFFu) | (POS_DONE << 16);
                     __syncwarp();
