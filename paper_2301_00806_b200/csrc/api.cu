@@ -689,6 +689,9 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
             return fail(WPM_EINTERNAL, "seed launch failed");
         const int est_warps = P->num_sms * 16;
         sp.hungry = std::max(64, est_warps / 2);
+        sp.backoff_max = 8192;
+        if (const char* e = std::getenv("WPM_HUNGRY")) sp.hungry = std::atoi(e);
+        if (const char* e = std::getenv("WPM_BACKOFF_MAX")) sp.backoff_max = std::max(32, std::atoi(e));
         CU(cudaEventRecord(P->ev[0], P->stream));
         if (ntasks > 0 && !launch_k3_search(sp, P->num_sms, P->stream, &P->warps))
             return fail(WPM_EINTERNAL, std::string("kernel 3 launch: ") + cudaGetErrorString(cudaGetLastError()));

@@ -117,6 +117,47 @@ struct WS {
 
 __device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
+// Predicated shared-memory updates: one instruction each, no branch, so the
+// warp never diverges around them (a C++ `if (cond) atomicXor(...)` costs a
+// BSSY/BSYNC pair plus BRA.DIV guards before the next warp intrinsic).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void red_xor_if(uint32_t* p, uint32_t v, bool pred) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.shared.xor.b32 [%0], %1; }" ::"r"(smem_addr(p)),
+                 "r"(v), "r"((uint32_t)pred)
+                 : "memory");
+}
+__device__ __forceinline__ void red_and_if(uint32_t* p, uint32_t v, bool pred) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.shared.and.b32 [%0], %1; }" ::"r"(smem_addr(p)),
+                 "r"(v), "r"((uint32_t)pred)
+                 : "memory");
+}
+__device__ __forceinline__ void red_or_if(uint32_t* p, uint32_t v, bool pred) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.shared.or.b32 [%0], %1; }" ::"r"(smem_addr(p)),
+                 "r"(v), "r"((uint32_t)pred)
+                 : "memory");
+}
+__device__ __forceinline__ void st_u8_if(uint8_t* p, uint32_t v, bool pred) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u8 [%0], %1; }" ::"r"(smem_addr(p)), "r"(v),
+                 "r"((uint32_t)pred)
+                 : "memory");
+}
+// predicated shared atomic add returning the old word (0 when not executed)
+__device__ __forceinline__ uint32_t atom_add_if(uint32_t* p, uint32_t v, bool pred) {
+    uint32_t old = 0;
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %3, 0; @q atom.shared.add.u32 %0, [%1], %2; }"
+                 : "+r"(old)
+                 : "r"(smem_addr(p)), "r"(v), "r"((uint32_t)pred)
+                 : "memory");
+    return old;
+}
+__device__ __forceinline__ void st_u16_if(uint16_t* p, uint32_t v, bool pred) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u16 [%0], %1; }" ::"r"(smem_addr(p)), "r"(v),
+                 "r"((uint32_t)pred)
+                 : "memory");
+}
+
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
@@ -132,35 +173,27 @@ __device__ __forceinline__ void apply_exclusions(WS& w, const MapView& mp, int l
     const int sh_l = mp.lpf_shift, k = lane & ((1 << sh_l) - 1), per = 32 >> sh_l;
     for (int e0 = lo; e0 < hi; e0 += per) {
         const int e = e0 + (lane >> sh_l);
-        bool dead = false;
-        if (e < hi && k < mp.n) {
-            const int g = w.trail[e] & 0x7FFF;
-            const int r = __ldg(mp.fr + g * mp.fs + k);
-            const unsigned sh = (r & 3) * 8;
-            const unsigned ob = (atomicSub(&w.rsw[r >> 2], 4u << sh) >> sh) & 0xFFu;
-            dead = ob == (1u | (1u << 2));             // (1,1) -> (1,0)
-            if (ob == (1u | (1u << 2)) || ob == (1u | (2u << 2)))  // leaves / enters b1
-                atomicXor(&w.b1[r >> 5], 1u << (r & 31));
-        }
-        w.ndead += __popc(__ballot_sync(FULL, dead));
+        const bool act = e < hi && k < mp.n;
+        const int g = act ? (w.trail[e] & 0x7FFF) : 0;
+        const int r = act ? __ldg(mp.fr + g * mp.fs + k) : 0;
+        const unsigned sh = (r & 3) * 8;
+        const unsigned ob = (atom_add_if(w.rsw + (r >> 2), 0u - (4u << sh), act) >> sh) & 0xFFu;
+        // (1,1) -> (1,0): dead and leaves the forced set; (1,2) -> (1,1): enters it
+        red_xor_if(w.b1 + (r >> 5), 1u << (r & 31), act && (ob == 5u || ob == 9u));
+        w.ndead += __popc(__ballot_sync(FULL, act && ob == 5u));
     }
 }
 
 // exclude one facet (a tried sibling)
 __device__ __forceinline__ void exclude_one(WS& w, const MapView& mp, int g, int lane) {
-    if (lane == 0) {
-        w.fst[g] = FOUT;
-        w.trail[w.tl] = (uint16_t)g;
-    }
-    bool dead = false;
-    if (lane < mp.n) {
-        const int r = __ldg(mp.fr + g * mp.fs + lane);
-        const unsigned sh = (r & 3) * 8;
-        const unsigned ob = (atomicSub(&w.rsw[r >> 2], 4u << sh) >> sh) & 0xFFu;
-        dead = ob == (1u | (1u << 2));
-        if (ob == (1u | (1u << 2)) || ob == (1u | (2u << 2))) atomicXor(&w.b1[r >> 5], 1u << (r & 31));
-    }
-    w.ndead += __popc(__ballot_sync(FULL, dead));
+    st_u8_if(w.fst + g, FOUT, lane == 0);
+    st_u16_if(w.trail + w.tl, (uint32_t)g, lane == 0);
+    const bool act = lane < mp.n;
+    const int r = act ? __ldg(mp.fr + g * mp.fs + lane) : 0;
+    const unsigned sh = (r & 3) * 8;
+    const unsigned ob = (atom_add_if(w.rsw + (r >> 2), 0u - (4u << sh), act) >> sh) & 0xFFu;
+    red_xor_if(w.b1 + (r >> 5), 1u << (r & 31), act && (ob == 5u || ob == 9u));
+    w.ndead += __popc(__ballot_sync(FULL, act && ob == 5u));
     w.tl += 1;
     __syncwarp();
 }
@@ -199,23 +232,21 @@ __device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, c
     const int r = pr.r;
     const unsigned b = pr.b;
     const unsigned c = b & 3u, a = b >> 2;   // c in {0,1}, a >= 1 (f is undecided)
-    const bool opened = act && c == 0u, closed = act && c == 1u;
-    if (act) {
-        w.rs[r] = (uint8_t)(b + 1u - 4u);    // c + 1, a - 1
-        const unsigned bit = 1u << (r & 31);
-        atomicXor(&w.open[r >> 5], bit);       // 0 -> 1 sets, 1 -> 2 clears
-        if ((c == 1u && a == 1u) || (c == 0u && a == 2u)) atomicXor(&w.b1[r >> 5], bit);
-    }
-    const unsigned bo = __ballot_sync(FULL, opened), bc = __ballot_sync(FULL, closed);
-    const unsigned bd = __ballot_sync(FULL, opened && a == 1u);
-    w.nopen += __popc(bo) - __popc(bc);
-    w.ndead += __popc(bd);
-    if (closed) w.scratch[__popc(bc & lanemask_lt(lane))] = (uint16_t)r;
-    if (lane == 0) {
-        w.fst[f] = FIN;
-        w.inb[f >> 5] |= 1u << (f & 31);
-        w.trail[w.tl] = (uint16_t)(f | TR_INC);
-    }
+    const bool closed = act && c == 1u;
+    // branch-free: every lane k < n updates its ridge (c + 1, a - 1); the open
+    // bit always flips (0 -> 1 opens, 1 -> 2 closes); the forced bit flips on
+    // (1,1) -> (2,0) and (0,2) -> (1,1).  Opening with a = 0 cannot happen:
+    // probe_facet filtered those includes.
+    const unsigned bit = 1u << (r & 31);
+    st_u8_if(w.rs + r, b + 1u - 4u, act);
+    red_xor_if(w.open + (r >> 5), bit, act);
+    red_xor_if(w.b1 + (r >> 5), bit, act && (b == 5u || b == 8u));
+    const unsigned bc = __ballot_sync(FULL, closed);
+    w.nopen += mp.n - 2 * __popc(bc);
+    st_u16_if(w.scratch + __popc(bc & lanemask_lt(lane)), (uint32_t)r, closed);
+    st_u8_if(w.fst + f, FIN, lane == 0);
+    red_or_if(w.inb + (f >> 5), 1u << (f & 31), lane == 0);
+    st_u16_if(w.trail + w.tl, (uint32_t)(f | TR_INC), lane == 0);
     w.tl += 1;
     w.size += 1;
     __syncwarp();
@@ -227,21 +258,14 @@ __device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, c
     int E = 0;
     for (int j0 = 0; j0 < ncl; j0 += 4) {
         const int j = j0 + (lane >> 3), q = lane & 7;
-        bool v = false;
-        int g = 0;
-        if (j < ncl) {
-            const int rr = w.scratch[j];
-            if (q < mp.ps) {
-                g = __ldg(mp.rp + rr * mp.ps + q);
-                v = g != NONE16 && w.fst[g] == FU;
-            }
-        }
+        const bool slot = j < ncl && q < mp.ps;
+        const int rr = w.scratch[j & 31];
+        const int g0 = slot ? (int)__ldg(mp.rp + rr * mp.ps + q) : (int)NONE16;
+        const int g = g0 == NONE16 ? 0 : g0;
+        const bool v = g0 != NONE16 && w.fst[g] == FU;
         const unsigned bv = __ballot_sync(FULL, v);
-        if (v) {
-            const int pos = base + E + __popc(bv & lanemask_lt(lane));
-            w.trail[pos] = (uint16_t)g;
-            w.fst[g] = FOUT;
-        }
+        st_u16_if(w.trail + base + E + __popc(bv & lanemask_lt(lane)), (uint32_t)g, v);
+        st_u8_if(w.fst + g, FOUT, v);
         E += __popc(bv);
     }
     if (E) {
@@ -262,45 +286,33 @@ __device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, c
 __device__ __forceinline__ void undo_to(WS& w, const MapView& mp, int mark, int lane) {
     const int lo = mark, hi = w.tl;
     if (hi <= lo) return;
-#ifdef WPM_V_SYNC
-    __syncwarp();
-#endif
     for (int e0 = lo; e0 < hi; e0 += 32) {
         const int e = e0 + lane;
-        bool inc = false;
-        if (e < hi) {
-            const unsigned t = w.trail[e];
-            const int g = (int)(t & 0x7FFFu);
-            w.fst[g] = FU;
-            inc = (t & TR_INC) != 0u;
-            if (inc) atomicAnd(&w.inb[g >> 5], ~(1u << (g & 31)));
-        }
+        const bool act = e < hi;
+        const unsigned t = act ? (unsigned)w.trail[e] : 0u;
+        const int g = (int)(t & 0x7FFFu);
+        const bool inc = act && (t & TR_INC);
+        st_u8_if(w.fst + g, FU, act);
+        red_and_if(w.inb + (g >> 5), ~(1u << (g & 31)), inc);
         w.size -= __popc(__ballot_sync(FULL, inc));
     }
-#ifdef WPM_V_SYNC
-    __syncwarp();
-#endif
     const int sh_l = mp.lpf_shift, k = lane & ((1 << sh_l) - 1), per = 32 >> sh_l;
     for (int e0 = lo; e0 < hi; e0 += per) {
         const int e = e0 + (lane >> sh_l);
-        bool o0 = false, o1 = false, z0 = false, z1 = false;
-        if (e < hi && k < mp.n) {
-            const unsigned t = w.trail[e];
-            const int g = (int)(t & 0x7FFFu);
-            const int r = __ldg(mp.fr + g * mp.fs + k);
-            const unsigned delta = (t & TR_INC) ? 3u : 4u;  // (c-1, a+1) or (a+1)
-            const unsigned sh = (r & 3) * 8;
-            const unsigned ob = (atomicAdd(&w.rsw[r >> 2], delta << sh) >> sh) & 0xFFu;
-            const unsigned nb = ob + delta;
-            o0 = (ob & 3u) == 1u;
-            o1 = (nb & 3u) == 1u;
-            const bool f0 = ob == 5u, f1 = nb == 5u;  // (1,1): forced
-            z0 = ob == 1u;                            // (1,0): dead
-            z1 = nb == 1u;
-            const unsigned bit = 1u << (r & 31);
-            if (o0 != o1) atomicXor(&w.open[r >> 5], bit);
-            if (f0 != f1) atomicXor(&w.b1[r >> 5], bit);
-        }
+        const bool act = e < hi && k < mp.n;
+        const unsigned t = act ? (unsigned)w.trail[e] : 0u;
+        const int g = (int)(t & 0x7FFFu);
+        const int r = act ? __ldg(mp.fr + g * mp.fs + k) : 0;
+        const unsigned delta = (t & TR_INC) ? 3u : 4u;  // (c-1, a+1) or (a+1)
+        const unsigned sh = (r & 3) * 8;
+        const unsigned ob = (atom_add_if(w.rsw + (r >> 2), delta << sh, act) >> sh) & 0xFFu;
+        const unsigned nb = ob + delta;
+        const bool o0 = act && (ob & 3u) == 1u, o1 = act && (nb & 3u) == 1u;
+        const bool f0 = ob == 5u, f1 = nb == 5u;            // (1,1): forced
+        const bool z0 = act && ob == 1u, z1 = act && nb == 1u;  // (1,0): dead
+        const unsigned bit = 1u << (r & 31);
+        red_xor_if(w.open + (r >> 5), bit, o0 != o1);
+        red_xor_if(w.b1 + (r >> 5), bit, act && f0 != f1);
         w.nopen += __popc(__ballot_sync(FULL, o1 && !o0)) - __popc(__ballot_sync(FULL, o0 && !o1));
         w.ndead += __popc(__ballot_sync(FULL, z1 && !z0)) - __popc(__ballot_sync(FULL, z0 && !z1));
     }
@@ -382,12 +394,10 @@ __device__ __forceinline__ unsigned select_ridge(const WS& w, int nw, int lane) 
 // the undecided candidates of an OPEN frame's ridge from slot pos: first one
 __device__ __forceinline__ int first_candidate(const WS& w, const MapView& mp, int ridge, int pos, int* slot,
                                                int lane) {
-    int g = 0;
-    bool ok = false;
-    if (lane >= pos && lane < mp.ps) {
-        g = __ldg(mp.rp + ridge * mp.ps + lane);
-        ok = g != NONE16 && w.fst[g] == FU;
-    }
+    const bool in_range = lane >= pos && lane < mp.ps;
+    const int g0 = in_range ? (int)__ldg(mp.rp + ridge * mp.ps + lane) : (int)NONE16;
+    const int g = g0 == NONE16 ? 0 : g0;
+    const bool ok = g0 != NONE16 && w.fst[g] == FU;
     const unsigned b = __ballot_sync(FULL, ok);
     if (!b) return -1;
     const int q = __ffs(b) - 1;
@@ -470,7 +480,7 @@ __device__ __forceinline__ bool descend(WS& w, const MapView& mp, const SearchPa
 // rebuild the warp state from an IN/OUT record (+ closure: a ridge with two
 // IN candidates excludes the rest).  Returns false if infeasible.
 __device__ __forceinline__ bool load_state(WS& w, const MapView& mp, const uint32_t* rec_in, const uint32_t* rec_out,
-                                           int lane) {
+                                           bool closure, int lane) {
     const int M = mp.M, N = mp.N, mw = (M + 31) >> 5, nw = mp.nw;
     int size = 0;
     for (int i = lane; i < mw; i += 32) {
@@ -489,39 +499,44 @@ __device__ __forceinline__ bool load_state(WS& w, const MapView& mp, const uint3
     __syncwarp();  // reconverge after the divergent loops before the CREDUX
     w.size = (int)__reduce_add_sync(FULL, (unsigned)size);
     __syncwarp();
-    // pass 1: IN counts; a count >= 3 is infeasible
-    bool bad = false;
-    for (int r = lane; r < N; r += 32) {
-        unsigned c = 0;
-        for (int q = 0; q < mp.ps; ++q) {
-            const int g = __ldg(mp.rp + r * mp.ps + q);
-            c += g != NONE16 && w.fst[g] == FIN;
+    if (closure) {
+        // pass 1: IN counts; a count >= 3 is infeasible
+        bool bad = false;
+        for (int r = lane; r < N; r += 32) {
+            unsigned c = 0;
+            for (int q = 0; q < mp.ps; ++q) {
+                const int g = __ldg(mp.rp + r * mp.ps + q);
+                c += g != NONE16 && w.fst[g] == FIN;
+            }
+            bad |= c > 2u;
+            w.rs[r] = (uint8_t)min(c, 2u);
         }
-        bad |= c > 2u;
-        w.rs[r] = (uint8_t)min(c, 2u);
+        if (__any_sync(FULL, bad)) return false;
+        __syncwarp();
+        // closure: undecided facets on a closed ridge are excluded
+        for (int f = lane; f < M; f += 32) {
+            if (w.fst[f] != FU) continue;
+            bool on_closed = false;
+            for (int k = 0; k < mp.n; ++k) on_closed |= w.rs[__ldg(mp.fr + f * mp.fs + k)] == 2u;
+            if (on_closed) w.fst[f] = FOUT;
+        }
+        __syncwarp();
     }
-    if (__any_sync(FULL, bad)) return false;
-    __syncwarp();
-    // closure: undecided facets on a closed ridge are excluded
-    for (int f = lane; f < M; f += 32) {
-        if (w.fst[f] != FU) continue;
-        bool on_closed = false;
-        for (int k = 0; k < mp.n; ++k) on_closed |= w.rs[__ldg(mp.fr + f * mp.fs + k)] == 2u;
-        if (on_closed) w.fst[f] = FOUT;
-    }
-    __syncwarp();
-    // pass 2: undecided counts, open / b1 bitsets, open / dead tallies
+    // pass 2 (the only pass for states produced by the search itself, which
+    // are closed already): counts, open / b1 bitsets, open / dead tallies
     int nopen = 0, ndead = 0;
     for (int r0 = 0; r0 < nw * 32; r0 += 32) {
         const int r = r0 + lane;
         bool op = false, dd = false, one = false;
         if (r < N) {
-            unsigned a = 0;
+            unsigned a = 0, ci = 0;
             for (int q = 0; q < mp.ps; ++q) {
-                const int g = __ldg(mp.rp + r * mp.ps + q);
-                a += g != NONE16 && w.fst[g] == FU;
+                const int g0 = __ldg(mp.rp + r * mp.ps + q);
+                const unsigned s = g0 != NONE16 ? w.fst[g0] : (unsigned)FOUT;
+                a += s == FU;
+                ci += s == FIN;
             }
-            const unsigned c = w.rs[r];
+            const unsigned c = closure ? (unsigned)w.rs[r] : ci;
             w.rs[r] = (uint8_t)(c | (a << 2));
             op = c == 1u;
             dd = op && a == 0u;
@@ -658,7 +673,7 @@ __global__ void __launch_bounds__(128) k3_search(const __grid_constant__ SearchP
                     break;
                 }
                 __nanosleep(backoff);
-                backoff = min(backoff * 2u, 2048u);
+                backoff = min(backoff * 2u, (unsigned)p.backoff_max);
             }
         }
         t = __shfl_sync(FULL, t, 0);
@@ -685,7 +700,9 @@ __global__ void __launch_bounds__(128) k3_search(const __grid_constant__ SearchP
         mp.ps = md.rp_stride;
         ++tasks;
 
-        if (load_state(w, mp, rec + 4, rec + 4 + p.mw, lane)) {
+        // only pinned ENTRY tasks need the closure pass; seeded roots (nothing
+        // IN) and donated frames (a state of the search) are closed already
+        if (load_state(w, mp, rec + 4, rec + 4 + p.mw, kind == T_ENTRY, lane)) {
             if (kind == T_SINGLE) {
                 const Probe pr = probe_facet(w, mp, (int)h1, lane);
                 ++nodes;

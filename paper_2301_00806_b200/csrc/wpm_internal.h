@@ -31,6 +31,7 @@ struct SearchParams {
     unsigned long long* qctl;  // [0] tail << 32 | head, [2] pending, [3] tasks done, [4] nodes
     int qcap, recw, mw;
     int hungry;                 // donate while queued tasks < hungry
+    int backoff_max;            // ns, idle warps' polling backoff cap
     // output
     uint32_t* out_bits;         // out_cap * w32
     uint16_t* out_map;
