@@ -29,8 +29,10 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, {"debug": "libwpm_b200_dbg.so", "traps": "libwpm_b200_trap.so"}.get(
-    os.environ.get("WPM_DEBUG_LIB", ""), "libwpm_b200.so"))
+# WPM_DEBUG_LIB=debug|traps|<variant> selects a diagnostic build of the same sources
+_VARIANT = os.environ.get("WPM_DEBUG_LIB", "")
+LIB_PATH = os.path.join(_HERE, {"": "libwpm_b200.so", "debug": "libwpm_b200_dbg.so"}.get(
+    _VARIANT, f"libwpm_b200_{_VARIANT}.so"))
 
 WPM_OK = 0
 WPM_EINTERNAL = 1

@@ -157,7 +157,7 @@ struct wpm_plan {
     int64_t facet_cap = WPM_CAP_UBT;
     std::vector<int32_t> M, N, cap;
     std::vector<MapDesc> desc;
-    int maxM = 0, maxN = 0, maxDepth = 0, w32 = 0, mw = 0;
+    int maxM = 0, maxN = 0, maxDepth = 0, w32 = 0, mw = 0, rw = 0;
     // device tables
     DevBuf<MapDesc> d_maps;
     DevBuf<uint32_t> d_facets, d_ridges;
@@ -174,8 +174,8 @@ struct wpm_plan {
     int qcap = 0, recw = 0;
     DevBuf<int32_t> d_task_map, d_task_f, d_task_kind;
     // outputs
-    DevBuf<uint32_t> d_out_bits, d_sorted_bits;
-    DevBuf<uint16_t> d_out_map, d_sorted_map;
+    DevBuf<uint32_t> d_out_keys, d_sorted_bits;  // key rows from kernel 3; canonical rows
+    DevBuf<uint16_t> d_sorted_map;
     DevBuf<unsigned long long> d_out_ctl, d_per_map;
     DevBuf<uint32_t> d_idx_a;
     DevBuf<uint8_t> d_temp;
@@ -412,6 +412,7 @@ static int plan_build_tables(wpm_plan* P, const std::vector<uint32_t>& foff) {
     CU(cudaMemcpyAsync(P->d_maps.p, P->desc.data(), K * sizeof(MapDesc), cudaMemcpyHostToDevice, P->stream));
     P->mw = (P->maxM + 31) / 32;
     P->w32 = 2 * ((P->maxM + 63) / 64);
+    P->rw = key_words_for(P->w32) + 1;
     P->recw = 4 + 2 * P->mw;
     CU(cudaStreamSynchronize(P->stream));
     return WPM_OK;
@@ -644,13 +645,12 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         // needed if the WPM count exceeds it; the count is then known)
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
-        const unsigned long long row = (unsigned long long)P->w32 * 4 + 2;
+        const unsigned long long row = (unsigned long long)P->rw * 4 * 3;  // keys + sort temp + sorted rows
         P->out_cap = std::min<unsigned long long>(std::max<unsigned long long>(fr / 16 / row, 1ull << 20), 1ull << 26);
     }
     CU(cudaEventRecord(P->ev[4], P->stream));
     for (int attempt = 0; attempt < 2; ++attempt) {
-        if (P->d_out_bits.ensure(P->out_cap * P->w32) || P->d_out_map.ensure(P->out_cap))
-            return fail(WPM_EINTERNAL, "device allocation failed (output)");
+        if (P->d_out_keys.ensure(P->out_cap * P->rw)) return fail(WPM_EINTERNAL, "device allocation failed (output)");
         if (ntasks) {
             CU(cudaMemcpyAsync(P->d_task_map.p, tm.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
             CU(cudaMemcpyAsync(P->d_task_f.p, tf.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
@@ -677,12 +677,11 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         sp.qcap = qcap;
         sp.recw = P->recw;
         sp.mw = P->mw;
-        sp.out_bits = P->d_out_bits.p;
-        sp.out_map = P->d_out_map.p;
+        sp.out_keys = P->d_out_keys.p;
         sp.out_ctl = P->d_out_ctl.p;
         sp.per_map = P->d_per_map.p;
         sp.out_cap = P->out_cap;
-        sp.w32 = P->w32;
+        sp.rw = P->rw;
         if (launch_seed_tasks(sp, ntasks, P->d_task_map.p, P->d_task_f.p, P->d_task_kind.p,
                               P->has_pins ? P->d_pin_in.p : nullptr, P->has_pins ? P->d_pin_out.p : nullptr,
                               P->stream))
@@ -711,15 +710,14 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
     // canonical sort
     const long long total = P->total;
     const size_t tb = canon_sort_temp_bytes(std::max<long long>(total, 1), P->w32);
-    if (P->d_temp.ensure(tb) || P->d_idx_a.ensure(total + 1) || P->d_sorted_bits.ensure((size_t)total * P->w32 + 1) ||
+    if (P->d_temp.ensure(tb) || P->d_sorted_bits.ensure((size_t)total * P->w32 + 1) ||
         P->d_sorted_map.ensure(total + 1))
         return fail(WPM_EINTERNAL, "device allocation failed (sort)");
     CU(cudaMemsetAsync(P->d_out_ctl.p + 1, 0, 8, P->stream));
     CU(cudaMemsetAsync(P->d_per_map.p, 0xFF, K * 8, P->stream));  // first row per map, -1 = none
     CU(cudaEventRecord(P->ev[2], P->stream));
-    if (canon_sort(P->d_out_bits.p, P->d_out_map.p, total, P->w32, P->d_sorted_bits.p, P->d_sorted_map.p,
-                   P->d_temp.p, P->d_temp.n, P->d_idx_a.p, (long long*)P->d_per_map.p, P->d_out_ctl.p + 1,
-                   P->stream))
+    if (canon_sort_keys(P->d_out_keys.p, total, P->w32, P->d_sorted_bits.p, P->d_sorted_map.p, P->d_temp.p,
+                        P->d_temp.n, (long long*)P->d_per_map.p, P->d_out_ctl.p + 1, P->stream))
         return fail(WPM_EINTERNAL, std::string("canonical sort: ") + cudaGetErrorString(cudaGetLastError()));
     CU(cudaEventRecord(P->ev[3], P->stream));
     unsigned long long dups = 0;
@@ -795,13 +793,17 @@ extern "C" int wpm_canonical_sort_device(int32_t device, const uint32_t* bits32,
         if (dups) *dups = 0;
         return WPM_OK;
     }
+    const int kw = key_words_for(words32);
+    if (kw < 0) return fail(WPM_EINVAL, "rows wider than 64 words");
     DevBuf<uint8_t> temp;
-    DevBuf<uint32_t> idx;
+    DevBuf<uint32_t> keys;
     DevBuf<unsigned long long> d;
     const size_t tb = canon_sort_temp_bytes(count, words32);
-    if (temp.ensure(tb) || idx.ensure(count) || d.ensure(1)) return fail(WPM_EINTERNAL, "allocation failed (sort)");
+    if (temp.ensure(tb) || keys.ensure((size_t)count * (kw + 1)) || d.ensure(1))
+        return fail(WPM_EINTERNAL, "allocation failed (sort)");
     CU(cudaMemsetAsync(d.p, 0, 8, st));
-    if (canon_sort(bits32, map_ids, count, words32, out_bits32, out_map, temp.p, temp.n, idx.p, nullptr, d.p, st))
+    if (canon_pack(bits32, map_ids, count, words32, keys.p, st) ||
+        canon_sort_keys(keys.p, count, words32, out_bits32, out_map, temp.p, temp.n, nullptr, d.p, st))
         return fail(WPM_EINTERNAL, std::string("canonical sort: ") + cudaGetErrorString(cudaGetLastError()));
     unsigned long long h = 0;
     CU(cudaMemcpyAsync(&h, d.p, 8, cudaMemcpyDeviceToHost, st));

@@ -433,11 +433,10 @@ __device__ __forceinline__ void emit(const WS& w, const MapView& mp, const Searc
     unsigned long long slot = 0;
     if (lane == 0) slot = atomicAdd(&p.out_ctl[0], 1ull);
     slot = __shfl_sync(FULL, slot, 0);
-    if (slot < p.out_cap) {
-        uint32_t* o = p.out_bits + slot * (unsigned long long)p.w32;
-        const int mw = (mp.M + 31) >> 5;
-        for (int i = lane; i < p.w32; i += 32) o[i] = i < mw ? w.inb[i] : 0u;
-        if (lane == 0) p.out_map[slot] = (uint16_t)mp.map;
+    if (slot < p.out_cap) {  // key row: bitset words, zero padded, then the map id
+        uint32_t* o = p.out_keys + slot * (unsigned long long)p.rw;
+        const int mw = (mp.M + 31) >> 5, last = p.rw - 1;
+        for (int i = lane; i < p.rw; i += 32) o[i] = i < mw ? w.inb[i] : (i == last ? (uint32_t)mp.map : 0u);
     }
 }
 

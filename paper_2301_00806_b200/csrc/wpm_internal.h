@@ -32,13 +32,12 @@ struct SearchParams {
     int qcap, recw, mw;
     int hungry;                 // donate while queued tasks < hungry
     int backoff_max;            // ns, idle warps' polling backoff cap
-    // output
-    uint32_t* out_bits;         // out_cap * w32
-    uint16_t* out_map;
-    unsigned long long* out_ctl;  // [0] count, [1] overflow flag
-    unsigned long long* per_map;  // num_maps counts
+    // output: one key row per WPM = kw bitset words (zero padded) + the map id
+    uint32_t* out_keys;         // out_cap * rw
+    unsigned long long* out_ctl;  // [0] count, [1] duplicates (after the sort)
+    unsigned long long* per_map;  // scratch: first row per map (after the sort)
     unsigned long long out_cap;
-    int w32;
+    int rw;                     // key row words = key_words_for(w32) + 1
 };
 
 // seeds root tasks (map, f) in queue order; required/forbidden lists for ENTRY tasks
@@ -49,12 +48,18 @@ int launch_seed_tasks(const SearchParams& p, int ntasks, const int32_t* d_task_m
 // returns grid size used (0 on error)
 int launch_k3_search(const SearchParams& p, int num_sms, cudaStream_t st, int* warps_out);
 
-// canonical sort: orders out_bits/out_map (count rows) by (map, canonical order)
-// into sorted_bits, reports duplicates
-int canon_sort(const uint32_t* d_bits, const uint16_t* d_map, long long count, int w32,
-               uint32_t* d_sorted_bits, uint16_t* d_sorted_map, void* d_temp, size_t temp_bytes,
-               uint32_t* d_idx_a, long long* d_first_row, unsigned long long* d_dups, cudaStream_t st);
+// canonical sort (k4_canon.cu).  Key rows: key_words_for(w32) bitset words +
+// the map id.  canon_sort_keys sorts them in place by (map, canonical order)
+// and splits them into sorted_bits (w32 words per row) / sorted_map, with the
+// first row of each map and the adjacent-duplicate count.
+int key_words_for(int w32);
 size_t canon_sort_temp_bytes(long long count, int w32);
+int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sorted_bits, uint16_t* d_sorted_map,
+                    void* d_temp, size_t temp_bytes, long long* d_first_row, unsigned long long* d_dups,
+                    cudaStream_t st);
+// rows (w32 words) + uint16 map ids -> key rows
+int canon_pack(const uint32_t* d_bits, const uint16_t* d_map, long long count, int w32, uint32_t* d_keys,
+               cudaStream_t st);
 
 // INT32 lane-op issue peak (LOP3 + IADD3 chains over every SM), ops/s
 int int_peak_measure(int device, double* ops_per_s);
