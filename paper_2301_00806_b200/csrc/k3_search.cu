@@ -47,6 +47,8 @@
 #include <cstdint>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 
 #include "wpm_dev.cuh"
 #include "wpm_internal.h"
@@ -632,7 +634,10 @@ __device__ __forceinline__ void try_donate(WS& w, const MapView& mp, const Searc
     }
 }
 
-__global__ void __launch_bounds__(128) k3_search(const __grid_constant__ SearchParams p,
+#ifndef K3_MIN_BLOCKS
+#define K3_MIN_BLOCKS 8  // 32 warps/SM: the register budget that measured fastest
+#endif
+__global__ void __launch_bounds__(128, K3_MIN_BLOCKS) k3_search(const __grid_constant__ SearchParams p,
                                                  const __grid_constant__ Layout L) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -833,6 +838,7 @@ int launch_k3_search(const SearchParams& p, int num_sms, cudaStream_t st, int* w
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_search, 32 * wpb, smem) != cudaSuccess ||
         per_sm < 1)
         return 0;
+    if (const char* e = std::getenv("WPM_BLOCKS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
     const int grid = per_sm * num_sms;
     k3_search<<<grid, 32 * wpb, smem, st>>>(p, L);
     if (cudaGetLastError() != cudaSuccess) return 0;
