@@ -181,7 +181,7 @@ struct wpm_plan {
     DevBuf<uint8_t> d_temp;
     unsigned long long out_cap = 0;
     // last run
-    long long total = 0, nodes = 0, tasks = 0, dups = 0;
+    long long total = 0, nodes = 0, tasks = 0, dups = 0, reruns = 0;
     std::vector<unsigned long long> per_map;
     float ms_search = 0, ms_sort = 0, ms_total = 0;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -632,7 +632,7 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
     P->qcap = qcap;
     if (P->d_qrec.ensure((size_t)qcap * P->recw) || P->d_qready.ensure(qcap) || P->d_qctl.ensure(8) ||
         P->d_task_map.ensure(ntasks + 1) || P->d_task_f.ensure(ntasks + 1) || P->d_task_kind.ensure(ntasks + 1) ||
-        P->d_out_ctl.ensure(2) || P->d_per_map.ensure(K))
+        P->d_out_ctl.ensure(4) || P->d_per_map.ensure(K))
         return fail(WPM_EINTERNAL, "device allocation failed (queue)");
     if (P->has_pins) {
         if (P->d_pin_in.ensure(P->mw) || P->d_pin_out.ensure(P->mw))
@@ -649,7 +649,13 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         P->out_cap = std::min<unsigned long long>(std::max<unsigned long long>(fr / 16 / row, 1ull << 20), 1ull << 26);
     }
     CU(cudaEventRecord(P->ev[4], P->stream));
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    // frame stack sized for the branch depths the search reaches in practice
+    // (<= 37 measured up to n = 11); a run that outgrows it is redone with
+    // the worst-case layout (fewer warps per SM)
+    int frame_cap = 64;
+    if (const char* e = std::getenv("WPM_FRAME_CAP")) frame_cap = std::max(1, std::atoi(e));
+    bool full_depth = P->maxDepth <= frame_cap;
+    for (int attempt = 0; attempt < 3; ++attempt) {
         if (P->d_out_keys.ensure(P->out_cap * P->rw)) return fail(WPM_EINTERNAL, "device allocation failed (output)");
         if (ntasks) {
             CU(cudaMemcpyAsync(P->d_task_map.p, tm.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
@@ -660,13 +666,13 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         unsigned long long ctl[8] = {(unsigned long long)ntasks << 32, 0, (unsigned long long)ntasks, 0, 0, 0, 0, 0};
         CU(cudaMemcpyAsync(P->d_qctl.p, ctl, sizeof(ctl), cudaMemcpyHostToDevice, P->stream));
         CU(cudaMemsetAsync(P->d_qready.p, 0, (size_t)qcap * 8, P->stream));
-        CU(cudaMemsetAsync(P->d_out_ctl.p, 0, 16, P->stream));
+        CU(cudaMemsetAsync(P->d_out_ctl.p, 0, 32, P->stream));
         SearchParams sp{};
         sp.num_maps = K;
         sp.max_M = P->maxM;
         sp.max_N = P->maxN;
         sp.max_n = P->n;
-        sp.max_depth = P->maxDepth;
+        sp.max_depth = full_depth ? P->maxDepth : frame_cap;
         sp.maps = P->d_maps.p;
         sp.fr = P->d_fr.p;
         sp.rp = P->d_rp.p;
@@ -695,16 +701,22 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         if (ntasks > 0 && !launch_k3_search(sp, P->num_sms, P->stream, &P->warps))
             return fail(WPM_EINTERNAL, std::string("kernel 3 launch: ") + cudaGetErrorString(cudaGetLastError()));
         CU(cudaEventRecord(P->ev[1], P->stream));
-        unsigned long long octl[2], qc[8];
-        CU(cudaMemcpyAsync(octl, P->d_out_ctl.p, 16, cudaMemcpyDeviceToHost, P->stream));
+        unsigned long long octl[4], qc[8];
+        CU(cudaMemcpyAsync(octl, P->d_out_ctl.p, 32, cudaMemcpyDeviceToHost, P->stream));
         CU(cudaMemcpyAsync(qc, P->d_qctl.p, sizeof(qc), cudaMemcpyDeviceToHost, P->stream));
         CU(cudaStreamSynchronize(P->stream));
         P->h2d += (long long)sizeof(ctl);
-        P->d2h += 16 + (long long)sizeof(qc);
+        P->d2h += 32 + (long long)sizeof(qc);
         P->total = (long long)octl[0];
         P->tasks = (long long)qc[3];
         P->nodes = (long long)qc[4];
+        if (octl[2]) {  // frame stack overflowed: redo with the full-depth layout
+            full_depth = true;
+            ++P->reruns;
+            continue;
+        }
         if (octl[0] <= P->out_cap) break;
+        ++P->reruns;
         P->out_cap = octl[0] + octl[0] / 8 + 1024;  // exact count known now: rerun once
     }
     // canonical sort

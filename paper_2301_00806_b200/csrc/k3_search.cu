@@ -471,6 +471,13 @@ __device__ __forceinline__ bool descend(WS& w, const MapView& mp, const SearchPa
                 continue;
             }
         }
+        if (w.depth >= p.max_depth) {
+            // frame stack full (the launch sized it below the worst case to
+            // fit more warps): flag the run as incomplete; the host discards
+            // it and reruns with the full-depth layout
+            if (lane == 0) atomicExch(&p.out_ctl[2], 1ull);
+            return false;
+        }
         if (lane == 0) w.frames[w.depth] = make_uint2(ridge, NO_CHILD);
         w.depth += 1;
         __syncwarp();
