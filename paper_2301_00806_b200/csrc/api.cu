@@ -26,10 +26,6 @@
 #include "wpm_dev.cuh"
 #include "wpm_internal.h"
 
-namespace wpm {
-int k3_layout_bytes(int maxM, int maxN, int maxDepth);
-}
-
 using namespace wpm;
 
 namespace {
@@ -177,7 +173,6 @@ struct wpm_plan {
     DevBuf<uint32_t> d_out_keys, d_sorted_bits;  // key rows from kernel 3; canonical rows
     DevBuf<uint16_t> d_sorted_map;
     DevBuf<unsigned long long> d_out_ctl, d_per_map;
-    DevBuf<uint32_t> d_idx_a;
     DevBuf<uint8_t> d_temp;
     unsigned long long out_cap = 0;
     // last run

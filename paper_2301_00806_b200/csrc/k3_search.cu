@@ -64,35 +64,46 @@ constexpr uint32_t CLOSED_FRAME = 0xFFFFu;
 constexpr uint32_t POS_DONE = 0xFFFFu;
 constexpr uint32_t NO_CHILD = 0xFFFFu;
 constexpr int CHECK_EVERY = 32;  // nodes between looks at the queue word
+constexpr int FRAME_CAP = 64;    // frame stack of the fast layouts (measured depth <= 37)
 
 enum TaskKind : uint32_t { T_SINGLE = 0, T_OPEN = 1, T_CLOSED = 2, T_ENTRY = 3 };
 
-// per-warp shared-memory layout, byte offsets
-struct Layout {
-    int rs, fst, open, b1, inb, late, trail, frames, scratch, bytes;
-    int nw, mw;
+constexpr int a16(int x) { return (x + 15) & ~15; }
+
+// Per-warp shared-memory layout of one size class: every offset is a
+// compile-time constant, so each shared access is (warp base register +
+// immediate + index) -- one register for the whole state, no address
+// conversions in the PTX helpers.
+template <int NMAX, int MMAX, int DMAX>
+struct LC {
+    static constexpr int kN = NMAX, kM = MMAX, kDepth = DMAX;
+    static constexpr int NP = a16(NMAX + 32), MP = a16(MMAX + 32);
+    static constexpr int NW = (NMAX + 31) / 32, MW = (MMAX + 31) / 32;
+    static constexpr int RS = 0;                           // uint8 per ridge: count | undecided << 2
+    static constexpr int FST = RS + NP;                    // uint8 per facet: U / IN / OUT
+    static constexpr int OPEN = FST + MP;                  // open ridges (count 1)
+    static constexpr int B1 = OPEN + a16(4 * NW + 4);      // open ridges with one undecided candidate
+    static constexpr int INB = B1 + a16(4 * NW + 4);       // IN facet bitset
+    static constexpr int LATE = INB + a16(4 * MW + 4);     // donation scratch
+    static constexpr int TRAIL = LATE + a16(4 * MW + 4);   // uint16 per decision (bit 15: include)
+    static constexpr int FRAMES = TRAIL + a16(2 * MP);     // uint2 per branch frame
+    static constexpr int SCRATCH = FRAMES + a16(8 * (DMAX + 2));  // closing-ridge list
+    static constexpr int BYTES = SCRATCH + 64;
 };
 
-__host__ __device__ inline int align16(int x) { return (x + 15) & ~15; }
-
-__host__ __device__ inline Layout make_layout(int maxM, int maxN, int maxDepth) {
-    Layout L;
-    const int MP = align16(maxM + 32), NP = align16(maxN + 32);
-    L.nw = (maxN + 31) / 32;
-    L.mw = (maxM + 31) / 32;
-    int o = 0;
-    L.rs = o;      o += NP;                       // uint8 per ridge: count | undecided << 2
-    L.fst = o;     o += MP;                       // uint8 per facet: U / IN / OUT
-    L.open = o;    o += align16(4 * L.nw + 4);    // open ridges (count 1)
-    L.b1 = o;      o += align16(4 * L.nw + 4);    // open ridges with exactly one undecided candidate
-    L.inb = o;     o += align16(4 * L.mw + 4);    // IN facet bitset
-    L.late = o;    o += align16(4 * L.mw + 4);    // donation scratch: facets decided after a frame
-    L.trail = o;   o += align16(2 * MP);          // uint16 per decision (bit 15: include)
-    L.frames = o;  o += align16(8 * (maxDepth + 2));
-    L.scratch = o; o += 64;                       // closing-ridge list
-    L.bytes = o;
-    return L;
-}
+// size classes (max ridges, max facets, frame capacity): the exact shapes of
+// the Picard-4 universes per n (max N, max M over the maps), so the per-warp
+// state is no larger than needed and L1 keeps room for the per-map tables,
+// plus the general layouts
+using C5 = LC<128, 128, FRAME_CAP>;       // n <= 5
+using C6 = LC<232, 136, FRAME_CAP>;
+using C7 = LC<420, 208, FRAME_CAP>;
+using C8 = LC<720, 312, FRAME_CAP>;
+using C9 = LC<1152, 440, FRAME_CAP>;
+using C10 = LC<1792, 616, FRAME_CAP>;
+using C11 = LC<2688, 840, FRAME_CAP>;
+using CG = LC<4096, 2048, FRAME_CAP>;     // any universe within the device limits
+using CGF = LC<4096, 2048, 2050>;         // full depth: the rerun after a frame overflow
 
 struct MapView {
     int M, N, n, cap, map, nw;
@@ -102,19 +113,30 @@ struct MapView {
     int fs, ps;     // strides of fr (= n) and rp (<= 8, 0xFFFF padded)
 };
 
-// the warp's search state: shared arrays + register scalars
+// the warp's search state: its shared region + register scalars
+template <class C>
 struct WS {
-    uint8_t* rs;
-    uint32_t* rsw;
-    uint8_t* fst;
-    uint32_t* open;
-    uint32_t* b1;
-    uint32_t* inb;
-    uint32_t* late;
-    uint16_t* trail;
-    uint2* frames;      // .x = ridge | pos << 16, .y = cur | cm << 16 (cm: trail length before cur)
-    uint16_t* scratch;
+    uint8_t* base;  // generic pointer to the warp's region (shared)
+    uint32_t sb;    // the same as a 32-bit shared-window address
     int size, nopen, ndead, tl, depth;
+    __device__ __forceinline__ uint8_t* rs() const { return base + C::RS; }
+    __device__ __forceinline__ uint8_t* fst() const { return base + C::FST; }
+    __device__ __forceinline__ uint32_t* open() const { return reinterpret_cast<uint32_t*>(base + C::OPEN); }
+    __device__ __forceinline__ uint32_t* b1() const { return reinterpret_cast<uint32_t*>(base + C::B1); }
+    __device__ __forceinline__ uint32_t* inb() const { return reinterpret_cast<uint32_t*>(base + C::INB); }
+    __device__ __forceinline__ uint32_t* late() const { return reinterpret_cast<uint32_t*>(base + C::LATE); }
+    __device__ __forceinline__ uint16_t* trail() const { return reinterpret_cast<uint16_t*>(base + C::TRAIL); }
+    __device__ __forceinline__ uint2* frames() const { return reinterpret_cast<uint2*>(base + C::FRAMES); }
+    __device__ __forceinline__ uint16_t* scratch() const { return reinterpret_cast<uint16_t*>(base + C::SCRATCH); }
+    // shared-window addresses for the PTX helpers
+    __device__ __forceinline__ uint32_t a_rs_word(int r) const { return sb + C::RS + (r & ~3); }
+    __device__ __forceinline__ uint32_t a_rs(int r) const { return sb + C::RS + r; }
+    __device__ __forceinline__ uint32_t a_fst(int f) const { return sb + C::FST + f; }
+    __device__ __forceinline__ uint32_t a_open(int r) const { return sb + C::OPEN + ((r >> 5) << 2); }
+    __device__ __forceinline__ uint32_t a_b1(int r) const { return sb + C::B1 + ((r >> 5) << 2); }
+    __device__ __forceinline__ uint32_t a_inb(int f) const { return sb + C::INB + ((f >> 5) << 2); }
+    __device__ __forceinline__ uint32_t a_trail(int e) const { return sb + C::TRAIL + 2 * e; }
+    __device__ __forceinline__ uint32_t a_scratch(int j) const { return sb + C::SCRATCH + 2 * j; }
 };
 
 __device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) - 1u; }
@@ -122,42 +144,39 @@ __device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) 
 // Predicated shared-memory updates: one instruction each, no branch, so the
 // warp never diverges around them (a C++ `if (cond) atomicXor(...)` costs a
 // BSSY/BSYNC pair plus BRA.DIV guards before the next warp intrinsic).
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void red_xor_if(uint32_t* p, uint32_t v, bool pred) {
-    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.shared.xor.b32 [%0], %1; }" ::"r"(smem_addr(p)),
-                 "r"(v), "r"((uint32_t)pred)
+__device__ __forceinline__ void red_xor_if(uint32_t a, uint32_t v, bool pred) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.shared.xor.b32 [%0], %1; }" ::"r"(a), "r"(v),
+                 "r"((uint32_t)pred)
                  : "memory");
 }
-__device__ __forceinline__ void red_and_if(uint32_t* p, uint32_t v, bool pred) {
-    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.shared.and.b32 [%0], %1; }" ::"r"(smem_addr(p)),
-                 "r"(v), "r"((uint32_t)pred)
+__device__ __forceinline__ void red_and_if(uint32_t a, uint32_t v, bool pred) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.shared.and.b32 [%0], %1; }" ::"r"(a), "r"(v),
+                 "r"((uint32_t)pred)
                  : "memory");
 }
-__device__ __forceinline__ void red_or_if(uint32_t* p, uint32_t v, bool pred) {
-    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.shared.or.b32 [%0], %1; }" ::"r"(smem_addr(p)),
-                 "r"(v), "r"((uint32_t)pred)
+__device__ __forceinline__ void red_or_if(uint32_t a, uint32_t v, bool pred) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.shared.or.b32 [%0], %1; }" ::"r"(a), "r"(v),
+                 "r"((uint32_t)pred)
                  : "memory");
 }
-__device__ __forceinline__ void st_u8_if(uint8_t* p, uint32_t v, bool pred) {
-    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u8 [%0], %1; }" ::"r"(smem_addr(p)), "r"(v),
+__device__ __forceinline__ void st_u8_if(uint32_t a, uint32_t v, bool pred) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u8 [%0], %1; }" ::"r"(a), "r"(v),
+                 "r"((uint32_t)pred)
+                 : "memory");
+}
+__device__ __forceinline__ void st_u16_if(uint32_t a, uint32_t v, bool pred) {
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u16 [%0], %1; }" ::"r"(a), "r"(v),
                  "r"((uint32_t)pred)
                  : "memory");
 }
 // predicated shared atomic add returning the old word (0 when not executed)
-__device__ __forceinline__ uint32_t atom_add_if(uint32_t* p, uint32_t v, bool pred) {
+__device__ __forceinline__ uint32_t atom_add_if(uint32_t a, uint32_t v, bool pred) {
     uint32_t old = 0;
     asm volatile("{ .reg .pred q; setp.ne.u32 q, %3, 0; @q atom.shared.add.u32 %0, [%1], %2; }"
                  : "+r"(old)
-                 : "r"(smem_addr(p)), "r"(v), "r"((uint32_t)pred)
+                 : "r"(a), "r"(v), "r"((uint32_t)pred)
                  : "memory");
     return old;
-}
-__device__ __forceinline__ void st_u16_if(uint16_t* p, uint32_t v, bool pred) {
-    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.shared.u16 [%0], %1; }" ::"r"(smem_addr(p)), "r"(v),
-                 "r"((uint32_t)pred)
-                 : "memory");
 }
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
@@ -171,30 +190,32 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 // open: c == 1.  b1: c == 1 && a == 1.  dead: c == 1 && a == 0.
 
 // a -= 1 on every ridge of the facets trail[lo..hi) (already marked OUT)
-__device__ __forceinline__ void apply_exclusions(WS& w, const MapView& mp, int lo, int hi, int lane) {
+template <class C>
+__device__ __forceinline__ void apply_exclusions(WS<C>& w, const MapView& mp, int lo, int hi, int lane) {
     const int sh_l = mp.lpf_shift, k = lane & ((1 << sh_l) - 1), per = 32 >> sh_l;
     for (int e0 = lo; e0 < hi; e0 += per) {
         const int e = e0 + (lane >> sh_l);
         const bool act = e < hi && k < mp.n;
-        const int g = act ? (w.trail[e] & 0x7FFF) : 0;
+        const int g = act ? (w.trail()[e] & 0x7FFF) : 0;
         const int r = act ? __ldg(mp.fr + g * mp.fs + k) : 0;
         const unsigned sh = (r & 3) * 8;
-        const unsigned ob = (atom_add_if(w.rsw + (r >> 2), 0u - (4u << sh), act) >> sh) & 0xFFu;
+        const unsigned ob = (atom_add_if(w.a_rs_word(r), 0u - (4u << sh), act) >> sh) & 0xFFu;
         // (1,1) -> (1,0): dead and leaves the forced set; (1,2) -> (1,1): enters it
-        red_xor_if(w.b1 + (r >> 5), 1u << (r & 31), act && (ob == 5u || ob == 9u));
+        red_xor_if(w.a_b1(r), 1u << (r & 31), act && (ob == 5u || ob == 9u));
         w.ndead += __popc(__ballot_sync(FULL, act && ob == 5u));
     }
 }
 
 // exclude one facet (a tried sibling)
-__device__ __forceinline__ void exclude_one(WS& w, const MapView& mp, int g, int lane) {
-    st_u8_if(w.fst + g, FOUT, lane == 0);
-    st_u16_if(w.trail + w.tl, (uint32_t)g, lane == 0);
+template <class C>
+__device__ __forceinline__ void exclude_one(WS<C>& w, const MapView& mp, int g, int lane) {
+    st_u8_if(w.a_fst(g), FOUT, lane == 0);
+    st_u16_if(w.a_trail(w.tl), (uint32_t)g, lane == 0);
     const bool act = lane < mp.n;
     const int r = act ? __ldg(mp.fr + g * mp.fs + lane) : 0;
     const unsigned sh = (r & 3) * 8;
-    const unsigned ob = (atom_add_if(w.rsw + (r >> 2), 0u - (4u << sh), act) >> sh) & 0xFFu;
-    red_xor_if(w.b1 + (r >> 5), 1u << (r & 31), act && (ob == 5u || ob == 9u));
+    const unsigned ob = (atom_add_if(w.a_rs_word(r), 0u - (4u << sh), act) >> sh) & 0xFFu;
+    red_xor_if(w.a_b1(r), 1u << (r & 31), act && (ob == 5u || ob == 9u));
     w.ndead += __popc(__ballot_sync(FULL, act && ob == 5u));
     w.tl += 1;
     __syncwarp();
@@ -211,44 +232,38 @@ struct Probe {
     bool dead;
 };
 
-__device__ __forceinline__ Probe probe_facet(const WS& w, const MapView& mp, int f, int lane) {
+template <class C>
+__device__ __forceinline__ Probe probe_facet(const WS<C>& w, const MapView& mp, int f, int lane) {
     Probe pr{0, 4u, false};
-#ifdef WPM_TRAPS
-    if (f < 0 || f >= mp.M) {
-        if (lane == 0)
-            printf("WPM_TRAP probe f=%d M=%d nopen=%d ndead=%d size=%d tl=%d depth=%d\n", f, mp.M, w.nopen, w.ndead,
-                   w.size, w.tl, w.depth);
-        __trap();
-    }
-#endif
     if (lane < mp.n) {
         pr.r = __ldg(mp.fr + f * mp.fs + lane);
-        pr.b = w.rs[pr.r];
+        pr.b = w.rs()[pr.r];
     }
     pr.dead = __any_sync(FULL, pr.b == (1u << 2) && lane < mp.n);
     return pr;
 }
 
-__device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, const Probe& pr, int lane) {
+template <class C>
+__device__ __forceinline__ void include_facet(WS<C>& w, const MapView& mp, int f, const Probe& pr, int lane) {
     const bool act = lane < mp.n;
     const int r = pr.r;
     const unsigned b = pr.b;
-    const unsigned c = b & 3u, a = b >> 2;   // c in {0,1}, a >= 1 (f is undecided)
+    const unsigned c = b & 3u;               // c in {0,1}, a >= 1 (f is undecided)
     const bool closed = act && c == 1u;
     // branch-free: every lane k < n updates its ridge (c + 1, a - 1); the open
     // bit always flips (0 -> 1 opens, 1 -> 2 closes); the forced bit flips on
     // (1,1) -> (2,0) and (0,2) -> (1,1).  Opening with a = 0 cannot happen:
     // probe_facet filtered those includes.
     const unsigned bit = 1u << (r & 31);
-    st_u8_if(w.rs + r, b + 1u - 4u, act);
-    red_xor_if(w.open + (r >> 5), bit, act);
-    red_xor_if(w.b1 + (r >> 5), bit, act && (b == 5u || b == 8u));
+    st_u8_if(w.a_rs(r), b + 1u - 4u, act);
+    red_xor_if(w.a_open(r), bit, act);
+    red_xor_if(w.a_b1(r), bit, act && (b == 5u || b == 8u));
     const unsigned bc = __ballot_sync(FULL, closed);
     w.nopen += mp.n - 2 * __popc(bc);
-    st_u16_if(w.scratch + __popc(bc & lanemask_lt(lane)), (uint32_t)r, closed);
-    st_u8_if(w.fst + f, FIN, lane == 0);
-    red_or_if(w.inb + (f >> 5), 1u << (f & 31), lane == 0);
-    st_u16_if(w.trail + w.tl, (uint32_t)(f | TR_INC), lane == 0);
+    st_u16_if(w.a_scratch(__popc(bc & lanemask_lt(lane))), (uint32_t)r, closed);
+    st_u8_if(w.a_fst(f), FIN, lane == 0);
+    red_or_if(w.a_inb(f), 1u << (f & 31), lane == 0);
+    st_u16_if(w.a_trail(w.tl), (uint32_t)(f | TR_INC), lane == 0);
     w.tl += 1;
     w.size += 1;
     __syncwarp();
@@ -261,13 +276,13 @@ __device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, c
     for (int j0 = 0; j0 < ncl; j0 += 4) {
         const int j = j0 + (lane >> 3), q = lane & 7;
         const bool slot = j < ncl && q < mp.ps;
-        const int rr = w.scratch[j & 31];
+        const int rr = w.scratch()[j & 31];
         const int g0 = slot ? (int)__ldg(mp.rp + rr * mp.ps + q) : (int)NONE16;
         const int g = g0 == NONE16 ? 0 : g0;
-        const bool v = g0 != NONE16 && w.fst[g] == FU;
+        const bool v = g0 != NONE16 && w.fst()[g] == FU;
         const unsigned bv = __ballot_sync(FULL, v);
-        st_u16_if(w.trail + base + E + __popc(bv & lanemask_lt(lane)), (uint32_t)g, v);
-        st_u8_if(w.fst + g, FOUT, v);
+        st_u16_if(w.a_trail(base + E + __popc(bv & lanemask_lt(lane))), (uint32_t)g, v);
+        st_u8_if(w.a_fst(g), FOUT, v);
         E += __popc(bv);
     }
     if (E) {
@@ -285,36 +300,37 @@ __device__ __forceinline__ void include_facet(WS& w, const MapView& mp, int f, c
 // applied with shared atomics; each atomic returns the exact old byte, so the
 // open / forced / dead transitions it reports are exact and their sum
 // telescopes to the right totals and bitsets whatever the interleaving.
-__device__ __forceinline__ void undo_to(WS& w, const MapView& mp, int mark, int lane) {
+template <class C>
+__device__ __forceinline__ void undo_to(WS<C>& w, const MapView& mp, int mark, int lane) {
     const int lo = mark, hi = w.tl;
     if (hi <= lo) return;
     for (int e0 = lo; e0 < hi; e0 += 32) {
         const int e = e0 + lane;
         const bool act = e < hi;
-        const unsigned t = act ? (unsigned)w.trail[e] : 0u;
+        const unsigned t = act ? (unsigned)w.trail()[e] : 0u;
         const int g = (int)(t & 0x7FFFu);
         const bool inc = act && (t & TR_INC);
-        st_u8_if(w.fst + g, FU, act);
-        red_and_if(w.inb + (g >> 5), ~(1u << (g & 31)), inc);
+        st_u8_if(w.a_fst(g), FU, act);
+        red_and_if(w.a_inb(g), ~(1u << (g & 31)), inc);
         w.size -= __popc(__ballot_sync(FULL, inc));
     }
     const int sh_l = mp.lpf_shift, k = lane & ((1 << sh_l) - 1), per = 32 >> sh_l;
     for (int e0 = lo; e0 < hi; e0 += per) {
         const int e = e0 + (lane >> sh_l);
         const bool act = e < hi && k < mp.n;
-        const unsigned t = act ? (unsigned)w.trail[e] : 0u;
+        const unsigned t = act ? (unsigned)w.trail()[e] : 0u;
         const int g = (int)(t & 0x7FFFu);
         const int r = act ? __ldg(mp.fr + g * mp.fs + k) : 0;
         const unsigned delta = (t & TR_INC) ? 3u : 4u;  // (c-1, a+1) or (a+1)
         const unsigned sh = (r & 3) * 8;
-        const unsigned ob = (atom_add_if(w.rsw + (r >> 2), delta << sh, act) >> sh) & 0xFFu;
+        const unsigned ob = (atom_add_if(w.a_rs_word(r), delta << sh, act) >> sh) & 0xFFu;
         const unsigned nb = ob + delta;
         const bool o0 = act && (ob & 3u) == 1u, o1 = act && (nb & 3u) == 1u;
-        const bool f0 = ob == 5u, f1 = nb == 5u;            // (1,1): forced
+        const bool f0 = ob == 5u, f1 = nb == 5u;                // (1,1): forced
         const bool z0 = act && ob == 1u, z1 = act && nb == 1u;  // (1,0): dead
         const unsigned bit = 1u << (r & 31);
-        red_xor_if(w.open + (r >> 5), bit, o0 != o1);
-        red_xor_if(w.b1 + (r >> 5), bit, act && f0 != f1);
+        red_xor_if(w.a_open(r), bit, o0 != o1);
+        red_xor_if(w.a_b1(r), bit, act && f0 != f1);
         w.nopen += __popc(__ballot_sync(FULL, o1 && !o0)) - __popc(__ballot_sync(FULL, o0 && !o1));
         w.ndead += __popc(__ballot_sync(FULL, z1 && !z0)) - __popc(__ballot_sync(FULL, z0 && !z1));
     }
@@ -326,7 +342,8 @@ __device__ __forceinline__ void undo_to(WS& w, const MapView& mp, int mark, int 
 // Debug builds: recompute every derived quantity from the facet statuses and
 // trap on the first mismatch (counts, open / forced bitsets, open / dead
 // tallies, IN bitset, size).
-__device__ void debug_check(const WS& w, const MapView& mp, int lane, int where) {
+template <class C>
+__device__ void debug_check(const WS<C>& w, const MapView& mp, int lane, int where) {
     __syncwarp();
     int bad = 0, nopen = 0, ndead = 0, size = 0;
     for (int r = lane; r < mp.N; r += 32) {
@@ -334,21 +351,22 @@ __device__ void debug_check(const WS& w, const MapView& mp, int lane, int where)
         for (int q = 0; q < mp.ps; ++q) {
             const int g = __ldg(mp.rp + r * mp.ps + q);
             if (g == NONE16) continue;
-            c += w.fst[g] == FIN;
-            a += w.fst[g] == FU;
+            c += w.fst()[g] == FIN;
+            a += w.fst()[g] == FU;
         }
-        const unsigned b = w.rs[r];
+        const unsigned b = w.rs()[r];
         if (b != (c | (a << 2))) bad |= 1;
         const bool op = c == 1, f1 = c == 1 && a == 1;
-        if (((w.open[r >> 5] >> (r & 31)) & 1u) != (unsigned)op) bad |= 2;
-        if (((w.b1[r >> 5] >> (r & 31)) & 1u) != (unsigned)f1) bad |= 4;
+        if (((w.open()[r >> 5] >> (r & 31)) & 1u) != (unsigned)op) bad |= 2;
+        if (((w.b1()[r >> 5] >> (r & 31)) & 1u) != (unsigned)f1) bad |= 4;
         nopen += op;
         ndead += op && a == 0;
     }
     for (int f = lane; f < mp.M; f += 32) {
-        size += w.fst[f] == FIN;
-        if (((w.inb[f >> 5] >> (f & 31)) & 1u) != (unsigned)(w.fst[f] == FIN)) bad |= 8;
+        size += w.fst()[f] == FIN;
+        if (((w.inb()[f >> 5] >> (f & 31)) & 1u) != (unsigned)(w.fst()[f] == FIN)) bad |= 8;
     }
+    __syncwarp();
     nopen = (int)__reduce_add_sync(FULL, (unsigned)nopen);
     ndead = (int)__reduce_add_sync(FULL, (unsigned)ndead);
     size = (int)__reduce_add_sync(FULL, (unsigned)size);
@@ -370,9 +388,10 @@ __device__ void debug_check(const WS& w, const MapView& mp, int lane, int where)
 
 // MRV branch ridge: the lowest open ridge with one undecided candidate, else
 // the open ridge with the fewest (ties: lowest id).  Returns ridge | a << 16.
-__device__ __forceinline__ unsigned select_ridge(const WS& w, int nw, int lane) {
+template <class C>
+__device__ __forceinline__ unsigned select_ridge(const WS<C>& w, int nw, int lane) {
     for (int i0 = 0; i0 < nw; i0 += 32) {
-        const unsigned word = (i0 + lane < nw) ? w.b1[i0 + lane] : 0u;
+        const unsigned word = (i0 + lane < nw) ? w.b1()[i0 + lane] : 0u;
         const unsigned bw = __ballot_sync(FULL, word != 0u);
         if (bw) {
             const int l = __ffs(bw) - 1;
@@ -382,11 +401,11 @@ __device__ __forceinline__ unsigned select_ridge(const WS& w, int nw, int lane) 
     }
     unsigned best = 0xFFFFFFFFu;
     for (int i = lane; i < nw; i += 32) {
-        unsigned bits = w.open[i];
+        unsigned bits = w.open()[i];
         while (bits) {
             const int r = i * 32 + __ffs(bits) - 1;
             bits &= bits - 1u;
-            best = min(best, ((unsigned)(w.rs[r] >> 2) << 16) | (unsigned)r);
+            best = min(best, ((unsigned)(w.rs()[r] >> 2) << 16) | (unsigned)r);
         }
     }
     __syncwarp();  // reconverge after the divergent scan before the CREDUX
@@ -394,12 +413,13 @@ __device__ __forceinline__ unsigned select_ridge(const WS& w, int nw, int lane) 
 }
 
 // the undecided candidates of an OPEN frame's ridge from slot pos: first one
-__device__ __forceinline__ int first_candidate(const WS& w, const MapView& mp, int ridge, int pos, int* slot,
+template <class C>
+__device__ __forceinline__ int first_candidate(const WS<C>& w, const MapView& mp, int ridge, int pos, int* slot,
                                                int lane) {
     const bool in_range = lane >= pos && lane < mp.ps;
     const int g0 = in_range ? (int)__ldg(mp.rp + ridge * mp.ps + lane) : (int)NONE16;
     const int g = g0 == NONE16 ? 0 : g0;
-    const bool ok = g0 != NONE16 && w.fst[g] == FU;
+    const bool ok = g0 != NONE16 && w.fst()[g] == FU;
     const unsigned b = __ballot_sync(FULL, ok);
     if (!b) return -1;
     const int q = __ffs(b) - 1;
@@ -408,13 +428,14 @@ __device__ __forceinline__ int first_candidate(const WS& w, const MapView& mp, i
 }
 
 // next undecided child of a frame from its pos; -1 if none
-__device__ __forceinline__ int next_child(const WS& w, const MapView& mp, uint2 fr, int* new_pos, int lane) {
+template <class C>
+__device__ __forceinline__ int next_child(const WS<C>& w, const MapView& mp, uint2 fr, int* new_pos, int lane) {
     const uint32_t ridge = fr.x & 0xFFFFu, pos = fr.x >> 16;
     if (pos == POS_DONE) return -1;
     if (ridge == CLOSED_FRAME) {
         for (int p0 = (int)pos; p0 < mp.M; p0 += 32) {
             const int f = p0 + lane;
-            const unsigned b = __ballot_sync(FULL, f < mp.M && w.fst[f] == FU);
+            const unsigned b = __ballot_sync(FULL, f < mp.M && w.fst()[f] == FU);
             if (b) {
                 const int c = p0 + __ffs(b) - 1;
                 *new_pos = c + 1;
@@ -431,14 +452,15 @@ __device__ __forceinline__ int next_child(const WS& w, const MapView& mp, uint2 
 
 // --------------------------------------------------------------- the search
 
-__device__ __forceinline__ void emit(const WS& w, const MapView& mp, const SearchParams& p, int lane) {
+template <class C>
+__device__ __forceinline__ void emit(const WS<C>& w, const MapView& mp, const SearchParams& p, int lane) {
     unsigned long long slot = 0;
     if (lane == 0) slot = atomicAdd(&p.out_ctl[0], 1ull);
     slot = __shfl_sync(FULL, slot, 0);
     if (slot < p.out_cap) {  // key row: bitset words, zero padded, then the map id
         uint32_t* o = p.out_keys + slot * (unsigned long long)p.rw;
         const int mw = (mp.M + 31) >> 5, last = p.rw - 1;
-        for (int i = lane; i < p.rw; i += 32) o[i] = i < mw ? w.inb[i] : (i == last ? (uint32_t)mp.map : 0u);
+        for (int i = lane; i < p.rw; i += 32) o[i] = i < mw ? w.inb()[i] : (i == last ? (uint32_t)mp.map : 0u);
     }
 }
 
@@ -446,7 +468,8 @@ __device__ __forceinline__ void emit(const WS& w, const MapView& mp, const Searc
 // entry): emit / prune, follow forced moves as a chain of includes, stop at
 // the next real branch point by pushing its frame.  Returns true if a frame
 // was pushed; false if the descent ended (dead, pruned, or a leaf).
-__device__ __forceinline__ bool descend(WS& w, const MapView& mp, const SearchParams& p, unsigned long long& nodes,
+template <class C>
+__device__ __forceinline__ bool descend(WS<C>& w, const MapView& mp, const SearchParams& p, unsigned long long& nodes,
                                         int lane) {
     for (;;) {
         if (w.ndead) return false;
@@ -471,14 +494,14 @@ __device__ __forceinline__ bool descend(WS& w, const MapView& mp, const SearchPa
                 continue;
             }
         }
-        if (w.depth >= p.max_depth) {
-            // frame stack full (the launch sized it below the worst case to
-            // fit more warps): flag the run as incomplete; the host discards
-            // it and reruns with the full-depth layout
+        if (w.depth >= C::kDepth) {
+            // frame stack full (the fast layouts hold FRAME_CAP frames): flag the
+            // run as incomplete; the host discards it and reruns with the
+            // full-depth layout
             if (lane == 0) atomicExch(&p.out_ctl[2], 1ull);
             return false;
         }
-        if (lane == 0) w.frames[w.depth] = make_uint2(ridge, NO_CHILD);
+        if (lane == 0) w.frames()[w.depth] = make_uint2(ridge, NO_CHILD);
         w.depth += 1;
         __syncwarp();
         return true;
@@ -487,22 +510,23 @@ __device__ __forceinline__ bool descend(WS& w, const MapView& mp, const SearchPa
 
 // rebuild the warp state from an IN/OUT record (+ closure: a ridge with two
 // IN candidates excludes the rest).  Returns false if infeasible.
-__device__ __forceinline__ bool load_state(WS& w, const MapView& mp, const uint32_t* rec_in, const uint32_t* rec_out,
-                                           bool closure, int lane) {
+template <class C>
+__device__ __forceinline__ bool load_state(WS<C>& w, const MapView& mp, const uint32_t* rec_in,
+                                           const uint32_t* rec_out, bool closure, int lane) {
     const int M = mp.M, N = mp.N, mw = (M + 31) >> 5, nw = mp.nw;
+    uint8_t* rs = w.rs();
+    uint8_t* fst = w.fst();
     int size = 0;
     for (int i = lane; i < mw; i += 32) {
         const uint32_t iv = __ldcg(rec_in + i);
-        w.inb[i] = iv;
+        w.inb()[i] = iv;
         size += __popc(iv);
     }
     for (int f0 = 0; f0 < M; f0 += 32) {
         const int f = f0 + lane;
         const uint32_t iv = __ldcg(rec_in + (f0 >> 5)), ov = __ldcg(rec_out + (f0 >> 5));
         const uint32_t bit = 1u << lane;
-        if (f < M) {
-            w.fst[f] = (iv & bit) ? FIN : ((ov & bit) ? FOUT : FU);
-        }
+        if (f < M) fst[f] = (iv & bit) ? FIN : ((ov & bit) ? FOUT : FU);
     }
     __syncwarp();  // reconverge after the divergent loops before the CREDUX
     w.size = (int)__reduce_add_sync(FULL, (unsigned)size);
@@ -514,19 +538,19 @@ __device__ __forceinline__ bool load_state(WS& w, const MapView& mp, const uint3
             unsigned c = 0;
             for (int q = 0; q < mp.ps; ++q) {
                 const int g = __ldg(mp.rp + r * mp.ps + q);
-                c += g != NONE16 && w.fst[g] == FIN;
+                c += g != NONE16 && fst[g] == FIN;
             }
             bad |= c > 2u;
-            w.rs[r] = (uint8_t)min(c, 2u);
+            rs[r] = (uint8_t)min(c, 2u);
         }
         if (__any_sync(FULL, bad)) return false;
         __syncwarp();
         // closure: undecided facets on a closed ridge are excluded
         for (int f = lane; f < M; f += 32) {
-            if (w.fst[f] != FU) continue;
+            if (fst[f] != FU) continue;
             bool on_closed = false;
-            for (int k = 0; k < mp.n; ++k) on_closed |= w.rs[__ldg(mp.fr + f * mp.fs + k)] == 2u;
-            if (on_closed) w.fst[f] = FOUT;
+            for (int k = 0; k < mp.n; ++k) on_closed |= rs[__ldg(mp.fr + f * mp.fs + k)] == 2u;
+            if (on_closed) fst[f] = FOUT;
         }
         __syncwarp();
     }
@@ -540,20 +564,20 @@ __device__ __forceinline__ bool load_state(WS& w, const MapView& mp, const uint3
             unsigned a = 0, ci = 0;
             for (int q = 0; q < mp.ps; ++q) {
                 const int g0 = __ldg(mp.rp + r * mp.ps + q);
-                const unsigned s = g0 != NONE16 ? w.fst[g0] : (unsigned)FOUT;
+                const unsigned s = g0 != NONE16 ? fst[g0] : (unsigned)FOUT;
                 a += s == FU;
                 ci += s == FIN;
             }
-            const unsigned c = closure ? (unsigned)w.rs[r] : ci;
-            w.rs[r] = (uint8_t)(c | (a << 2));
+            const unsigned c = closure ? (unsigned)rs[r] : ci;
+            rs[r] = (uint8_t)(c | (a << 2));
             op = c == 1u;
             dd = op && a == 0u;
             one = op && a == 1u;
         }
         const unsigned bo = __ballot_sync(FULL, op), b1 = __ballot_sync(FULL, one);
         if (lane == 0) {
-            w.open[r0 >> 5] = bo;
-            w.b1[r0 >> 5] = b1;
+            w.open()[r0 >> 5] = bo;
+            w.b1()[r0 >> 5] = b1;
         }
         nopen += __popc(bo);
         ndead += __popc(__ballot_sync(FULL, dd));
@@ -569,34 +593,36 @@ __device__ __forceinline__ bool load_state(WS& w, const MapView& mp, const uint3
 // donate the shallowest frame that still has an untried child.  The
 // frame's state = the current state minus every decision on the trail at or
 // after mk (`late`), with its in-progress child excluded.
-__device__ __forceinline__ void try_donate(WS& w, const MapView& mp, const SearchParams& p, int lane) {
+template <class C>
+__device__ __forceinline__ void try_donate(WS<C>& w, const MapView& mp, const SearchParams& p, int lane) {
     const int M = mp.M, mw = (M + 31) >> 5;
+    uint32_t* late = w.late();
+    const uint8_t* fst = w.fst();
     for (int d = 0; d < w.depth; ++d) {
-        const uint2 fr = w.frames[d];
+        const uint2 fr = w.frames()[d];
         const uint32_t ridge = fr.x & 0xFFFFu, pos = fr.x >> 16;
         if (pos == POS_DONE) continue;
         const bool busy = (fr.y & 0xFFFFu) != NO_CHILD && d + 1 < w.depth;
         const int mk = busy ? (int)(fr.y >> 16) : w.tl;  // the frame's own state
         const int cur = busy ? (int)(fr.y & 0xFFFFu) : -1;
-        for (int i = lane; i < mw; i += 32) w.late[i] = 0u;
+        for (int i = lane; i < mw; i += 32) late[i] = 0u;
         __syncwarp();
         for (int e = mk + lane; e < w.tl; e += 32) {
-            const int g = w.trail[e] & 0x7FFF;
-            atomicOr(&w.late[g >> 5], 1u << (g & 31));
+            const int g = w.trail()[e] & 0x7FFF;
+            atomicOr(&late[g >> 5], 1u << (g & 31));
         }
         __syncwarp();
         bool any = false;
         if (ridge == CLOSED_FRAME) {
             for (int f0 = (int)pos; f0 < M && !any; f0 += 32) {
                 const int f = f0 + lane;
-                any = __any_sync(FULL, f < M && f != cur &&
-                                           (w.fst[f] == FU || ((w.late[f >> 5] >> (f & 31)) & 1u)));
+                any = __any_sync(FULL, f < M && f != cur && (fst[f] == FU || ((late[f >> 5] >> (f & 31)) & 1u)));
             }
         } else {
             bool ok = false;
             if (lane >= (int)pos && lane < mp.ps) {
                 const int g = __ldg(mp.rp + ridge * mp.ps + lane);
-                ok = g != NONE16 && g != cur && (w.fst[g] == FU || ((w.late[g >> 5] >> (g & 31)) & 1u));
+                ok = g != NONE16 && g != cur && (fst[g] == FU || ((late[g >> 5] >> (g & 31)) & 1u));
             }
             any = __any_sync(FULL, ok);
         }
@@ -619,8 +645,8 @@ __device__ __forceinline__ void try_donate(WS& w, const MapView& mp, const Searc
             const int f = f0 + lane;
             bool in = false, out = false;
             if (f < M) {
-                const uint8_t s = w.fst[f];
-                const bool before = !((w.late[f >> 5] >> (f & 31)) & 1u);
+                const uint8_t s = fst[f];
+                const bool before = !((late[f >> 5] >> (f & 31)) & 1u);
                 in = s == FIN && before;
                 out = (s == FOUT && before) || f == cur;
             }
@@ -634,32 +660,20 @@ __device__ __forceinline__ void try_donate(WS& w, const MapView& mp, const Searc
         __syncwarp();
         if (lane == 0) {
             atomicExch(&p.qready[t % (unsigned long long)p.qcap], t + 1ull);
-            w.frames[d].x = ridge | (POS_DONE << 16);  // exhausted here
+            w.frames()[d].x = ridge | (POS_DONE << 16);  // exhausted here
         }
         __syncwarp();
         return;
     }
 }
 
-#ifndef K3_MIN_BLOCKS
-#define K3_MIN_BLOCKS 8  // 32 warps/SM: the register budget that measured fastest
-#endif
-__global__ void __launch_bounds__(128, K3_MIN_BLOCKS) k3_search(const __grid_constant__ SearchParams p,
-                                                 const __grid_constant__ Layout L) {
+template <class C>
+__global__ void __launch_bounds__(128, 8) k3_search(const __grid_constant__ SearchParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint8_t* base = smem + wid * L.bytes;
-    WS w;
-    w.rs = base + L.rs;
-    w.rsw = reinterpret_cast<uint32_t*>(base + L.rs);
-    w.fst = base + L.fst;
-    w.late = reinterpret_cast<uint32_t*>(base + L.late);
-    w.open = reinterpret_cast<uint32_t*>(base + L.open);
-    w.b1 = reinterpret_cast<uint32_t*>(base + L.b1);
-    w.inb = reinterpret_cast<uint32_t*>(base + L.inb);
-    w.trail = reinterpret_cast<uint16_t*>(base + L.trail);
-    w.frames = reinterpret_cast<uint2*>(base + L.frames);
-    w.scratch = reinterpret_cast<uint16_t*>(base + L.scratch);
+    WS<C> w;
+    w.base = smem + wid * C::BYTES;
+    w.sb = static_cast<uint32_t>(__cvta_generic_to_shared(w.base));
     unsigned long long nodes = 0, tasks = 0;
 
     for (;;) {
@@ -726,7 +740,8 @@ __global__ void __launch_bounds__(128, K3_MIN_BLOCKS) k3_search(const __grid_con
                 descend(w, mp, p, nodes, lane);
             } else if (w.ndead == 0) {  // resume a donated frame
                 if (lane == 0)
-                    w.frames[0] = make_uint2((kind == T_CLOSED ? CLOSED_FRAME : h1) | ((h2 & 0xFFFFu) << 16), NO_CHILD);
+                    w.frames()[0] =
+                        make_uint2((kind == T_CLOSED ? CLOSED_FRAME : h1) | ((h2 & 0xFFFFu) << 16), NO_CHILD);
                 w.depth = 1;
                 __syncwarp();
             }
@@ -735,7 +750,7 @@ __global__ void __launch_bounds__(128, K3_MIN_BLOCKS) k3_search(const __grid_con
         unsigned long long qword = ld_relaxed_u64(&p.qctl[0]);  // prefetched queue state
         unsigned long long next_check = nodes + CHECK_EVERY;
         while (w.depth > 0) {
-            const uint2 fr = w.frames[w.depth - 1];
+            const uint2 fr = w.frames()[w.depth - 1];
             int npos = 0;
             const int c = next_child(w, mp, fr, &npos, lane);
             if (c < 0) {
@@ -743,21 +758,22 @@ __global__ void __launch_bounds__(128, K3_MIN_BLOCKS) k3_search(const __grid_con
                 // current child, then exclude that child there
                 w.depth -= 1;
                 if (w.depth > 0) {
-                    const uint2 pf = w.frames[w.depth - 1];
+                    const uint2 pf = w.frames()[w.depth - 1];
                     undo_to(w, mp, (int)(pf.y >> 16), lane);
                     DEBUG_CHECK(w, mp, lane, 3);
                     exclude_one(w, mp, (int)(pf.y & 0xFFFFu), lane);
                     DEBUG_CHECK(w, mp, lane, 4);
                     if ((pf.x & 0xFFFFu) != CLOSED_FRAME && w.ndead) {
-                        if (lane == 0) w.frames[w.depth - 1].x = (pf.x & 0xFFFFu) | (POS_DONE << 16);
+                        if (lane == 0) w.frames()[w.depth - 1].x = (pf.x & 0xFFFFu) | (POS_DONE << 16);
                         __syncwarp();
                     }
                 }
                 continue;
             }
             const int cm = w.tl;
-            if (lane == 0) w.frames[w.depth - 1] = make_uint2((fr.x & 0xFFFFu) | ((uint32_t)npos << 16),
-                                                              (uint32_t)c | ((uint32_t)cm << 16));
+            if (lane == 0)
+                w.frames()[w.depth - 1] =
+                    make_uint2((fr.x & 0xFFFFu) | ((uint32_t)npos << 16), (uint32_t)c | ((uint32_t)cm << 16));
             __syncwarp();
             const Probe pr = probe_facet(w, mp, c, lane);
             ++nodes;
@@ -773,7 +789,7 @@ __global__ void __launch_bounds__(128, K3_MIN_BLOCKS) k3_search(const __grid_con
                 exclude_one(w, mp, c, lane);
                 DEBUG_CHECK(w, mp, lane, 7);
                 if ((fr.x & 0xFFFFu) != CLOSED_FRAME && w.ndead) {
-                    if (lane == 0) w.frames[w.depth - 1].x = (fr.x & 0xFFFFu) | (POS_DONE << 16);
+                    if (lane == 0) w.frames()[w.depth - 1].x = (fr.x & 0xFFFFu) | (POS_DONE << 16);
                     __syncwarp();
                 }
             }
@@ -824,6 +840,24 @@ __global__ void seed_tasks(SearchParams p, int ntasks, const int32_t* __restrict
     if (lane == 0) p.qready[t] = (unsigned long long)t + 1ull;
 }
 
+template <class C>
+int launch_class(const SearchParams& p, int num_sms, cudaStream_t st, int* warps_out) {
+    const int wpb = 4;  // warps per CTA
+    const size_t smem = (size_t)C::BYTES * wpb;
+    if (cudaFuncSetAttribute(k3_search<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return 0;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_search<C>, 32 * wpb, smem) != cudaSuccess ||
+        per_sm < 1)
+        return 0;
+    if (const char* e = std::getenv("WPM_BLOCKS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
+    const int grid = per_sm * num_sms;
+    k3_search<C><<<grid, 32 * wpb, smem, st>>>(p);
+    if (cudaGetLastError() != cudaSuccess) return 0;
+    if (warps_out) *warps_out = grid * wpb;
+    return grid;
+}
+
 }  // namespace
 
 int launch_seed_tasks(const SearchParams& p, int ntasks, const int32_t* d_task_map, const int32_t* d_task_f,
@@ -835,24 +869,19 @@ int launch_seed_tasks(const SearchParams& p, int ntasks, const int32_t* d_task_m
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+// the smallest size class that holds the plan (max_depth > FRAME_CAP asks for
+// the full-depth layout)
 int launch_k3_search(const SearchParams& p, int num_sms, cudaStream_t st, int* warps_out) {
-    const Layout L = make_layout(p.max_M, p.max_N, p.max_depth);
-    const int wpb = 4;  // warps per CTA
-    const size_t smem = (size_t)L.bytes * wpb;
-    if (cudaFuncSetAttribute(k3_search, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return 0;
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_search, 32 * wpb, smem) != cudaSuccess ||
-        per_sm < 1)
-        return 0;
-    if (const char* e = std::getenv("WPM_BLOCKS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
-    const int grid = per_sm * num_sms;
-    k3_search<<<grid, 32 * wpb, smem, st>>>(p, L);
-    if (cudaGetLastError() != cudaSuccess) return 0;
-    if (warps_out) *warps_out = grid * wpb;
-    return grid;
+    const int N = p.max_N, M = p.max_M;
+    if (p.max_depth > FRAME_CAP) return launch_class<CGF>(p, num_sms, st, warps_out);
+    if (N <= C5::kN && M <= C5::kM) return launch_class<C5>(p, num_sms, st, warps_out);
+    if (N <= C6::kN && M <= C6::kM) return launch_class<C6>(p, num_sms, st, warps_out);
+    if (N <= C7::kN && M <= C7::kM) return launch_class<C7>(p, num_sms, st, warps_out);
+    if (N <= C8::kN && M <= C8::kM) return launch_class<C8>(p, num_sms, st, warps_out);
+    if (N <= C9::kN && M <= C9::kM) return launch_class<C9>(p, num_sms, st, warps_out);
+    if (N <= C10::kN && M <= C10::kM) return launch_class<C10>(p, num_sms, st, warps_out);
+    if (N <= C11::kN && M <= C11::kM) return launch_class<C11>(p, num_sms, st, warps_out);
+    return launch_class<CG>(p, num_sms, st, warps_out);
 }
-
-int k3_layout_bytes(int maxM, int maxN, int maxDepth) { return make_layout(maxM, maxN, maxDepth).bytes; }
 
 }  // namespace wpm
