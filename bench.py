@@ -137,9 +137,10 @@ def reference_arm(args):
 
 
 METRIC = "search nodes/sec and wall time to enumerate all WPMs per Picard-4 dim n"
-# per step, from the ncu launch list of this command (profiles/r01_bench_n5_launches.txt):
-# seed_tasks + k3_search + iota_u32 + 13 CUB merge-sort kernels + gather_rows
-LAUNCHES_PER_STEP = 17
+# per step at n = 5, from the ncu launch list of this command
+# (profiles/r01_bench_n5_launches.txt): seed_tasks + k3_search + CUB merge sort
+# of the key rows (1 block sort + 9 partition/merge pairs) + split_rows
+LAUNCHES_PER_STEP = 22
 
 
 def _profile_summary(n):
@@ -191,6 +192,8 @@ def main():
     ap.add_argument("--n", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-n", dest="per_n", action="store_false",
+                    help="skip the n = 2..11 sweep (1 GPU only)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -264,7 +267,7 @@ def main():
     # e2e: the reference-facing one-shot C-ABI call, host buffers, all copies inside
     e2e_times = []
     h2d = d2h = 0
-    for i in range(max(2, min(args.steps, 5)) + 1):
+    for i in range(max(2, min(args.steps, 10)) + 1):
         barrier()
         t0 = time.perf_counter()
         r = wpm_orbits_oneshot(wpm, n, dev, rank, world)
@@ -296,6 +299,13 @@ def main():
                           "note": "the kernel is issue-bound: one DFS per warp has O(n) lanes of work per node; "
                                   "see profiles/r01_k3_n5_ncu.txt"}}
 
+    num_maps = plan.num_maps
+    per_n = None
+    if world == 1 and args.per_n:
+        plan.close()
+        per_n = sweep_per_n(wpm, dev, flush, g)
+        plan = None
+
     if rank == 0:
         cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(n, expect_nodes)
         line = {
@@ -303,28 +313,67 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64 (GF(2) bitsets)",
             "data": "synthetic (IDCM orbit maps, deterministic; no dataset)",
-            "config": {"workload": f"Picard 4, n={n} (m={n + 4}): all {plan.num_maps} characteristic maps, UBT cap "
-                                   "(BASELINE configs[1])", "n": n, "maps": plan.num_maps, "wpms": tot_wpms,
+            "config": {"workload": f"Picard 4, n={n} (m={n + 4}): all {num_maps} characteristic maps, UBT cap "
+                                   "(BASELINE configs[1])", "n": n, "maps": num_maps, "wpms": tot_wpms,
                        "dfs_nodes": tot_nodes, "l2": "flushed (256 MB write) between timed steps",
                        "parallelism": f"root-task shards x{world}"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "wall_ms": e2e_s * 1e3, "call": "wpm_enumerate_orbits (one-shot C-ABI)"},
+                    "wall_ms": e2e_s * 1e3, "min_ms": min(e2e_times) * 1e3, "samples_ms": [round(t * 1e3, 3) for t in e2e_times],
+                    "call": "wpm_enumerate_orbits (one-shot C-ABI)"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clocks,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
-            "gpu_launches_per_step": {"seed_tasks": 1, "k3_search": 1, "iota_u32": 1, "cub_merge_sort": 13,
-                                      "gather_rows": 1},
+            "gpu_launches_per_step": {"seed_tasks": 1, "k3_search": 1, "cub_merge_sort": 19, "split_rows": 1},
             "breakdown_ms": {"search": ms_k3, "sort": ms_sort / args.steps, "step": ms_step},
             "parity": {"wpms_expected": expect_wpms, "nodes_expected": expect_nodes,
                        "ok": tot_wpms == expect_wpms and tot_nodes == expect_nodes},
             "host_wall_s": t_host,
         }
+        if per_n is not None:
+            line["per_n"] = per_n
         print(json.dumps(line))
-    plan.close()
+    if plan is not None:
+        plan.close()
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def sweep_per_n(wpm, dev, flush, g, ns=range(2, 12), reps=3):
+    """The metric is quoted per Picard-4 dimension n: every n = 2..11 (all maps,
+    UBT cap) on this GPU -- device time of search + sort (median of `reps`
+    runs after one warm-up, L2 flushed before each) and the one-shot C-ABI
+    call with host buffers; parity of counts and nodes against the golden
+    file."""
+    import torch
+
+    rows = []
+    for n in ns:
+        with wpm.Plan.orbits(n, device=dev) as p:
+            p.run()
+            runs = []
+            for _ in range(reps):
+                flush.zero_()
+                torch.cuda.synchronize(dev)
+                p.run()
+                st, tm = p.stats(), p.timing()
+                runs.append((tm["ms_total"], st["ms_search"], st["ms_sort"], st["nodes"]))
+            total = p.fetch().total
+        runs.sort()
+        ms, ms_search, ms_sort, nodes = runs[len(runs) // 2]
+        wpm.enumerate_orbits(n, device=dev)  # warm the one-shot path
+        t0 = time.perf_counter()
+        r = wpm.enumerate_orbits(n, device=dev)
+        e2e_ms = (time.perf_counter() - t0) * 1e3
+        want = g["dfs"][str(n)]
+        rows.append({"n": n, "m": n + 4, "maps": r.num_maps, "wpms": total, "nodes": nodes,
+                     "ms_step": round(ms, 3), "ms_search": round(ms_search, 3), "ms_sort": round(ms_sort, 3),
+                     "nodes_per_s": nodes / (ms * 1e-3), "e2e_ms": round(e2e_ms, 3),
+                     "d2h_bytes": int(r.d2h_bytes),
+                     "parity_ok": total == want["sum"] and r.total == want["sum"] and nodes == want["nodes"]})
+        del r
+    return rows
 
 
 class _E2E:
