@@ -345,23 +345,32 @@ def sweep_per_n(wpm, dev, flush, g, ns=range(2, 12), reps=3):
     UBT cap) on this GPU -- device time of search + sort (median of `reps`
     runs after one warm-up, L2 flushed before each) and the one-shot C-ABI
     call with host buffers; parity of counts and nodes against the golden
-    file."""
+    file.  Also Algorithm 2 lines 7 / 13 (union + support + seedness filter,
+    pipeline.hpp:58-89) on each run's resident result: device ms and counts
+    against golden.json["line13"]."""
     import torch
 
     rows = []
     for n in ns:
         with wpm.Plan.orbits(n, device=dev) as p:
             p.run()
-            runs = []
+            runs, l13 = [], []
             for _ in range(reps):
                 flush.zero_()
                 torch.cuda.synchronize(dev)
                 p.run()
                 st, tm = p.stats(), p.timing()
                 runs.append((tm["ms_total"], st["ms_search"], st["ms_sort"], st["nodes"]))
+                # Algorithm 2 lines 7 / 13 on the resident result (k5_line13.cu)
+                lines = p.line13()
+                lt = p.line13_timing()
+                l13.append((lt["ms_union"] + lt["ms_filter"], lt["ms_union"], lt["ms_filter"], lines))
             total = p.fetch().total
         runs.sort()
         ms, ms_search, ms_sort, nodes = runs[len(runs) // 2]
+        l13.sort()
+        ms13, ms_union, ms_filter, (line7, line13) = l13[len(l13) // 2]
+        want13 = g.get("line13", {}).get(str(n), {})
         wpm.enumerate_orbits(n, device=dev)  # warm the one-shot path
         t0 = time.perf_counter()
         r = wpm.enumerate_orbits(n, device=dev)
@@ -371,7 +380,10 @@ def sweep_per_n(wpm, dev, flush, g, ns=range(2, 12), reps=3):
                      "ms_step": round(ms, 3), "ms_search": round(ms_search, 3), "ms_sort": round(ms_sort, 3),
                      "nodes_per_s": nodes / (ms * 1e-3), "e2e_ms": round(e2e_ms, 3),
                      "d2h_bytes": int(r.d2h_bytes),
-                     "parity_ok": total == want["sum"] and r.total == want["sum"] and nodes == want["nodes"]})
+                     "parity_ok": total == want["sum"] and r.total == want["sum"] and nodes == want["nodes"],
+                     "line13": {"line7": line7, "line13": line13, "ms": round(ms13, 3), "ms_union": round(ms_union, 3),
+                                "ms_filter": round(ms_filter, 3),
+                                "parity_ok": (line7, line13) == (want13.get("line7"), want13.get("line13"))}})
         del r
     return rows
 

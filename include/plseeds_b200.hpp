@@ -16,6 +16,8 @@
 //      enumerate_wpm        search.hpp:141-258 (kernels 2-3 + canonical sort)
 //      enumerate_orbits     the per-orbit loop of pipeline.hpp:383-397, one launch
 //      write_complex(es)    complex_io.hpp:21-39
+//      pipeline_line13      pipeline.hpp:52-89 lines 1-13 (union, support, is_seed on the GPU)
+//      is_seed              classify.hpp:51-53 (batch, on the GPU)
 //      purity_error, cap_exceeded_error, format_error   errors.hpp:10-32
 //
 // 2. Inside a program that already includes the reference headers
@@ -284,6 +286,72 @@ inline void write_complexes(std::ostream& os, const std::vector<PureComplex>& li
     }
 }
 
+// ---- Algorithm 2 lines 7 and 13 (pipeline.hpp:58-89) on the device
+
+// PipelineResult's line7 / line13 (pipeline.hpp:23-30) and the line-13
+// survivors in the labeled set's order (the `survivors` of pipeline.hpp:74-89)
+struct Line13Result {
+    long long line7 = 0;
+    long long line13 = 0;
+    std::vector<PureComplex> survivors;
+    double ms_union = 0, ms_filter = 0;
+};
+
+namespace detail {
+struct Complexes {
+    wpm_complexes_t* c = nullptr;
+    ~Complexes() { wpm_complexes_free(c); }
+};
+inline std::vector<PureComplex> complexes_of(const wpm_complexes_t* c) {
+    std::vector<PureComplex> out;
+    out.reserve(static_cast<std::size_t>(c->count));
+    for (std::int64_t i = 0; i < c->count; ++i) {
+        PureComplex K;
+        K.m = c->m;
+        K.n = c->n;
+        for (std::int64_t j = c->offsets[i]; j < c->offsets[i + 1]; ++j) K.facets.emplace_back(c->facets[j]);
+        out.push_back(std::move(K));
+    }
+    return out;
+}
+}  // namespace detail
+
+// lines 1-13 of pipeline(n, db) (pipeline.hpp:52-89): every orbit map, UBT cap
+inline Line13Result pipeline_line13(int n, int p = 4, int device = 0, std::int64_t facet_cap = WPM_CAP_UBT) {
+    detail::Complexes C;
+    check(wpm_pipeline_line13(n, p, facet_cap, device, &C.c));
+    Line13Result r;
+    r.line7 = C.c->line7;
+    r.line13 = C.c->line13;
+    r.ms_union = C.c->ms_union;
+    r.ms_filter = C.c->ms_filter;
+    r.survivors = detail::complexes_of(C.c);
+    return r;
+}
+
+// is_seed (classify.hpp:51-53) over a batch, on the device
+inline std::vector<char> is_seed(const std::vector<PureComplex>& list, int device = 0) {
+    std::vector<char> out(list.size(), 0);
+    std::size_t i = 0;
+    while (i < list.size()) {  // one call per run of equal (m, n)
+        std::size_t j = i;
+        std::vector<std::int64_t> off{0};
+        std::vector<std::uint64_t> fac;
+        while (j < list.size() && list[j].m == list[i].m && list[j].n == list[i].n) {
+            for (const auto& f : list[j].facets) fac.push_back(f.bits);
+            off.push_back(static_cast<std::int64_t>(fac.size()));
+            ++j;
+        }
+        std::vector<std::uint8_t> flags(j - i);
+        check(wpm_seed_flags(list[i].m, list[i].n, static_cast<std::int64_t>(j - i), off.data(), fac.data(), device,
+                             flags.data()));
+        for (std::size_t k = i; k < j; ++k) out[k] = static_cast<char>(flags[k - i] & 1);
+        i = j;
+    }
+    return out;
+}
+inline bool is_seed(const PureComplex& K, int device = 0) { return is_seed(std::vector<PureComplex>{K}, device)[0]; }
+
 }  // namespace plseeds_b200
 
 // ---------------------------------------------------------------------------
@@ -355,6 +423,51 @@ inline std::vector<PureComplex> enumerate_wpm(const SearchJob& job) {
         std::vector<VertexSet> fs;
         for (const auto& f : K.facets) fs.emplace_back(f.bits);
         out.emplace_back(job.m, job.n, std::move(fs), /*embedded=*/true);
+    }
+    return out;
+}
+
+}  // namespace b200
+}  // namespace plseeds
+#endif
+
+// Line-13 adapter for programs that include plseeds/classify.hpp (or
+// pipeline.hpp) first: the reference's own PureComplex type in and out.
+#ifdef PLSEEDS_CLASSIFY_HPP
+namespace plseeds {
+namespace b200 {
+
+// is_seed(K) (classify.hpp:51-53) for a batch, on the device
+inline std::vector<char> is_seed(const std::vector<PureComplex>& list, int device = 0) {
+    std::vector<plseeds_b200::PureComplex> in;
+    in.reserve(list.size());
+    for (const auto& K : list) {
+        plseeds_b200::PureComplex k;
+        k.m = K.m;
+        k.n = K.n;
+        for (const auto& f : K.facets) k.facets.emplace_back(f.bits);
+        in.push_back(std::move(k));
+    }
+    return plseeds_b200::is_seed(in, device);
+}
+
+struct Line13Result {
+    long long line7 = 0, line13 = 0;
+    std::vector<PureComplex> survivors;  // pipeline.hpp:74-89, in order
+};
+
+// lines 1-13 of pipeline(n, db) (pipeline.hpp:52-89) with the reference's types
+inline Line13Result pipeline_line13(int n, int device = 0) {
+    const auto r = plseeds_b200::pipeline_line13(n, 4, device);
+    Line13Result out;
+    out.line7 = r.line7;
+    out.line13 = r.line13;
+    out.survivors.reserve(r.survivors.size());
+    for (const auto& K : r.survivors) {
+        std::vector<VertexSet> fs;
+        fs.reserve(K.facets.size());
+        for (const auto& f : K.facets) fs.emplace_back(f.bits);
+        out.survivors.emplace_back(K.m, K.n, std::move(fs));
     }
     return out;
 }

@@ -21,6 +21,14 @@
  *   wpm_plan_fetch / wpm_result_*  <- std::vector<PureComplex> return value (search.hpp:141)
  *   wpm_enumerate           <- enumerate_wpm(job) one-shot     search.hpp:141-258
  *   wpm_write_cplx          <- write_complexes(os, list)       include/plseeds/complex_io.hpp:21-39
+ *   wpm_plan_run_kernel_basis <- enumerate_wpm's own algorithm (kernel basis + combination-space
+ *                              odometer, search.hpp:141-258) with every leaf on the GPU
+ *   wpm_plan_line13         <- Algorithm 2 lines 7 and 13      include/plseeds/pipeline.hpp:58-89
+ *                              (std::set union of the per-orbit lists; support == full(m),
+ *                              complex.hpp:64-70; is_seed, classify.hpp:51-53)
+ *   wpm_seed_flags          <- is_seed(K) / K.support() over a batch (classify.hpp:22-53,
+ *                              complex.hpp:192-221)
+ *   wpm_pipeline_line13     <- pipeline(n, db) lines 1-13     include/plseeds/pipeline.hpp:52-89
  *
  * Status codes mirror the CLI exit codes (tools/plseeds_cli.cpp:31-35):
  * 0 ok, 2 format/purity/invalid argument, 3 infeasible, 5 cap exceeded,
@@ -92,6 +100,21 @@ typedef struct {
     int64_t d2h_bytes;           /* device->host bytes (result included) */
 } wpm_result_t;
 
+/* labeled complexes on [m] with facets of size n (PureComplex, complex.hpp:23-55),
+ * in the canonical order of std::set<std::vector<VertexSet>> (pipeline.hpp:58). */
+typedef struct {
+    int32_t m, n;
+    int64_t count;
+    int64_t *offsets;            /* count + 1 */
+    uint64_t *facets;            /* offsets[count] masks (bit v = vertex v), ascending per complex */
+    int32_t words;               /* uint64 words per complex in `bits` */
+    uint64_t *bits;              /* count * words: characteristic bitsets over ALL n-subsets of [m]
+                                    in ascending mask order (catalog.hpp:112-120) */
+    int64_t line7, line13;       /* Algorithm 2 line counts of the run that produced the list */
+    double ms_union, ms_filter;  /* device time of the union (line 7) and the filters (line 13) */
+    int64_t h2d_bytes, d2h_bytes;
+} wpm_complexes_t;
+
 /* ---------------------------------------------------------------- host */
 const char *wpm_last_error(void);
 int wpm_device_count(void);
@@ -146,6 +169,39 @@ int wpm_canonical_sort_device(int32_t device, const uint32_t *bits32, const uint
 /* Measured INT32 lane-op peak of `device` (LOP3/IADD3 issue, all SMs), ops/s:
  * the roofline denominator of the integer-issue-bound search. */
 int wpm_int_peak(int32_t device, double *ops_per_s);
+/* Algorithm 1 exactly as the reference runs it (search.hpp:141-258): the
+ * reference's kernel basis per map on the host (gf2_kernel bitmatrix.hpp:125-153,
+ * convenient_basis kernel_basis.hpp:198-235, pins via apply_link_constraints
+ * :248-321), then EVERY leaf of its combination space (search.hpp:62-104) on
+ * the device: XOR of the block deltas, count cap, wpm_counts_ok (:114-131).
+ * Same output set and result layout as wpm_plan_run; a space larger than
+ * candidate_cap returns 5 (cap_exceeded_error, search.hpp:147-150). */
+int wpm_plan_run_kernel_basis(wpm_plan_t *plan, uint64_t candidate_cap, int64_t *total_out);
+/* leaves visited (= the sum of the combination-space sizes), leaves inside the
+ * cap that went through wpm_counts_ok, host basis time, device leaf time */
+int wpm_plan_kernel_basis_stats(const wpm_plan_t *plan, int64_t *leaves, int64_t *checked, double *ms_prep,
+                                double *ms_leaves);
+/* combination_space(basis).size_saturated(), kernel dimension s and induced
+ * blocks of map `map` (after wpm_plan_run_kernel_basis) */
+int wpm_plan_combination_space(const wpm_plan_t *plan, int32_t map, uint64_t *space, int32_t *s, int32_t *blocks);
+/* Algorithm 2 lines 7 and 13 on the last run's results (pipeline.hpp:58-89),
+ * on the device: the union of every map's WPMs as labeled complexes (line 7,
+ * exact duplicates across maps removed), then full support and is_seed
+ * (line 13).  Needs C(m, n) <= 2048 (every Picard-4 n).  Results stay
+ * resident until the next run. */
+int wpm_plan_line13(wpm_plan_t *plan, int64_t *line7, int64_t *line13);
+int wpm_plan_line13_timing(const wpm_plan_t *plan, double *ms_union, double *ms_filter);
+/* which = 7: the union; which = 13: the survivors of the filters; canonical order */
+int wpm_plan_fetch_complexes(wpm_plan_t *plan, int32_t which, wpm_complexes_t **out);
+void wpm_complexes_free(wpm_complexes_t *list);
+/* write_complexes (complex_io.hpp:34-39) of a list; returns bytes needed */
+int64_t wpm_write_complexes(const wpm_complexes_t *list, char *buf, int64_t buf_len);
+/* Batch of pure complexes (CSR facet masks, any facet order): flags_out[i]
+ * bit 0 = is_seed(K) (classify.hpp:51), bit 1 = K.support() == full(m).
+ * Validates like PureComplex (complex.hpp:37-55): labels in 1..m, every
+ * facet of size n, no duplicates -> 2.  m <= 16, <= WPM_MAX_FACETS facets. */
+int wpm_seed_flags(int32_t m, int32_t n, int64_t count, const int64_t *offsets, const uint64_t *facets,
+                   int32_t device, uint8_t *flags_out);
 void wpm_plan_destroy(wpm_plan_t *plan);
 
 /* ---------------------------------------------------------------- one-shot */
@@ -153,6 +209,9 @@ int wpm_enumerate(const wpm_job_t *job, wpm_result_t **out);
 /* Algorithm-2 loop for one n: every orbit map, UBT (or given) cap. */
 int wpm_enumerate_orbits(int32_t n, int32_t p, int64_t facet_cap, int32_t device, wpm_result_t **out);
 void wpm_result_free(wpm_result_t *res);
+/* Algorithm 2 lines 1-13 for one n (pipeline.hpp:52-89): orbits, search,
+ * union, filters; the line-13 survivors with both line counts. */
+int wpm_pipeline_line13(int32_t n, int32_t p, int64_t facet_cap, int32_t device, wpm_complexes_t **out);
 
 /* complex_io.hpp:21-39 for map `map` of a result; returns bytes needed,
  * writes at most buf_len. */

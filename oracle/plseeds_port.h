@@ -96,6 +96,25 @@ int64_t po_write_cplx(int m, int n, const uint64_t *universe, int M, const uint6
 /* canonical complex order on bitsets (search.hpp:254-255): <0, 0, >0 */
 int po_bits_cmp(const uint64_t *a, const uint64_t *b, int words);
 
+/* ---- Algorithm 2 lines 7 and 13 (oracle/line13_port.c) */
+/* complex.hpp:192-221: minimal non-faces of a complex on [m] (facet masks),
+ * canonical order; returns the count (writes at most cap) or -status */
+int po_minimal_nonfaces(int m, const uint64_t *facets, int k, uint64_t *out, int cap);
+/* classify.hpp:22-48: 1 and the witness (u < v) if some edge meets no
+ * minimal non-face in exactly one vertex, else 0 */
+int po_wedge_witness(const uint64_t *facets, int k, const uint64_t *mnfs, int nm, int *u, int *v);
+/* classify.hpp:51-53 (literal: face set -> minimal non-faces -> witness) */
+int po_is_seed(int m, const uint64_t *facets, int k);
+/* the same predicate by the swap characterisation (pure complex, facets
+ * ascending): no edge {u,v} met by every facet with K = (u v) K */
+int po_is_seed_swap(int m, const uint64_t *facets, int k);
+/* pipeline.hpp:58-89 on `count` complexes given as bitsets (words uint64)
+ * over po_all_subsets_universe(m, n): union (sort + unique, *line7_out),
+ * then full support + is_seed (literal != 0: po_is_seed, else the swap
+ * form).  Returns line13 and writes the survivors' rows in order. */
+int64_t po_line13(int m, int n, int words, const uint64_t *rows, int64_t count, int literal, int64_t *line7_out,
+                  uint64_t *survivors_out, int64_t *line7_rows_count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,11 +22,13 @@
 #include <cstring>
 #include <fstream>
 #include <iostream>
+#include <set>
 #include <sstream>
 #include <string>
 #include <vector>
 
 #include "plseeds/catalog.hpp"
+#include "plseeds/classify.hpp"
 #include "plseeds/charmap.hpp"
 #include "plseeds/complex_io.hpp"
 #include "plseeds/incidence.hpp"
@@ -168,6 +170,55 @@ int main(int argc, char** argv) {
             if (const char* out = arg_str(argc, argv, "--out")) {
                 std::ofstream os(out, std::ios::binary);
                 write_complexes(os, found);
+            }
+            return 0;
+        }
+        if (cmd == "seed") {
+            // per complex of a .cplx file: "<full support> <is_seed>" (classify.hpp:51)
+            std::ifstream in(argv[2]);
+            for (const PureComplex& K : read_complexes(in, /*embedded=*/true))
+                std::printf("%d %d\n", K.support() == VertexSet::full(K.m) ? 1 : 0, is_seed(K) ? 1 : 0);
+            return 0;
+        }
+        if (cmd == "line13") {
+            // Algorithm 2 lines 1-13 as pipeline.hpp:58-89 runs them (union of
+            // the per-orbit lists, then the Picard and seedness filters);
+            // --out writes the line-13 survivors in order as .cplx
+            const int n = std::atoi(argv[2]);
+            const int threads = arg_int(argc, argv, "--threads", 1);
+            const int m = n + 4;
+            const auto t0 = Clock::now();
+            std::set<std::vector<VertexSet>> labeled;
+            for (const auto& d : idcm_orbits(n, 4)) {
+                SearchJob job;
+                job.m = m;
+                job.n = n;
+                job.facets = matroid_universe(d);
+                const IncidenceMatrix A = incidence_matrix(job.facets);
+                job.basis = convenient_basis(kernel_basis(A), A);
+                job.properties = {ubt_property(n, static_cast<int>(job.facets.size()))};
+                job.threads = threads;
+                job.candidate_cap = ~0ull;
+                for (const PureComplex& K : enumerate_wpm(job)) labeled.insert(K.facets);
+            }
+            const double t_enum = since(t0);
+            const auto t1 = Clock::now();
+            std::vector<std::vector<VertexSet>> all(labeled.begin(), labeled.end());
+            std::vector<char> keep(all.size(), 0);
+            parallel_for_index(static_cast<long long>(all.size()), threads, [&](long long i) {
+                PureComplex K(m, n, all[static_cast<std::size_t>(i)], true);
+                if (K.support() != VertexSet::full(m)) return;
+                if (!is_seed(K)) return;
+                keep[static_cast<std::size_t>(i)] = 1;
+            });
+            std::vector<PureComplex> survivors;
+            for (std::size_t i = 0; i < all.size(); ++i)
+                if (keep[i]) survivors.emplace_back(m, n, all[i]);
+            std::printf("line7 %zu line13 %zu enum_seconds %.6f filter_seconds %.6f threads %d\n", all.size(),
+                        survivors.size(), t_enum, since(t1), threads);
+            if (const char* out = arg_str(argc, argv, "--out")) {
+                std::ofstream os(out, std::ios::binary);
+                write_complexes(os, survivors);
             }
             return 0;
         }

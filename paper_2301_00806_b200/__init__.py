@@ -24,7 +24,7 @@ from __future__ import annotations
 import ctypes
 import os
 from dataclasses import dataclass, field
-from typing import List, Optional, Sequence
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -109,7 +109,26 @@ class _Job(ctypes.Structure):
     ]
 
 
+class _Complexes(ctypes.Structure):
+    _fields_ = [
+        ("m", ctypes.c_int32),
+        ("n", ctypes.c_int32),
+        ("count", ctypes.c_int64),
+        ("offsets", ctypes.POINTER(ctypes.c_int64)),
+        ("facets", ctypes.POINTER(ctypes.c_uint64)),
+        ("words", ctypes.c_int32),
+        ("bits", ctypes.POINTER(ctypes.c_uint64)),
+        ("line7", ctypes.c_int64),
+        ("line13", ctypes.c_int64),
+        ("ms_union", ctypes.c_double),
+        ("ms_filter", ctypes.c_double),
+        ("h2d_bytes", ctypes.c_int64),
+        ("d2h_bytes", ctypes.c_int64),
+    ]
+
+
 _ResultP = ctypes.POINTER(_Result)
+_ComplexesP = ctypes.POINTER(_Complexes)
 _PlanP = ctypes.c_void_p
 
 _SIGS = {
@@ -151,6 +170,20 @@ _SIGS = {
     "wpm_enumerate_orbits": (ctypes.c_int, [_i32, _i32, _i64, _i32, ctypes.POINTER(_ResultP)]),
     "wpm_result_free": (None, [_ResultP]),
     "wpm_write_cplx": (_i64, [_ResultP, _i32, _i32, _i32, _u64p, ctypes.c_char_p, _i64]),
+    "wpm_plan_line13": (ctypes.c_int, [_PlanP, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "wpm_plan_line13_timing": (ctypes.c_int, [_PlanP, ctypes.POINTER(ctypes.c_double),
+                                              ctypes.POINTER(ctypes.c_double)]),
+    "wpm_plan_fetch_complexes": (ctypes.c_int, [_PlanP, _i32, ctypes.POINTER(_ComplexesP)]),
+    "wpm_complexes_free": (None, [_ComplexesP]),
+    "wpm_write_complexes": (_i64, [_ComplexesP, ctypes.c_char_p, _i64]),
+    "wpm_seed_flags": (ctypes.c_int, [_i32, _i32, _i64, ctypes.POINTER(_i64), _u64p, _i32,
+                                      ctypes.POINTER(ctypes.c_uint8)]),
+    "wpm_pipeline_line13": (ctypes.c_int, [_i32, _i32, _i64, _i32, ctypes.POINTER(_ComplexesP)]),
+    "wpm_plan_run_kernel_basis": (ctypes.c_int, [_PlanP, ctypes.c_uint64, ctypes.POINTER(_i64)]),
+    "wpm_plan_kernel_basis_stats": (ctypes.c_int, [_PlanP, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                                                   ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "wpm_plan_combination_space": (ctypes.c_int, [_PlanP, _i32, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(_i32),
+                                                  ctypes.POINTER(_i32)]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -360,6 +393,43 @@ class Plan:
         _check(_lib.wpm_plan_fetch(self._h, ctypes.byref(rp)))
         return Result(rp)
 
+    def run_kernel_basis(self, candidate_cap: int = (1 << 64) - 1) -> int:
+        """Algorithm 1 as the reference runs it (search.hpp:141-258): the
+        reference's kernel basis on the host, EVERY combination-space leaf on
+        the device (k6_odometer.cu); same result layout as run()."""
+        tot = _i64()
+        _check(_lib.wpm_plan_run_kernel_basis(self._h, ctypes.c_uint64(candidate_cap), ctypes.byref(tot)))
+        return int(tot.value)
+
+    def kernel_basis_stats(self) -> dict:
+        a, b, c, d = _i64(), _i64(), ctypes.c_double(), ctypes.c_double()
+        _check(_lib.wpm_plan_kernel_basis_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
+                                                ctypes.byref(d)))
+        return {"leaves": int(a.value), "checked": int(b.value), "ms_prep": c.value, "ms_leaves": d.value}
+
+    def combination_space(self, i: int) -> dict:
+        sp, s, nb = ctypes.c_uint64(), _i32(), _i32()
+        _check(_lib.wpm_plan_combination_space(self._h, i, ctypes.byref(sp), ctypes.byref(s), ctypes.byref(nb)))
+        return {"space": int(sp.value), "s": int(s.value), "blocks": int(nb.value)}
+
+    def line13(self) -> Tuple[int, int]:
+        """Algorithm 2 lines 7 and 13 (pipeline.hpp:58-89) on the last run, on
+        the device: (union size, survivors of the support + seedness filters)."""
+        a, b = _i64(), _i64()
+        _check(_lib.wpm_plan_line13(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return int(a.value), int(b.value)
+
+    def line13_timing(self) -> dict:
+        a, b = ctypes.c_double(), ctypes.c_double()
+        _check(_lib.wpm_plan_line13_timing(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return {"ms_union": a.value, "ms_filter": b.value}
+
+    def fetch_complexes(self, which: int = 13) -> "Complexes":
+        """The line-7 union (which=7) or the line-13 survivors (which=13)."""
+        cp = _ComplexesP()
+        _check(_lib.wpm_plan_fetch_complexes(self._h, which, ctypes.byref(cp)))
+        return Complexes(cp)
+
     def close(self) -> None:
         if self._h:
             _lib.wpm_plan_destroy(self._h)
@@ -412,6 +482,81 @@ class Result:
 
     def map_bits(self, i: int) -> np.ndarray:
         return self.bits[self.offsets[i]:self.offsets[i + 1]]
+
+
+class Complexes:
+    """Host copy of a labeled complex list (wpm_complexes_t): `facets[offsets[i]:
+    offsets[i+1]]` are the facet masks of complex i (bit v = vertex v), `bits`
+    the characteristic rows over all n-subsets of [m] (ascending masks)."""
+
+    def __init__(self, cp):
+        c = cp.contents
+        self.m, self.n, self.count = c.m, c.n, c.count
+        self.line7, self.line13 = c.line7, c.line13
+        self.ms_union, self.ms_filter = c.ms_union, c.ms_filter
+        self.h2d_bytes, self.d2h_bytes = c.h2d_bytes, c.d2h_bytes
+        self.words = c.words
+        self._cp = cp
+        self.offsets = np.ctypeslib.as_array(c.offsets, shape=(c.count + 1,))
+        nf = int(self.offsets[-1])
+        self.facets = (np.ctypeslib.as_array(c.facets, shape=(max(nf, 1),))[:nf] if nf
+                       else np.zeros(0, dtype=np.uint64))
+        nb = c.count * c.words
+        self.bits = (np.ctypeslib.as_array(c.bits, shape=(max(nb, 1),))[:nb].reshape(c.count, c.words) if nb
+                     else np.zeros((0, c.words), dtype=np.uint64))
+
+    def __len__(self) -> int:
+        return int(self.count)
+
+    def complex(self, i: int) -> List[int]:
+        return [int(x) for x in self.facets[self.offsets[i]:self.offsets[i + 1]]]
+
+    def cplx_bytes(self) -> bytes:
+        """write_complexes (complex_io.hpp:34-39) of the whole list."""
+        need = _lib.wpm_write_complexes(self._cp, None, 0)
+        if need < 0:
+            _check(-need)
+        buf = ctypes.create_string_buffer(int(need) + 1)
+        _lib.wpm_write_complexes(self._cp, buf, need)
+        return buf.raw[:need]
+
+    def __del__(self):
+        cp = getattr(self, "_cp", None)
+        if cp is not None:
+            self._cp = None
+            self.offsets = self.facets = self.bits = None
+            _lib.wpm_complexes_free(cp)
+
+
+def seed_flags(m: int, n: int, complexes: Sequence[Sequence[int]], device: int = 0) -> np.ndarray:
+    """is_seed (classify.hpp:51) and full support (complex.hpp:64) of a batch
+    of pure complexes on the device: uint8 flags, bit 0 = seed, bit 1 = full
+    support.  Raises like PureComplex's validation (complex.hpp:37-55)."""
+    off = np.zeros(len(complexes) + 1, dtype=np.int64)
+    for i, K in enumerate(complexes):
+        off[i + 1] = off[i] + len(K)
+    fac = np.zeros(max(int(off[-1]), 1), dtype=np.uint64)
+    k = 0
+    for K in complexes:
+        for f in K:
+            fac[k] = int(f)
+            k += 1
+    flags = np.zeros(max(len(complexes), 1), dtype=np.uint8)
+    _check(_lib.wpm_seed_flags(m, n, len(complexes), off.ctypes.data_as(ctypes.POINTER(_i64)),
+                               fac.ctypes.data_as(_u64p), device, flags.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))))
+    return flags[:len(complexes)]
+
+
+def is_seed(m: int, n: int, facets: Sequence[int], device: int = 0) -> bool:
+    """classify.hpp:51 for one complex (device)."""
+    return bool(seed_flags(m, n, [facets], device)[0] & 1)
+
+
+def pipeline_line13(n: int, p: int = 4, facet_cap: int = WPM_CAP_UBT, device: int = 0) -> Complexes:
+    """Algorithm 2 lines 1-13 for one n (pipeline.hpp:52-89), one call."""
+    cp = _ComplexesP()
+    _check(_lib.wpm_pipeline_line13(n, p, facet_cap, device, ctypes.byref(cp)))
+    return Complexes(cp)
 
 
 # ----------------------------------------------------------------- the drop-in

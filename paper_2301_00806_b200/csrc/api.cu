@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "../../include/wpm_b200.h"
+#include "kbasis.h"
 #include "wpm_dev.cuh"
 #include "wpm_internal.h"
 
@@ -182,6 +183,25 @@ struct wpm_plan {
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     int warps = 0;
     long long h2d = 0, d2h = 0;  // bytes moved by create + run + fetch
+    bool ran = false;
+    // Algorithm 2 lines 7 / 13 of the last run (k5_line13.cu)
+    DevBuf<uint16_t> d_gidx, d_unrank, d_l13_map;
+    DevBuf<uint32_t> d_l13_keys, d_l13_rows, d_l13_iota, d_l13_uidx, d_l13_sidx;
+    DevBuf<uint8_t> d_l13_flags, d_l13_temp;
+    DevBuf<int> d_l13_num;
+    DevBuf<unsigned long long> d_l13_dups;
+    std::vector<uint16_t> unrank;  // all n-subsets of [m], ascending, 0-based masks
+    long long line7 = -1, line13 = -1;
+    int gw = 0;
+    float ms_union = 0, ms_filter = 0;
+    // Algorithm 1 (k6_odometer.cu): the reference's combination space per map
+    std::vector<CombinationSpaceHost> spaces;
+    DevBuf<OdoMap> d_odo_maps;
+    DevBuf<int> d_odo_blk;
+    DevBuf<uint32_t> d_odo_words;
+    DevBuf<unsigned long long> d_odo_ctl;
+    long long leaves = 0, checked = 0;
+    double ms_prep = 0;
 };
 
 // ------------------------------------------------------------------ host
@@ -588,6 +608,8 @@ extern "C" int32_t wpm_plan_incidence(wpm_plan_t* P, int32_t map, uint64_t* ridg
     return N;
 }
 
+static int plan_sort(wpm_plan* P);
+
 static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
     const int K = P->num_maps;
     // root tasks: (f, map) f-major so the largest subtrees start first;
@@ -692,6 +714,11 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         sp.backoff_max = 8192;
         if (const char* e = std::getenv("WPM_HUNGRY")) sp.hungry = std::atoi(e);
         if (const char* e = std::getenv("WPM_BACKOFF_MAX")) sp.backoff_max = std::max(32, std::atoi(e));
+        // donation checks: every 16 nodes for small tables (cheap task
+        // loads; n <= 6 ramps/tails faster), 32 otherwise (n = 11 loads cost
+        // O(N) per donated task) -- measured sweep in DESIGN.md
+        sp.check_every = P->maxN <= 256 ? 16 : 32;
+        if (const char* e = std::getenv("WPM_CHECK_EVERY")) sp.check_every = std::max(1, std::atoi(e));
         CU(cudaEventRecord(P->ev[0], P->stream));
         if (ntasks > 0 && !launch_k3_search(sp, P->num_sms, P->stream, &P->warps))
             return fail(WPM_EINTERNAL, std::string("kernel 3 launch: ") + cudaGetErrorString(cudaGetLastError()));
@@ -705,6 +732,11 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         P->total = (long long)octl[0];
         P->tasks = (long long)qc[3];
         P->nodes = (long long)qc[4];
+        if (std::getenv("WPM_PROFILE") && (qc[5] | qc[6] | qc[7])) {
+            const double all = (double)(qc[5] + qc[6] + qc[7]);
+            std::fprintf(stderr, "[wpm] warp clocks: busy %.1f%%  waiting %.1f%%  final wait %.1f%%  (tasks %llu)\n",
+                         100.0 * qc[5] / all, 100.0 * qc[6] / all, 100.0 * qc[7] / all, qc[3]);
+        }
         if (octl[2]) {  // frame stack overflowed: redo with the full-depth layout
             full_depth = true;
             ++P->reruns;
@@ -714,7 +746,13 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         ++P->reruns;
         P->out_cap = octl[0] + octl[0] / 8 + 1024;  // exact count known now: rerun once
     }
-    // canonical sort
+    return plan_sort(P);
+}
+
+// canonical sort of the key rows in d_out_keys (P->total of them), per-map
+// counts from the group boundaries; shared by the DFS and the odometer runs
+static int plan_sort(wpm_plan* P) {
+    const int K = P->num_maps;
     const long long total = P->total;
     const size_t tb = canon_sort_temp_bytes(std::max<long long>(total, 1), P->w32);
     if (P->d_temp.ensure(tb) || P->d_sorted_bits.ensure((size_t)total * P->w32 + 1) ||
@@ -756,8 +794,11 @@ extern "C" int wpm_plan_run(wpm_plan_t* P, int32_t shard_index, int32_t shard_co
     if (shard_index < 0 || shard_index >= shard_count) return fail(WPM_EINVAL, "bad shard index");
     CU(cudaSetDevice(P->device));
     g_alloc_stream = P->stream;
+    P->ran = false;
+    P->line7 = P->line13 = -1;
     const int rc = plan_search(P, shard_index, shard_count);
     if (rc) return rc;
+    P->ran = true;
     if (total_out) *total_out = P->total;
     return WPM_OK;
 }
@@ -970,4 +1011,470 @@ extern "C" int64_t wpm_write_cplx(const wpm_result_t* R, int32_t map, int32_t m,
             }
     }
     return len;
+}
+
+// ------------------------------------------------------------------ Algorithm 2 lines 7 / 13
+
+namespace {
+
+uint32_t host_binom(int a, int b) { return binom_small(a, b); }
+
+// all n-subsets of [m] in ascending mask order (catalog.hpp:112-120), 0-based
+std::vector<uint16_t> subsets_ascending(int m, int n) {
+    std::vector<uint16_t> out;
+    for (uint32_t x = 0; x < (1u << m); ++x)
+        if (__builtin_popcount(x) == n) out.push_back((uint16_t)x);
+    return out;
+}
+
+}  // namespace
+
+// pipeline.hpp:58-89: union of the last run's WPM lists (line 7), then the
+// full-support and seedness filters (line 13), resident on the device
+extern "C" int wpm_plan_line13(wpm_plan_t* P, int64_t* line7_out, int64_t* line13_out) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (!P->ran) return fail(WPM_EINVAL, "line 13 needs a completed wpm_plan_run");
+    const int m = P->m, n = P->n;
+    const long long U = host_binom(m, n);
+    if (m > 16 || U > 2048) return fail(WPM_EINVAL, "line 13 needs C(m, n) <= 2048 facets in the label universe");
+    CU(cudaSetDevice(P->device));
+    g_alloc_stream = P->stream;
+    const int gw = (int)((U + 31) / 32);
+    const int kw = key_words_for(gw);
+    const long long cnt = P->total;
+    P->gw = gw;
+    if (P->unrank.empty()) {
+        P->unrank = subsets_ascending(m, n);
+        if (P->d_unrank.ensure(U)) return fail(WPM_EINTERNAL, "device allocation failed (line 13)");
+        CU(cudaMemcpyAsync(P->d_unrank.p, P->unrank.data(), U * 2, cudaMemcpyHostToDevice, P->stream));
+        P->h2d += U * 2;
+    }
+    const size_t tsort = canon_sort_temp_bytes(std::max<long long>(cnt, 1), gw);
+    const size_t tsel = l13_select_temp_bytes(std::max<long long>(cnt, 1));
+    size_t total_facets = 0;
+    for (const MapDesc& d : P->desc) total_facets = std::max<size_t>(total_facets, d.facet_off + d.M);
+    if (P->d_gidx.ensure(total_facets) || P->d_l13_keys.ensure((size_t)cnt * (kw + 1)) ||
+        P->d_l13_rows.ensure((size_t)cnt * gw) || P->d_l13_map.ensure(cnt) || P->d_l13_iota.ensure(cnt) ||
+        P->d_l13_uidx.ensure(cnt) || P->d_l13_sidx.ensure(cnt) || P->d_l13_flags.ensure(cnt) ||
+        P->d_l13_temp.ensure(std::max(tsort, tsel)) || P->d_l13_num.ensure(2) || P->d_l13_dups.ensure(1))
+        return fail(WPM_EINTERNAL, "device allocation failed (line 13)");
+    CU(cudaEventRecord(P->ev[0], P->stream));
+    CU(cudaMemsetAsync(P->d_l13_dups.p, 0, 8, P->stream));
+    if (l13_global_rank(P->num_maps, P->d_maps.p, P->d_facets.p, P->d_gidx.p, P->stream) ||
+        l13_remap(P->d_sorted_bits.p, P->d_sorted_map.p, cnt, P->w32, P->d_maps.p, P->d_gidx.p, kw,
+                  P->d_l13_keys.p, P->num_sms, P->stream) ||
+        canon_sort_keys(P->d_l13_keys.p, cnt, gw, P->d_l13_rows.p, P->d_l13_map.p, P->d_l13_temp.p,
+                        P->d_l13_temp.n, nullptr, P->d_l13_dups.p, P->stream) ||
+        l13_unique(P->d_l13_rows.p, cnt, gw, P->d_l13_flags.p, P->d_l13_iota.p, P->d_l13_uidx.p, P->d_l13_num.p,
+                   P->d_l13_temp.p, P->d_l13_temp.n, P->stream))
+        return fail(WPM_EINTERNAL, std::string("line 7 union: ") + cudaGetErrorString(cudaGetLastError()));
+    CU(cudaEventRecord(P->ev[1], P->stream));
+    if (cnt > 0) CU(cudaMemsetAsync(P->d_l13_flags.p, 0, cnt, P->stream));
+    if (l13_filter(P->d_l13_rows.p, gw, P->d_l13_uidx.p, P->d_l13_num.p, cnt, P->d_unrank.p, m, (int)U,
+                   P->d_l13_flags.p, P->d_l13_sidx.p, P->d_l13_num.p + 1, P->d_l13_temp.p, P->d_l13_temp.n,
+                   P->num_sms, P->stream))
+        return fail(WPM_EINTERNAL, std::string("line 13 filter: ") + cudaGetErrorString(cudaGetLastError()));
+    CU(cudaEventRecord(P->ev[2], P->stream));
+    int num[2] = {0, 0};
+    unsigned long long dups = 0;
+    CU(cudaMemcpyAsync(num, P->d_l13_num.p, 8, cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaMemcpyAsync(&dups, P->d_l13_dups.p, 8, cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaStreamSynchronize(P->stream));
+    P->d2h += 16;
+    if ((long long)num[0] + (long long)dups != cnt)
+        return fail(WPM_EINTERNAL, "line 7: unique + duplicate rows != rows");
+    P->line7 = num[0];
+    P->line13 = num[1];
+    CU(cudaEventElapsedTime(&P->ms_union, P->ev[0], P->ev[1]));
+    CU(cudaEventElapsedTime(&P->ms_filter, P->ev[1], P->ev[2]));
+    if (line7_out) *line7_out = P->line7;
+    if (line13_out) *line13_out = P->line13;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_line13_timing(const wpm_plan_t* P, double* ms_union, double* ms_filter) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (ms_union) *ms_union = P->ms_union;
+    if (ms_filter) *ms_filter = P->ms_filter;
+    return WPM_OK;
+}
+
+// global bitset rows -> the C-ABI complex list (CSR of 1-based facet masks)
+static wpm_complexes_t* complexes_from_rows(int m, int n, int gw, const std::vector<uint16_t>& unr,
+                                            const uint32_t* rows, long long count) {
+    auto* C = new wpm_complexes_t();
+    C->m = m;
+    C->n = n;
+    C->count = count;
+    C->words = (gw + 1) / 2;
+    C->offsets = new int64_t[count + 1];
+    C->bits = new uint64_t[(size_t)count * C->words + 1];
+    long long nf = 0;
+    for (long long i = 0; i < count; ++i) {
+        const uint32_t* r = rows + (size_t)i * gw;
+        for (int w = 0; w < gw; ++w) nf += __builtin_popcount(r[w]);
+    }
+    C->facets = new uint64_t[nf + 1];
+    long long k = 0;
+    for (long long i = 0; i < count; ++i) {
+        const uint32_t* r = rows + (size_t)i * gw;
+        C->offsets[i] = k;
+        uint64_t* b = C->bits + (size_t)i * C->words;
+        for (int w = 0; w < C->words; ++w) b[w] = 0;
+        for (int w = 0; w < gw; ++w) {
+            b[w >> 1] |= (uint64_t)r[w] << ((w & 1) * 32);
+            for (uint32_t x = r[w]; x; x &= x - 1) C->facets[k++] = (uint64_t)unr[w * 32 + __builtin_ctz(x)] << 1;
+        }
+    }
+    C->offsets[count] = k;
+    return C;
+}
+
+extern "C" int wpm_plan_fetch_complexes(wpm_plan_t* P, int32_t which, wpm_complexes_t** out) {
+    *out = nullptr;
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (P->line7 < 0) return fail(WPM_EINVAL, "call wpm_plan_line13 first");
+    if (which != 7 && which != 13) return fail(WPM_EINVAL, "which must be 7 or 13");
+    CU(cudaSetDevice(P->device));
+    g_alloc_stream = P->stream;
+    const long long count = which == 7 ? P->line7 : P->line13;
+    const uint32_t* idx = which == 7 ? P->d_l13_uidx.p : P->d_l13_sidx.p;
+    const int gw = P->gw;
+    // the key buffer is free after the union: gather the selected rows there
+    if (l13_gather(P->d_l13_rows.p, gw, idx, count, P->d_l13_keys.p, P->stream))
+        return fail(WPM_EINTERNAL, "gather failed");
+    std::vector<uint32_t> h((size_t)count * gw + 1);
+    if (count) CU(cudaMemcpyAsync(h.data(), P->d_l13_keys.p, (size_t)count * gw * 4, cudaMemcpyDeviceToHost,
+                                  P->stream));
+    CU(cudaStreamSynchronize(P->stream));
+    P->d2h += (long long)count * gw * 4;
+    wpm_complexes_t* C = complexes_from_rows(P->m, P->n, gw, P->unrank, h.data(), count);
+    C->line7 = P->line7;
+    C->line13 = P->line13;
+    C->ms_union = P->ms_union;
+    C->ms_filter = P->ms_filter;
+    *out = C;
+    return WPM_OK;
+}
+
+extern "C" void wpm_complexes_free(wpm_complexes_t* C) {
+    if (!C) return;
+    delete[] C->offsets;
+    delete[] C->facets;
+    delete[] C->bits;
+    delete C;
+}
+
+extern "C" int64_t wpm_write_complexes(const wpm_complexes_t* C, char* buf, int64_t buf_len) {
+    if (!C) return -fail(WPM_EINVAL, "null complex list");
+    int64_t len = 0;
+    char line[512];
+    auto put = [&](const char* s, int k) {
+        if (len + k <= buf_len && buf) std::memcpy(buf + len, s, (size_t)k);
+        len += k;
+    };
+    for (int64_t i = 0; i < C->count; ++i) {  // complex_io.hpp:21-39
+        if (i > 0) put("\n", 1);
+        int k = std::snprintf(line, sizeof(line), "%d %d\n", C->m, C->n);
+        put(line, k);
+        for (int64_t j = C->offsets[i]; j < C->offsets[i + 1]; ++j) {
+            k = 0;
+            bool first = true;
+            for (uint64_t y = C->facets[j]; y; y &= y - 1) {
+                if (!first) line[k++] = ' ';
+                k += std::snprintf(line + k, sizeof(line) - (size_t)k, "%d", __builtin_ctzll(y));
+                first = false;
+            }
+            line[k++] = '\n';
+            put(line, k);
+        }
+    }
+    return len;
+}
+
+// is_seed (classify.hpp:51-53) and full support (complex.hpp:64-70) of a
+// batch of pure complexes; PureComplex validation (complex.hpp:37-55)
+extern "C" int wpm_seed_flags(int32_t m, int32_t n, int64_t count, const int64_t* offsets, const uint64_t* facets,
+                              int32_t device, uint8_t* flags_out) {
+    if (m < 1 || m > 16) return fail(WPM_EINVAL, "vertex count out of range (1..16 on the device)");
+    if (n < 0) return fail(WPM_EINVAL, "negative facet size");
+    if (count < 0 || (count > 0 && (!offsets || !flags_out))) return fail(WPM_EINVAL, "bad batch");
+    const uint64_t full = (((uint64_t)1 << m) - 1) << 1;
+    const long long nf = count > 0 ? offsets[count] : 0;
+    std::vector<uint16_t> masks((size_t)nf + 1);
+    int maxf = 1;
+    for (int64_t i = 0; i < count; ++i) {
+        const int64_t a = offsets[i], b = offsets[i + 1];
+        if (b < a || a < 0 || b > nf) return fail(WPM_EINVAL, "offsets not ascending");
+        if (b - a > WPM_MAX_FACETS) return fail(WPM_EINVAL, "complex with more than WPM_MAX_FACETS facets");
+        maxf = std::max<int>(maxf, (int)(b - a));
+        for (int64_t j = a; j < b; ++j) {
+            const uint64_t f = facets[j];
+            if (f & ~full) return fail(WPM_EINVAL, "facet uses a label outside 1..m");
+            if (__builtin_popcountll(f) != n) return fail(WPM_EINVAL, "purity: facet size differs from n");
+            masks[j] = (uint16_t)(f >> 1);
+        }
+        std::sort(masks.begin() + a, masks.begin() + b);  // PureComplex sorts its facets
+        for (int64_t j = a + 1; j < b; ++j)
+            if (masks[j] == masks[j - 1]) return fail(WPM_EINVAL, "duplicate facet");
+    }
+    auto* P = new wpm_plan();
+    int rc = plan_init(P, device);
+    if (rc == WPM_OK && count > 0) {
+        g_alloc_stream = P->stream;
+        DevBuf<uint16_t> dm;
+        DevBuf<long long> doff;
+        DevBuf<uint8_t> dfl;
+        maxf = (maxf + 7) & ~7;
+        if (dm.ensure(nf + 1) || doff.ensure(count + 1) || dfl.ensure(count)) {
+            rc = fail(WPM_EINTERNAL, "device allocation failed (seed flags)");
+        } else if (cudaMemcpyAsync(dm.p, masks.data(), (nf + 1) * 2, cudaMemcpyHostToDevice, P->stream) ||
+                   cudaMemcpyAsync(doff.p, offsets, (count + 1) * 8, cudaMemcpyHostToDevice, P->stream) ||
+                   l13_seed_flags(dm.p, doff.p, count, m, maxf, dfl.p, P->num_sms, P->stream) ||
+                   cudaMemcpyAsync(flags_out, dfl.p, count, cudaMemcpyDeviceToHost, P->stream) ||
+                   cudaStreamSynchronize(P->stream)) {
+            rc = fail(WPM_EINTERNAL, std::string("seed flags: ") + cudaGetErrorString(cudaGetLastError()));
+        }
+    }
+    wpm_plan_destroy(P);
+    return rc;
+}
+
+// pipeline.hpp:52-89 one-shot for one n: every orbit map, UBT (or the given)
+// cap, search + union + filters; returns the line-13 survivors
+extern "C" int wpm_pipeline_line13(int32_t n, int32_t p, int64_t facet_cap, int32_t device, wpm_complexes_t** out) {
+    *out = nullptr;
+    wpm_plan_t* P = nullptr;
+    int rc = wpm_plan_create_orbits(n, p, facet_cap, device, &P);
+    if (rc) return rc;
+    int64_t total = 0, l7 = 0, l13 = 0;
+    rc = wpm_plan_run(P, 0, 1, &total);
+    if (!rc) rc = wpm_plan_line13(P, &l7, &l13);
+    if (!rc) rc = wpm_plan_fetch_complexes(P, 13, out);
+    if (!rc) {
+        (*out)->h2d_bytes = P->h2d;
+        (*out)->d2h_bytes = P->d2h;
+    }
+    wpm_plan_destroy(P);
+    return rc;
+}
+
+// ------------------------------------------------------------------ Algorithm 1 (the reference's search)
+
+// IncidenceMatrix of a universe (incidence.hpp:34-55): ridges ascending, the
+// ridges of each facet ascending, the parents of each ridge ascending
+static void host_incidence(const std::vector<uint32_t>& facets, HostIncidence* A) {
+    std::vector<uint32_t> ridges;
+    for (uint32_t f : facets)
+        for (uint32_t x = f; x; x &= x - 1) ridges.push_back(f & ~(x & (0u - x)));
+    std::sort(ridges.begin(), ridges.end());
+    ridges.erase(std::unique(ridges.begin(), ridges.end()), ridges.end());
+    A->M = (int)facets.size();
+    A->N = (int)ridges.size();
+    A->cols.assign(A->M, {});
+    A->parents.assign(A->N, {});
+    for (int j = 0; j < A->M; ++j) {
+        const uint32_t f = facets[j];
+        for (uint32_t x = f; x; x &= x - 1) {
+            const uint32_t r = f & ~(x & (0u - x));
+            A->cols[j].push_back((int)(std::lower_bound(ridges.begin(), ridges.end(), r) - ridges.begin()));
+        }
+        std::sort(A->cols[j].begin(), A->cols[j].end());
+        for (int r : A->cols[j]) A->parents[r].push_back(j);
+    }
+}
+
+// enumerate_wpm exactly as the reference runs it (search.hpp:141-258): the
+// kernel basis on the host (kbasis.cpp), every leaf of the combination space
+// on the device (k6_odometer.cu), then the same canonical sort
+extern "C" int wpm_plan_run_kernel_basis(wpm_plan_t* P, uint64_t candidate_cap, int64_t* total_out) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    CU(cudaSetDevice(P->device));
+    g_alloc_stream = P->stream;
+    P->ran = false;
+    P->line7 = P->line13 = -1;
+    const int K = P->num_maps;
+    const int W32 = (P->maxM + 31) / 32;
+    const int Wb = odo_words_bucket(W32);
+    if (Wb < 0) return fail(WPM_EINVAL, "the odometer supports universes of at most 1024 facets");
+    const auto t0 = std::chrono::steady_clock::now();
+    // ---- the reference's basis and combination space, per map
+    P->spaces.assign(K, {});
+    for (int i = 0; i < K; ++i) {
+        const MapDesc& d = P->desc[i];
+        std::vector<uint32_t> fac(d.M);
+        CU(cudaMemcpy(fac.data(), P->d_facets.p + d.facet_off, d.M * 4, cudaMemcpyDeviceToHost));
+        P->d2h += 4LL * d.M;
+        HostIncidence A;
+        host_incidence(fac, &A);
+        std::vector<int> req, forb;
+        if (P->has_pins)
+            for (int j = 0; j < d.M; ++j) {
+                if ((P->pin_in[(size_t)i * P->mw + (j >> 5)] >> (j & 31)) & 1u) req.push_back(j);
+                if ((P->pin_out[(size_t)i * P->mw + (j >> 5)] >> (j & 31)) & 1u) forb.push_back(j);
+            }
+        if (build_space(A, req, forb, &P->spaces[i])) return fail(WPM_EINFEASIBLE, "link constraints are infeasible");
+        if (P->spaces[i].space > candidate_cap)  // search.hpp:147-150
+            return fail(WPM_ECAP, "combination space of " + std::to_string(P->spaces[i].space) +
+                                      " candidates exceeds cap " + std::to_string(candidate_cap));
+    }
+    // ---- device tables: vectors at stride Wb (zero padded)
+    std::vector<OdoMap> om(K);
+    std::vector<int> blk;  // ncand entries, then (after nblk) first-candidate entries
+    std::vector<int> ncand_all, first_all;
+    std::vector<uint32_t> words;
+    long long tasks = 0, leaves = 0;
+    // leaves per prefix: ~512 prefixes per lane of the whole grid (8 CTAs x 8
+    // warps per SM) -- the cap-passing leaves cluster in parts of the space,
+    // so small tasks on the dynamic queue keep the tail short (sweep 4 / 32 /
+    // 128 / 512 / 2048 / 8192 at n = 7: 311 / 139 / 78 / 72 / 83 / 109 ms) --
+    // and at most 64K leaves of inner loop per lane
+    unsigned long long all_leaves = 0;
+    for (const auto& cs : P->spaces) all_leaves += cs.space;
+    const unsigned long long lanes = (unsigned long long)P->num_sms * 64 * 32;
+    long long per_lane = 512;
+    if (const char* e = std::getenv("WPM_ODO_PER_LANE")) per_lane = std::max(1, std::atoi(e));
+    const long long inner_target = (long long)std::min<unsigned long long>(
+        65536, std::max<unsigned long long>(8, all_leaves / ((unsigned long long)per_lane * lanes)));
+    auto put_vec = [&](const uint32_t* v) {
+        for (int w = 0; w < Wb; ++w) words.push_back(w < W32 ? v[w] : 0u);
+    };
+    for (int i = 0; i < K; ++i) {
+        const CombinationSpaceHost& cs = P->spaces[i];
+        const int nb = (int)cs.ncand.size();
+        OdoMap& o = om[i];
+        o.map = i;
+        o.n = P->desc[i].n;
+        o.fs = P->desc[i].fr_stride;
+        o.cap = P->desc[i].cap;
+        o.nb = nb;
+        o.blk = (int)ncand_all.size();
+        o.fr_off = P->desc[i].fr_off;
+        // inner blocks: the last r, >= inner_target leaves per prefix (or every block)
+        long long inner = 1;
+        int r = 0;
+        while (r < nb && r < odo_max_inner() && inner < inner_target) inner *= cs.ncand[nb - 1 - r++];
+        o.r = r;
+        o.inner = inner;
+        o.outer = (long long)(cs.space / (unsigned long long)inner);
+        o.task0 = tasks;
+        tasks += (o.outer + 31) / 32;
+        leaves += (long long)cs.space;
+        o.base_off = (uint32_t)words.size();
+        std::vector<uint32_t> b32(cs.W32);
+        for (int w = 0; w < cs.W32; ++w) b32[w] = cs.base[w];
+        b32.resize(std::max(W32, cs.W32), 0u);
+        put_vec(b32.data());
+        int first = 0;
+        for (int b = 0; b < nb; ++b) {
+            ncand_all.push_back(cs.ncand[b]);
+            first_all.push_back(first);
+            first += cs.ncand[b];
+        }
+        o.delta_off = (uint32_t)words.size();
+        std::vector<uint32_t> v(std::max(W32, cs.W32), 0u);
+        for (int c = 0; c < first; ++c) {
+            std::fill(v.begin(), v.end(), 0u);
+            for (int w = 0; w < cs.W32; ++w) v[w] = cs.deltas[(size_t)c * cs.W32 + w];
+            put_vec(v.data());
+        }
+        o.step_off = (uint32_t)words.size();
+        int c0 = 0;
+        for (int b = 0; b < nb; ++b) {  // step c: delta[c] ^ delta[(c + 1) % ncand]
+            const int nc = cs.ncand[b];
+            for (int c = 0; c < nc; ++c) {
+                std::fill(v.begin(), v.end(), 0u);
+                const uint32_t* a = cs.deltas.data() + (size_t)(c0 + c) * cs.W32;
+                const uint32_t* z = cs.deltas.data() + (size_t)(c0 + (c + 1) % nc) * cs.W32;
+                for (int w = 0; w < cs.W32; ++w) v[w] = a[w] ^ z[w];
+                put_vec(v.data());
+            }
+            c0 += nc;
+        }
+    }
+    const int nblk = (int)ncand_all.size();
+    blk = ncand_all;
+    blk.insert(blk.end(), first_all.begin(), first_all.end());
+    if (P->d_odo_maps.ensure(K) || P->d_odo_blk.ensure(blk.size() + 1) || P->d_odo_words.ensure(words.size() + 1) ||
+        P->d_odo_ctl.ensure(4) || P->d_out_ctl.ensure(4) || P->d_per_map.ensure(K))
+        return fail(WPM_EINTERNAL, "device allocation failed (odometer)");
+    CU(cudaMemcpyAsync(P->d_odo_maps.p, om.data(), sizeof(OdoMap) * K, cudaMemcpyHostToDevice, P->stream));
+    if (!blk.empty())
+        CU(cudaMemcpyAsync(P->d_odo_blk.p, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice, P->stream));
+    CU(cudaMemcpyAsync(P->d_odo_words.p, words.data(), words.size() * 4, cudaMemcpyHostToDevice, P->stream));
+    P->h2d += (long long)(sizeof(OdoMap) * K + blk.size() * 4 + words.size() * 4);
+    P->ms_prep = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (P->out_cap == 0) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const unsigned long long row = (unsigned long long)P->rw * 4 * 3;
+        P->out_cap = std::min<unsigned long long>(std::max<unsigned long long>(fr / 16 / row, 1ull << 20), 1ull << 26);
+    }
+    CU(cudaEventRecord(P->ev[4], P->stream));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        if (P->d_out_keys.ensure(P->out_cap * P->rw)) return fail(WPM_EINTERNAL, "device allocation failed (output)");
+        CU(cudaMemsetAsync(P->d_out_ctl.p, 0, 32, P->stream));
+        CU(cudaMemsetAsync(P->d_odo_ctl.p, 0, 32, P->stream));
+        OdoParams op{};
+        op.maps = P->d_odo_maps.p;
+        op.num_maps = K;
+        op.blk_ncand = P->d_odo_blk.p;
+        op.blk_first = P->d_odo_blk.p + nblk;
+        op.words = P->d_odo_words.p;
+        op.fr = P->d_fr.p;
+        op.task_ctr = P->d_odo_ctl.p;
+        op.total_tasks = tasks;
+        op.cnt_words = (P->maxN + 31) / 32;  // ridge bitset words
+        op.out_keys = P->d_out_keys.p;
+        op.out_ctl = P->d_out_ctl.p;
+        op.out_cap = P->out_cap;
+        op.rw = P->rw;
+        op.leaf_ctr = P->d_odo_ctl.p + 1;
+        CU(cudaEventRecord(P->ev[0], P->stream));
+        if (tasks > 0 && launch_odometer(op, Wb, P->num_sms, P->stream))
+            return fail(WPM_EINTERNAL, std::string("odometer launch: ") + cudaGetErrorString(cudaGetLastError()));
+        CU(cudaEventRecord(P->ev[1], P->stream));
+        unsigned long long octl[4], oc[4];
+        CU(cudaMemcpyAsync(octl, P->d_out_ctl.p, 32, cudaMemcpyDeviceToHost, P->stream));
+        CU(cudaMemcpyAsync(oc, P->d_odo_ctl.p, 32, cudaMemcpyDeviceToHost, P->stream));
+        CU(cudaStreamSynchronize(P->stream));
+        P->d2h += 64;
+        P->total = (long long)octl[0];
+        P->leaves = (long long)oc[1];
+        P->checked = (long long)oc[2];
+        P->nodes = 0;
+        P->tasks = tasks;
+        if (P->leaves != leaves)
+            return fail(WPM_EINTERNAL, "odometer visited " + std::to_string(P->leaves) + " leaves, space is " +
+                                           std::to_string(leaves));
+        if (octl[0] <= P->out_cap) break;
+        P->out_cap = octl[0] + octl[0] / 8 + 1024;
+        ++P->reruns;
+    }
+    const int rc = plan_sort(P);
+    if (rc) return rc;
+    P->ran = true;
+    if (total_out) *total_out = P->total;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_kernel_basis_stats(const wpm_plan_t* P, int64_t* leaves, int64_t* checked, double* ms_prep,
+                                           double* ms_leaves) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (leaves) *leaves = P->leaves;
+    if (checked) *checked = P->checked;
+    if (ms_prep) *ms_prep = P->ms_prep;
+    if (ms_leaves) *ms_leaves = P->ms_search;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_combination_space(const wpm_plan_t* P, int32_t map, uint64_t* space, int32_t* s,
+                                          int32_t* blocks) {
+    if (!P || map < 0 || map >= P->num_maps || (int)P->spaces.size() != P->num_maps)
+        return fail(WPM_EINVAL, "no combination space (run wpm_plan_run_kernel_basis first)");
+    const CombinationSpaceHost& cs = P->spaces[map];
+    if (space) *space = cs.space;
+    if (s) *s = cs.s;
+    if (blocks) *blocks = cs.induced_blocks;
+    return WPM_OK;
 }

@@ -63,7 +63,6 @@ constexpr uint16_t TR_INC = 0x8000;
 constexpr uint32_t CLOSED_FRAME = 0xFFFFu;
 constexpr uint32_t POS_DONE = 0xFFFFu;
 constexpr uint32_t NO_CHILD = 0xFFFFu;
-constexpr int CHECK_EVERY = 32;  // nodes between looks at the queue word
 constexpr int FRAME_CAP = 64;    // frame stack of the fast layouts (measured depth <= 37)
 
 enum TaskKind : uint32_t { T_SINGLE = 0, T_OPEN = 1, T_CLOSED = 2, T_ENTRY = 3 };
@@ -675,6 +674,10 @@ __global__ void __launch_bounds__(128, 8) k3_search(const __grid_constant__ Sear
     w.base = smem + wid * C::BYTES;
     w.sb = static_cast<uint32_t>(__cvta_generic_to_shared(w.base));
     unsigned long long nodes = 0, tasks = 0;
+#ifdef WPM_PROFILE
+    // busy / waiting / final-wait clocks per warp (qctl[5..7]; WPM_PROFILE=1 prints them)
+    unsigned long long prof_busy = 0, prof_wait = 0, prof_t = clock64();
+#endif
 
     for (;;) {
         // ---- pop: a ticket queue.  One atomicAdd on the low half of the
@@ -702,6 +705,17 @@ __global__ void __launch_bounds__(128, 8) k3_search(const __grid_constant__ Sear
             }
         }
         t = __shfl_sync(FULL, t, 0);
+#ifdef WPM_PROFILE
+        {
+            const unsigned long long now = clock64();
+            if (t == -2) {
+                if (lane == 0) atomicAdd(&p.qctl[7], now - prof_t);
+            } else {
+                prof_wait += now - prof_t;
+            }
+            prof_t = now;
+        }
+#endif
         if (t == -2) break;
         const unsigned long long slot = (unsigned long long)t % (unsigned long long)p.qcap;
         __syncwarp();
@@ -748,7 +762,7 @@ __global__ void __launch_bounds__(128, 8) k3_search(const __grid_constant__ Sear
         }
         // ---- the DFS over branch frames
         unsigned long long qword = ld_relaxed_u64(&p.qctl[0]);  // prefetched queue state
-        unsigned long long next_check = nodes + CHECK_EVERY;
+        unsigned long long next_check = nodes + (unsigned)p.check_every;
         while (w.depth > 0) {
             const uint2 fr = w.frames()[w.depth - 1];
             int npos = 0;
@@ -794,7 +808,7 @@ __global__ void __launch_bounds__(128, 8) k3_search(const __grid_constant__ Sear
                 }
             }
             if (nodes >= next_check) {
-                next_check = nodes + CHECK_EVERY;
+                next_check = nodes + (unsigned)p.check_every;
                 // waiting warps <=> the head ticket ran ahead of the tail
                 const long long queued = (long long)(qword >> 32) - (long long)(qword & 0xFFFFFFFFull);
                 if (queued < (long long)p.hungry) try_donate(w, mp, p, lane);
@@ -803,10 +817,21 @@ __global__ void __launch_bounds__(128, 8) k3_search(const __grid_constant__ Sear
         }
         // task finished
         if (lane == 0) atomicAdd(&p.qctl[2], (unsigned long long)-1ll);
+#ifdef WPM_PROFILE
+        {
+            const unsigned long long now = clock64();
+            prof_busy += now - prof_t;
+            prof_t = now;
+        }
+#endif
     }
     if (lane == 0) {
         atomicAdd(&p.qctl[3], tasks);
         atomicAdd(&p.qctl[4], nodes);
+#ifdef WPM_PROFILE
+        atomicAdd(&p.qctl[5], prof_busy);
+        atomicAdd(&p.qctl[6], prof_wait);
+#endif
     }
 }
 

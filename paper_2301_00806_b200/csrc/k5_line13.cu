@@ -1,0 +1,327 @@
+// k5_line13.cu -- Algorithm 2 lines 7 and 13 on the device.
+//
+// Replaces, in the reference pipeline (pipeline.hpp:58-89):
+//   * line 7: `std::set<std::vector<VertexSet>> labeled` -- the union of the
+//     per-orbit WPM lists as labeled complexes (pipeline.hpp:58-70);
+//   * line 13: the Picard filter `K.support() == full(m)` (complex.hpp:64-70)
+//     and the seedness filter `is_seed(K)` (classify.hpp:51-53, i.e.
+//     wedge_witness over minimal_nonfaces, classify.hpp:22-48 and
+//     complex.hpp:192-221), in the labeled set's order (pipeline.hpp:76-89).
+//
+// Union.  A WPM of map i is a bitset over that map's universe.  Every
+// universe is a set of n-subsets of [m] in ascending-mask order, and for
+// n-subsets ascending mask = colex order, so re-indexing each facet by its
+// colex rank among ALL n-subsets of [m] (C(m,n) <= 1365 for Picard 4) maps a
+// WPM to a "global" bitset while preserving the canonical order of facet
+// lists.  The global rows are canonically sorted by the same sort as kernel
+// 3's output (k4_canon.cu, map id 0) and deduplicated: line 7.
+//
+// Seedness.  The reference builds the face poset, the minimal non-faces and
+// the edge list per complex.  For a PURE complex there is an equivalent
+// test (proof in DESIGN.md): the edge {u, v} is a wedge witness -- no
+// minimal non-face meets it in exactly one vertex -- iff
+//   (1) every facet meets {u, v}, and
+//   (2) the transposition (u v) maps facets to facets, and
+//   (3) {u, v} lies in some facet.
+// One warp per complex: the facet list (ascending masks) goes to shared
+// memory; the pairs that some facet misses entirely are marked from each
+// facet's complement (m - n = 4 vertices -> 6 pairs for Picard 4); only
+// the surviving pairs get the edge and swap checks (binary search of the
+// swapped facet in the list).  The oracle restates the reference literally
+// (oracle/line13_port.c) and the tests check both against the reference's
+// own is_seed (oracle/_ref).
+#include <cub/device/device_select.cuh>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "wpm_internal.h"
+
+namespace wpm {
+
+namespace {
+
+constexpr uint32_t FULL = 0xFFFFFFFFu;
+constexpr int L13_WARPS = 8;  // warps per CTA of the filters
+
+// colex rank of an n-subset (0-based mask) among all n-subsets of [m]
+__device__ __forceinline__ uint32_t colex_rank(uint32_t mask, const Binom& B) {
+    uint32_t r = 0;
+    int i = 1;
+    for (uint32_t x = mask; x; x &= x - 1, ++i) r += B.c[__ffs(x) - 1][i];
+    return r;
+}
+
+// gidx[facet_off + j] = colex rank of facet j of every map (kernel-1 masks
+// are 1-based: bit v = vertex v)
+__global__ void global_rank(const MapDesc* __restrict__ maps, const uint32_t* __restrict__ facets, Binom B,
+                            uint16_t* __restrict__ gidx) {
+    const MapDesc d = maps[blockIdx.x];
+    for (int j = threadIdx.x; j < d.M; j += blockDim.x)
+        gidx[d.facet_off + j] = (uint16_t)colex_rank(facets[d.facet_off + j] >> 1, B);
+}
+
+// one warp per WPM row: universe bits -> global key row (kw words + map 0)
+__global__ void remap_rows(const uint32_t* __restrict__ rows, const uint16_t* __restrict__ map_ids, long long count,
+                           int w32, const MapDesc* __restrict__ maps, const uint16_t* __restrict__ gidx, int kw,
+                           uint32_t* __restrict__ keys) {
+    __shared__ uint32_t buf[L13_WARPS][64];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* b = buf[wib];
+    const long long warps = (long long)gridDim.x * L13_WARPS;
+    for (long long row = (long long)blockIdx.x * L13_WARPS + wib; row < count; row += warps) {
+        for (int w = lane; w < kw; w += 32) b[w] = 0u;
+        __syncwarp();
+        const uint32_t off = maps[map_ids[row]].facet_off;
+        const uint32_t* src = rows + (size_t)row * w32;
+        for (int w = lane; w < w32; w += 32)
+            for (uint32_t x = src[w]; x; x &= x - 1) {
+                const uint32_t g = gidx[off + (uint32_t)(w * 32 + __ffs(x) - 1)];
+                atomicOr(&b[g >> 5], 1u << (g & 31));
+            }
+        __syncwarp();
+        uint32_t* dst = keys + (size_t)row * (kw + 1);
+        for (int w = lane; w <= kw; w += 32) dst[w] = w < kw ? b[w] : 0u;
+        __syncwarp();
+    }
+}
+
+// head flags of the sorted rows (first of each run of equal rows)
+__global__ void run_heads(const uint32_t* __restrict__ rows, long long count, int gw, uint8_t* __restrict__ head) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    bool h = i == 0;
+    if (!h) {
+        const uint32_t* a = rows + (size_t)i * gw;
+        const uint32_t* p = a - gw;
+        for (int w = 0; w < gw && !h; ++w) h = a[w] != p[w];
+    }
+    head[i] = h ? 1 : 0;
+}
+
+__global__ void iota32(uint32_t* idx, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) idx[i] = (uint32_t)i;
+}
+
+__device__ __forceinline__ bool has_mask(const uint16_t* list, int k, uint32_t key) {
+    int lo = 0, hi = k - 1;
+    while (lo <= hi) {
+        const int mid = (lo + hi) >> 1;
+        const uint32_t x = list[mid];
+        if (x == key) return true;
+        if (x < key) lo = mid + 1;
+        else hi = mid - 1;
+    }
+    return false;
+}
+
+// is_seed of a pure complex on [m] (facets ascending in `list`, 0-based
+// masks) by the swap characterisation; warp-collective, k and m uniform
+__device__ bool warp_is_seed(const uint16_t* list, int k, int m, uint32_t* pairs, int lane) {
+    const uint32_t full = (m >= 32) ? FULL : ((1u << m) - 1u);
+    if (lane < 8) pairs[lane] = 0u;
+    __syncwarp();
+    // (1): pair (u, v), u < v, bit u*16+v, is "missed" if some facet avoids both
+    for (int base = 0; base < k; base += 32) {
+        const int j = base + lane;
+        if (j < k) {
+            const uint32_t c = ~(uint32_t)list[j] & full;
+            for (uint32_t a = c; a; a &= a - 1) {
+                const int u = __ffs(a) - 1;
+                const uint32_t row = a & (a - 1);  // the missed vertices v > u
+                if (row) atomicOr(&pairs[u >> 1], row << ((u & 1) * 16));
+            }
+        }
+    }
+    __syncwarp();
+    bool seed = true;
+    for (int u = 0; u < m && seed; ++u) {
+        uint32_t cand = ~(pairs[u >> 1] >> ((u & 1) * 16)) & full & ~((2u << u) - 1u);
+        while (cand && seed) {
+            const int v = __ffs(cand) - 1;
+            cand &= cand - 1;
+            const uint32_t e = (1u << u) | (1u << v);
+            bool edge = false, ok = true;
+            for (int base = 0; base < k; base += 32) {
+                const int j = base + lane;
+                bool bad = false, both = false;
+                if (j < k) {
+                    const uint32_t f = list[j];
+                    const uint32_t hit = f & e;
+                    both = hit == e;
+                    // (2): a facet holding exactly one of u, v must map to a facet
+                    if (hit != 0u && hit != e) bad = !has_mask(list, k, f ^ e);
+                }
+                edge |= __any_sync(FULL, both);
+                if (__any_sync(FULL, bad)) {
+                    ok = false;
+                    break;
+                }
+            }
+            if (ok && edge) seed = false;  // (3): a witness edge
+        }
+    }
+    __syncwarp();
+    return seed;
+}
+
+// line-13 filter over the unique sorted rows: one warp per complex; decode
+// the global bitset into the ascending facet list, then support + seedness
+__global__ void filter_rows(const uint32_t* __restrict__ rows, int gw, const uint32_t* __restrict__ uidx,
+                            const int* __restrict__ num, const uint16_t* __restrict__ unrank, int m, int maxf,
+                            uint8_t* __restrict__ keep) {
+    extern __shared__ uint16_t l13_smem[];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint16_t* list = l13_smem + (size_t)wib * (maxf + 16);
+    uint32_t* pairs = reinterpret_cast<uint32_t*>(list + maxf);
+    const long long count = *num;
+    const uint32_t full = (1u << m) - 1u;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long i = (long long)blockIdx.x * (blockDim.x >> 5) + wib; i < count; i += warps) {
+        const uint32_t* row = rows + (size_t)uidx[i] * gw;
+        int total = 0;
+        uint32_t sup = 0u;
+        for (int base = 0; base < gw; base += 32) {
+            const int w = base + lane;
+            uint32_t x = w < gw ? row[w] : 0u;
+            const int c = __popc(x);
+            int inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(FULL, inc, o);
+                if (lane >= o) inc += t;
+            }
+            int pos = total + inc - c;
+            for (; x; x &= x - 1) {
+                const uint32_t f = unrank[w * 32 + __ffs(x) - 1];
+                list[pos++] = (uint16_t)f;
+                sup |= f;
+            }
+            total += __shfl_sync(FULL, inc, 31);
+        }
+        __syncwarp();
+        sup = __reduce_or_sync(FULL, sup);
+        bool k13 = sup == full;
+        if (k13) k13 = warp_is_seed(list, total, m, pairs, lane);
+        if (lane == 0) keep[i] = k13 ? 1 : 0;
+        __syncwarp();
+    }
+}
+
+// general batch: complexes as CSR lists of 0-based masks (ascending per
+// complex); flags bit 0 = is_seed, bit 1 = full support
+__global__ void seed_flags_csr(const uint16_t* __restrict__ masks, const long long* __restrict__ off, long long count,
+                               int m, int maxf, uint8_t* __restrict__ flags) {
+    extern __shared__ uint16_t l13_smem[];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint16_t* list = l13_smem + (size_t)wib * (maxf + 16);
+    uint32_t* pairs = reinterpret_cast<uint32_t*>(list + maxf);
+    const uint32_t full = (1u << m) - 1u;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long i = (long long)blockIdx.x * (blockDim.x >> 5) + wib; i < count; i += warps) {
+        const long long a = off[i];
+        const int k = (int)(off[i + 1] - a);
+        uint32_t sup = 0u;
+        for (int j = lane; j < k; j += 32) {
+            const uint16_t f = masks[a + j];
+            list[j] = f;
+            sup |= f;
+        }
+        __syncwarp();
+        sup = __reduce_or_sync(FULL, sup);
+        const bool s = warp_is_seed(list, k, m, pairs, lane);
+        if (lane == 0) flags[i] = (uint8_t)((s ? 1 : 0) | (sup == full ? 2 : 0));
+        __syncwarp();
+    }
+}
+
+__global__ void gather_sel(const uint32_t* __restrict__ rows, int gw, const uint32_t* __restrict__ idx,
+                           long long count, uint32_t* __restrict__ out) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count * gw) return;
+    const long long r = t / gw;
+    const int w = (int)(t - r * gw);
+    out[t] = rows[(size_t)idx[r] * gw + w];
+}
+
+size_t filter_smem(int maxf) { return (size_t)L13_WARPS * (maxf + 16) * sizeof(uint16_t); }
+
+}  // namespace
+
+int l13_global_rank(int num_maps, const MapDesc* d_maps, const uint32_t* d_facets, uint16_t* d_gidx,
+                    cudaStream_t st) {
+    global_rank<<<num_maps, 256, 0, st>>>(d_maps, d_facets, make_binom(), d_gidx);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int l13_remap(const uint32_t* d_rows, const uint16_t* d_map, long long count, int w32, const MapDesc* d_maps,
+              const uint16_t* d_gidx, int kw, uint32_t* d_keys, int num_sms, cudaStream_t st) {
+    if (count <= 0) return 0;
+    const long long blocks = std::min<long long>((count + L13_WARPS - 1) / L13_WARPS, (long long)num_sms * 16);
+    remap_rows<<<(unsigned)blocks, 32 * L13_WARPS, 0, st>>>(d_rows, d_map, count, w32, d_maps, d_gidx, kw, d_keys);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+size_t l13_select_temp_bytes(long long count) {
+    size_t a = 0;
+    cub::DeviceSelect::Flagged(nullptr, a, (const uint32_t*)nullptr, (const uint8_t*)nullptr, (uint32_t*)nullptr,
+                               (int*)nullptr, (int)count);
+    return a;
+}
+
+int l13_unique(const uint32_t* d_sorted, long long count, int gw, uint8_t* d_flags, uint32_t* d_iota,
+               uint32_t* d_uidx, int* d_num, void* d_temp, size_t temp_bytes, cudaStream_t st) {
+    if (count <= 0) return cudaMemsetAsync(d_num, 0, sizeof(int), st) == cudaSuccess ? 0 : 1;
+    const unsigned g = (unsigned)((count + 255) / 256);
+    run_heads<<<g, 256, 0, st>>>(d_sorted, count, gw, d_flags);
+    iota32<<<g, 256, 0, st>>>(d_iota, count);
+    size_t b = temp_bytes;
+    if (cub::DeviceSelect::Flagged(d_temp, b, d_iota, d_flags, d_uidx, d_num, (int)count, st) != cudaSuccess)
+        return 1;
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int l13_filter(const uint32_t* d_sorted, int gw, const uint32_t* d_uidx, const int* d_num, long long max_count,
+               const uint16_t* d_unrank, int m, int maxf, uint8_t* d_keep, uint32_t* d_sidx, int* d_num13,
+               void* d_temp, size_t temp_bytes, int num_sms, cudaStream_t st) {
+    if (max_count <= 0) return cudaMemsetAsync(d_num13, 0, sizeof(int), st) == cudaSuccess ? 0 : 1;
+    maxf = (maxf + 7) & ~7;  // keeps the per-warp pair words 4-byte aligned
+    const size_t smem = filter_smem(maxf);
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(filter_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return 1;
+    const long long blocks = std::min<long long>((max_count + L13_WARPS - 1) / L13_WARPS, (long long)num_sms * 8);
+    filter_rows<<<(unsigned)blocks, 32 * L13_WARPS, smem, st>>>(d_sorted, gw, d_uidx, d_num, d_unrank, m, maxf,
+                                                                d_keep);
+    if (cudaGetLastError() != cudaSuccess) return 1;
+    size_t b = temp_bytes;
+    // the unique count lives on the device: select over the upper bound, the
+    // tail flags beyond *d_num are cleared first by the caller
+    if (cub::DeviceSelect::Flagged(d_temp, b, d_uidx, d_keep, d_sidx, d_num13, (int)max_count, st) != cudaSuccess)
+        return 1;
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int l13_seed_flags(const uint16_t* d_masks, const long long* d_off, long long count, int m, int maxf,
+                   uint8_t* d_flags, int num_sms, cudaStream_t st) {
+    if (count <= 0) return 0;
+    maxf = (maxf + 7) & ~7;
+    const size_t smem = filter_smem(maxf);
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(seed_flags_csr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return 1;
+    const long long blocks = std::min<long long>((count + L13_WARPS - 1) / L13_WARPS, (long long)num_sms * 8);
+    seed_flags_csr<<<(unsigned)blocks, 32 * L13_WARPS, smem, st>>>(d_masks, d_off, count, m, maxf, d_flags);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int l13_gather(const uint32_t* d_rows, int gw, const uint32_t* d_idx, long long count, uint32_t* d_out,
+               cudaStream_t st) {
+    if (count <= 0) return 0;
+    const long long t = count * gw;
+    gather_sel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(d_rows, gw, d_idx, count, d_out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+}  // namespace wpm

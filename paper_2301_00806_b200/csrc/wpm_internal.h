@@ -32,6 +32,7 @@ struct SearchParams {
     int qcap, recw, mw;
     int hungry;                 // donate while queued tasks < hungry
     int backoff_max;            // ns, idle warps' polling backoff cap
+    int check_every;            // search nodes between looks at the queue word (donation check)
     // output: one key row per WPM = kw bitset words (zero padded) + the map id
     uint32_t* out_keys;         // out_cap * rw
     unsigned long long* out_ctl;  // [0] count, [1] duplicates (after the sort)
@@ -60,6 +61,52 @@ int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sort
 // rows (w32 words) + uint16 map ids -> key rows
 int canon_pack(const uint32_t* d_bits, const uint16_t* d_map, long long count, int w32, uint32_t* d_keys,
                cudaStream_t st);
+
+// Algorithm 2 lines 7 / 13 (k5_line13.cu)
+int l13_global_rank(int num_maps, const MapDesc* d_maps, const uint32_t* d_facets, uint16_t* d_gidx,
+                    cudaStream_t st);
+int l13_remap(const uint32_t* d_rows, const uint16_t* d_map, long long count, int w32, const MapDesc* d_maps,
+              const uint16_t* d_gidx, int kw, uint32_t* d_keys, int num_sms, cudaStream_t st);
+size_t l13_select_temp_bytes(long long count);
+int l13_unique(const uint32_t* d_sorted, long long count, int gw, uint8_t* d_flags, uint32_t* d_iota,
+               uint32_t* d_uidx, int* d_num, void* d_temp, size_t temp_bytes, cudaStream_t st);
+int l13_filter(const uint32_t* d_sorted, int gw, const uint32_t* d_uidx, const int* d_num, long long max_count,
+               const uint16_t* d_unrank, int m, int maxf, uint8_t* d_keep, uint32_t* d_sidx, int* d_num13,
+               void* d_temp, size_t temp_bytes, int num_sms, cudaStream_t st);
+int l13_seed_flags(const uint16_t* d_masks, const long long* d_off, long long count, int m, int maxf,
+                   uint8_t* d_flags, int num_sms, cudaStream_t st);
+int l13_gather(const uint32_t* d_rows, int gw, const uint32_t* d_idx, long long count, uint32_t* d_out,
+               cudaStream_t st);
+
+// Algorithm 1 on the device (k6_odometer.cu): the reference's combination
+// space, one map per OdoMap; vectors are Wb uint32 words (Wb =
+// odo_words_bucket(W32), zero padded)
+struct OdoMap {
+    int32_t map, n, fs, cap;      // plan map id, facet size, fr stride, facet cap (INT32_MAX = none)
+    int32_t nb, r, blk, pad;      // blocks (widest first), inner blocks (the last r), first block entry
+    uint32_t fr_off, base_off;    // into fr (uint16); base vector into words
+    uint32_t delta_off, step_off; // candidate / step vectors of the map's blocks into words
+    long long outer, task0, inner;  // outer prefixes, first warp task, leaves per prefix
+};
+struct OdoParams {
+    const OdoMap* maps;
+    int num_maps;
+    const int* blk_ncand;   // candidates per block
+    const int* blk_first;   // first candidate of each block within its map
+    const uint32_t* words;  // base / delta / step vectors
+    const uint16_t* fr;
+    unsigned long long* task_ctr;
+    long long total_tasks;
+    int cnt_words;          // ridge bitset words: ceil(max N / 32)
+    uint32_t* out_keys;
+    unsigned long long* out_ctl;  // [0] rows
+    unsigned long long out_cap;
+    int rw;
+    unsigned long long* leaf_ctr;  // [0] leaves visited, [1] cap-passing leaves checked
+};
+int odo_max_inner();
+int odo_words_bucket(int W32);
+int launch_odometer(const OdoParams& p, int Wb, int num_sms, cudaStream_t st);
 
 // INT32 lane-op issue peak (LOP3 + IADD3 chains over every SM), ops/s
 int int_peak_measure(int device, double* ops_per_s);

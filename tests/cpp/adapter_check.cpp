@@ -10,8 +10,10 @@
 // oracle/Makefile (target `ref`) into oracle/_ref/; run by tests/test_gpu_parity.py.
 #include <cstdio>
 #include <random>
+#include <set>
 
 #include "plseeds/catalog.hpp"
+#include "plseeds/classify.hpp"
 #include "plseeds/pipeline.hpp"
 #include "plseeds/search.hpp"
 #include "plseeds_b200.hpp"
@@ -98,6 +100,41 @@ int main() {
             std::printf("MISMATCH cap_exceeded_error not thrown\n");
             ++failures;
         }
+    }
+    // Algorithm 2 lines 7 and 13 (pipeline.hpp:58-89) vs the reference's own
+    // union + support + is_seed, n = 2..4
+    for (int n = 2; n <= 4; ++n) {
+        const int m = n + 4;
+        std::set<std::vector<VertexSet>> labeled;
+        for (const auto& d : idcm_orbits(n, 4)) {
+            auto job = make_job(matroid_universe(d), m, n);
+            job.properties = {ubt_property(n, static_cast<int>(job.facets.size()))};
+            for (const auto& K : enumerate_wpm(job)) labeled.insert(K.facets);
+        }
+        std::vector<PureComplex> survivors;
+        for (const auto& fs : labeled) {
+            PureComplex K(m, n, fs, true);
+            if (K.support() == VertexSet::full(m) && is_seed(K)) survivors.emplace_back(m, n, fs);
+        }
+        const auto got = b200::pipeline_line13(n);
+        if (got.line7 != (long long)labeled.size() || got.line13 != (long long)survivors.size() ||
+            !(got.survivors == survivors)) {
+            std::printf("MISMATCH line13 n=%d: reference %zu/%zu, b200 %lld/%lld\n", n, labeled.size(),
+                        survivors.size(), got.line7, got.line13);
+            ++failures;
+        }
+        ++jobs;
+    }
+    {  // batch is_seed on catalog complexes (test_classify.cpp:24-31)
+        const std::vector<PureComplex> cat = {s0(), simplex_boundary(2), square(), wedge(square(), 1), hexagon(),
+                                              octahedron(), pentagon(), suspension(pentagon())};
+        const auto got = b200::is_seed(cat);
+        for (std::size_t i = 0; i < cat.size(); ++i)
+            if ((got[i] != 0) != is_seed(cat[i])) {
+                std::printf("MISMATCH is_seed catalog %zu\n", i);
+                ++failures;
+            }
+        ++jobs;
     }
     std::printf("adapter_check: %d jobs, %d mismatches\n", jobs, failures);
     return failures ? 1 : 0;

@@ -71,6 +71,13 @@ class Oracle:
                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     ctypes.POINTER(_DfsResult)]
         L.dfs_result_free.argtypes = [ctypes.POINTER(_DfsResult)]
+        L.po_minimal_nonfaces.argtypes = [ctypes.c_int, _u64p, ctypes.c_int, _u64p, ctypes.c_int]
+        L.po_wedge_witness.argtypes = [_u64p, ctypes.c_int, _u64p, ctypes.c_int, _i32p, _i32p]
+        L.po_is_seed.argtypes = [ctypes.c_int, _u64p, ctypes.c_int]
+        L.po_is_seed_swap.argtypes = [ctypes.c_int, _u64p, ctypes.c_int]
+        L.po_line13.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _u64p, ctypes.c_int64, ctypes.c_int,
+                                ctypes.POINTER(ctypes.c_int64), _u64p, ctypes.POINTER(ctypes.c_int64)]
+        L.po_line13.restype = ctypes.c_int64
         L.dfs_enumerate_shard.argtypes = [ctypes.c_int, _u64p, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
                                           ctypes.c_int, ctypes.c_int, ctypes.POINTER(_DfsResult)]
 
@@ -207,3 +214,46 @@ class Oracle:
         x = np.ascontiguousarray(a, dtype=np.uint64)
         y = np.ascontiguousarray(b, dtype=np.uint64)
         return int(self.lib.po_bits_cmp(x.ctypes.data_as(_u64p), y.ctypes.data_as(_u64p), len(x)))
+
+    # -- Algorithm 2 lines 7 and 13 (oracle/line13_port.c)
+    def minimal_nonfaces(self, m: int, facets: Sequence[int]) -> List[int]:
+        f = _arr(facets, np.uint64)
+        out = np.zeros(1 << 16, dtype=np.uint64)
+        k = self.lib.po_minimal_nonfaces(m, f.ctypes.data_as(_u64p), len(facets), out.ctypes.data_as(_u64p),
+                                         len(out))
+        if k < 0:
+            raise ValueError("bad complex")
+        return [int(x) for x in out[:k]]
+
+    def wedge_witness(self, m: int, facets: Sequence[int]):
+        mnf = _arr(self.minimal_nonfaces(m, facets), np.uint64)
+        f = _arr(facets, np.uint64)
+        u = ctypes.c_int32(0)
+        v = ctypes.c_int32(0)
+        w = self.lib.po_wedge_witness(f.ctypes.data_as(_u64p), len(facets), mnf.ctypes.data_as(_u64p),
+                                      len(self.minimal_nonfaces(m, facets)), ctypes.byref(u), ctypes.byref(v))
+        return (u.value, v.value) if w == 1 else None
+
+    def is_seed(self, m: int, facets: Sequence[int], literal: bool = True) -> bool:
+        f = _arr(sorted(facets), np.uint64)
+        fn = self.lib.po_is_seed if literal else self.lib.po_is_seed_swap
+        r = fn(m, f.ctypes.data_as(_u64p), len(facets))
+        if r < 0:
+            raise ValueError("bad complex")
+        return bool(r)
+
+    def line13(self, m: int, n: int, rows: np.ndarray, literal: bool = False):
+        """pipeline.hpp:58-89 on complexes given as bitsets over the
+        all-subsets universe of (m, n): (line7, line13, survivor rows)."""
+        r = np.ascontiguousarray(rows, dtype=np.uint64)
+        cnt = r.shape[0]
+        w = r.shape[1]
+        if cnt == 0:
+            r = np.zeros((1, w), dtype=np.uint64)
+        surv = np.zeros((max(cnt, 1), w), dtype=np.uint64)
+        l7 = ctypes.c_int64(0)
+        k = self.lib.po_line13(m, n, w, r.ctypes.data_as(_u64p), cnt, 1 if literal else 0, ctypes.byref(l7),
+                               surv.ctypes.data_as(_u64p), None)
+        if k < 0:
+            raise ValueError("line13 failed")
+        return int(l7.value), int(k), surv[:k].copy()
