@@ -332,6 +332,18 @@ def main():
         }
         if per_n is not None:
             line["per_n"] = per_n
+            row = next((r for r in per_n if r["n"] == n), None)
+            if row and row.get("alg1"):
+                # the same algorithm on both sides: the reference's leaves per
+                # second (kernel basis + odometer), GPU vs the CPU reference run
+                a1 = row["alg1"]
+                line["alg1_reference_algorithm"] = {
+                    "leaves": a1["leaves"], "gpu_ms": round(a1["ms_prep_host"] + a1["ms_step"], 3),
+                    "gpu_leaves_per_s": a1["leaves"] / ((a1["ms_prep_host"] + a1["ms_step"]) * 1e-3),
+                    "cpu_leaves_per_s": (cpu["reference_leaves"] / cpu["wall_s"]) if cpu else None,
+                    "cpu_threads": cpu["cores"] if cpu else None, "parity_ok": a1["parity_ok"],
+                    "note": "leaves = combination-space leaves (search.hpp:62-104), the reference's own work unit; "
+                            "gpu_ms = host basis build + device leaf kernel + canonical sort"}
         print(json.dumps(line))
     if plan is not None:
         plan.close()
@@ -340,14 +352,16 @@ def main():
     return 0
 
 
-def sweep_per_n(wpm, dev, flush, g, ns=range(2, 12), reps=3):
+def sweep_per_n(wpm, dev, flush, g, ns=range(2, 12), reps=3, alg1_max_n=8):
     """The metric is quoted per Picard-4 dimension n: every n = 2..11 (all maps,
     UBT cap) on this GPU -- device time of search + sort (median of `reps`
     runs after one warm-up, L2 flushed before each) and the one-shot C-ABI
     call with host buffers; parity of counts and nodes against the golden
     file.  Also Algorithm 2 lines 7 / 13 (union + support + seedness filter,
     pipeline.hpp:58-89) on each run's resident result: device ms and counts
-    against golden.json["line13"]."""
+    against golden.json["line13"]; and, for n <= alg1_max_n, the reference's
+    own algorithm (kernel basis + every combination-space leaf on the GPU):
+    the reference's work unit (leaves) per second, apples to apples."""
     import torch
 
     rows = []
@@ -371,11 +385,37 @@ def sweep_per_n(wpm, dev, flush, g, ns=range(2, 12), reps=3):
         l13.sort()
         ms13, ms_union, ms_filter, (line7, line13) = l13[len(l13) // 2]
         want13 = g.get("line13", {}).get(str(n), {})
-        wpm.enumerate_orbits(n, device=dev)  # warm the one-shot path
-        t0 = time.perf_counter()
-        r = wpm.enumerate_orbits(n, device=dev)
-        e2e_ms = (time.perf_counter() - t0) * 1e3
         want = g["dfs"][str(n)]
+        alg1 = None
+        if n <= alg1_max_n:
+            # the reference's own search (Algorithm 1: kernel basis + every
+            # combination-space leaf, k6_odometer.cu), same maps and cap
+            with wpm.Plan.orbits(n, device=dev) as p:
+                ts = []
+                for _ in range(1 if n >= 8 else 3):
+                    flush.zero_()
+                    torch.cuda.synchronize(dev)
+                    tot1 = p.run_kernel_basis()
+                    st1 = p.kernel_basis_stats()
+                    ts.append((p.timing()["ms_total"], st1["ms_leaves"], st1["ms_prep"]))
+                    counts1 = p.fetch().counts
+                ts.sort()
+                ms1, ms_leaves, ms_prep = ts[len(ts) // 2]
+            ref_maps = g["ubt"].get(str(n), {}).get("maps")
+            want_counts = [m["wpms"] for m in ref_maps] if ref_maps else [m["wpms"] for m in want["maps"]]
+            alg1 = {"leaves": st1["leaves"], "cap_checked": st1["checked"], "ms_step": round(ms1, 3),
+                    "ms_leaves": round(ms_leaves, 3), "ms_prep_host": round(ms_prep, 3),
+                    "leaves_per_s": st1["leaves"] / (ms_leaves * 1e-3) if ms_leaves else None,
+                    "parity_ok": tot1 == want["sum"] and counts1 == want_counts}
+        wpm.enumerate_orbits(n, device=dev)  # warm the one-shot path
+        e2e = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            r = wpm.enumerate_orbits(n, device=dev)
+            e2e.append((time.perf_counter() - t0) * 1e3)
+            if len(e2e) < 3:
+                del r
+        e2e_ms = statistics.median(e2e)
         rows.append({"n": n, "m": n + 4, "maps": r.num_maps, "wpms": total, "nodes": nodes,
                      "ms_step": round(ms, 3), "ms_search": round(ms_search, 3), "ms_sort": round(ms_sort, 3),
                      "nodes_per_s": nodes / (ms * 1e-3), "e2e_ms": round(e2e_ms, 3),
@@ -383,7 +423,8 @@ def sweep_per_n(wpm, dev, flush, g, ns=range(2, 12), reps=3):
                      "parity_ok": total == want["sum"] and r.total == want["sum"] and nodes == want["nodes"],
                      "line13": {"line7": line7, "line13": line13, "ms": round(ms13, 3), "ms_union": round(ms_union, 3),
                                 "ms_filter": round(ms_filter, 3),
-                                "parity_ok": (line7, line13) == (want13.get("line7"), want13.get("line13"))}})
+                                "parity_ok": (line7, line13) == (want13.get("line7"), want13.get("line13"))},
+                     "alg1": alg1})
         del r
     return rows
 

@@ -156,6 +156,12 @@ __global__ void __launch_bounds__(32 * ODO_WARPS) odometer(const __grid_constant
         const uint32_t* step_in = bstep + (size_t)(om.r > 0 ? bfirst[bl] : 0) * W;
         int d_in = 0;
         int qn = 0;  // queued candidates (warp-uniform)
+        // a binary innermost block {0, g} (the usual case: free generators
+        // sort last) steps by g both ways: keep g in registers
+        const bool bin_in = om.r > 0 && nc_in == 2;
+        uint32_t g_in[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) g_in[w] = bin_in ? __ldg(step_in + w) : 0u;
         for (long long leaf = 0; leaf < om.inner; ++leaf) {
             int pc = 0;
 #pragma unroll
@@ -182,7 +188,12 @@ __global__ void __launch_bounds__(32 * ODO_WARPS) odometer(const __grid_constant
             }
             // advance the inner odometer (warp-uniform)
             if (om.r > 0) {
-                xor_words<W>(K, step_in + (size_t)d_in * W);
+                if (bin_in) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) K[w] ^= g_in[w];
+                } else {
+                    xor_words<W>(K, step_in + (size_t)d_in * W);
+                }
                 if (++d_in == nc_in) {  // wrapped: the step back to candidate 0 is applied; carry
                     d_in = 0;
                     for (int i = om.r - 2; i >= 0; --i) {
