@@ -29,6 +29,11 @@
  *   wpm_seed_flags          <- is_seed(K) / K.support() over a batch (classify.hpp:22-53,
  *                              complex.hpp:192-221)
  *   wpm_pipeline_line13     <- pipeline(n, db) lines 1-13     include/plseeds/pipeline.hpp:52-89
+ *   wpm_plan_line15         <- Algorithm 2 line 15             include/plseeds/pipeline.hpp:91-103
+ *                              (canonical_form, isomorphism.hpp:228-303, + first-appearance dedupe)
+ *   wpm_canonical_forms     <- canonical_form(K) / detail::refine_classes over a batch
+ *                              (isomorphism.hpp:162-303)
+ *   wpm_pipeline_line15     <- pipeline(n, db) lines 1-15     include/plseeds/pipeline.hpp:52-103
  *
  * Status codes mirror the CLI exit codes (tools/plseeds_cli.cpp:31-35):
  * 0 ok, 2 format/purity/invalid argument, 3 infeasible, 5 cap exceeded,
@@ -113,6 +118,8 @@ typedef struct {
     int64_t line7, line13;       /* Algorithm 2 line counts of the run that produced the list */
     double ms_union, ms_filter;  /* device time of the union (line 7) and the filters (line 13) */
     int64_t h2d_bytes, d2h_bytes;
+    int64_t line15;              /* Algorithm 2 line 15 count (-1 before wpm_plan_line15) */
+    double ms_canon, ms_dedupe;  /* device time of the canonical forms and of the class dedupe */
 } wpm_complexes_t;
 
 /* ---------------------------------------------------------------- host */
@@ -191,7 +198,19 @@ int wpm_plan_combination_space(const wpm_plan_t *plan, int32_t map, uint64_t *sp
  * resident until the next run. */
 int wpm_plan_line13(wpm_plan_t *plan, int64_t *line7, int64_t *line13);
 int wpm_plan_line13_timing(const wpm_plan_t *plan, double *ms_union, double *ms_filter);
-/* which = 7: the union; which = 13: the survivors of the filters; canonical order */
+/* Algorithm 2 line 15 on the last line-13 result (pipeline.hpp:91-103), on
+ * the device: canonical_form (isomorphism.hpp:228-303) of every survivor,
+ * then one representative per isomorphism class in order of first
+ * appearance.  Needs m <= 15, n <= 11.  *line15 = number of classes. */
+int wpm_plan_line15(wpm_plan_t *plan, int64_t *line15);
+/* device ms of the canonical forms and the dedupe; labelings completed and
+ * single-vertex placements of the canonical-labeling searches */
+int wpm_plan_line15_stats(const wpm_plan_t *plan, double *ms_canon, double *ms_dedupe, int64_t *labelings,
+                          int64_t *placements);
+/* which = 7: the union; which = 13: the survivors of the filters (canonical
+ * order); which = 14: the canonical form of every line-13 survivor, in
+ * survivor order (the `canon` vector of pipeline.hpp:93-96); which = 15: the
+ * line-15 representatives (canonical forms) in order of first appearance */
 int wpm_plan_fetch_complexes(wpm_plan_t *plan, int32_t which, wpm_complexes_t **out);
 void wpm_complexes_free(wpm_complexes_t *list);
 /* write_complexes (complex_io.hpp:34-39) of a list; returns bytes needed */
@@ -202,6 +221,13 @@ int64_t wpm_write_complexes(const wpm_complexes_t *list, char *buf, int64_t buf_
  * facet of size n, no duplicates -> 2.  m <= 16, <= WPM_MAX_FACETS facets. */
 int wpm_seed_flags(int32_t m, int32_t n, int64_t count, const int64_t *offsets, const uint64_t *facets,
                    int32_t device, uint8_t *flags_out);
+/* Batch canonical_form (isomorphism.hpp:228-303) of pure complexes (CSR facet
+ * masks, any order; validated like wpm_seed_flags): canon_out receives each
+ * complex's canonical facet masks, ascending, at the same offsets;
+ * classes_out (optional, count * m) the refined class of every vertex
+ * (detail::refine_classes, isomorphism.hpp:162-218).  m <= 15, n <= 11. */
+int wpm_canonical_forms(int32_t m, int32_t n, int64_t count, const int64_t *offsets, const uint64_t *facets,
+                        int32_t device, uint64_t *canon_out, int8_t *classes_out);
 void wpm_plan_destroy(wpm_plan_t *plan);
 
 /* ---------------------------------------------------------------- one-shot */
@@ -212,6 +238,10 @@ void wpm_result_free(wpm_result_t *res);
 /* Algorithm 2 lines 1-13 for one n (pipeline.hpp:52-89): orbits, search,
  * union, filters; the line-13 survivors with both line counts. */
 int wpm_pipeline_line13(int32_t n, int32_t p, int64_t facet_cap, int32_t device, wpm_complexes_t **out);
+/* Algorithm 2 lines 1-15 for one n (pipeline.hpp:52-103): lines 1-13, then
+ * the canonical forms and the first-appearance class representatives
+ * (line 15); the list holds the representatives and the line 7/13/15 counts. */
+int wpm_pipeline_line15(int32_t n, int32_t p, int64_t facet_cap, int32_t device, wpm_complexes_t **out);
 
 /* complex_io.hpp:21-39 for map `map` of a result; returns bytes needed,
  * writes at most buf_len. */

@@ -115,6 +115,15 @@ int po_is_seed_swap(int m, const uint64_t *facets, int k);
 int64_t po_line13(int m, int n, int words, const uint64_t *rows, int64_t count, int literal, int64_t *line7_out,
                   uint64_t *survivors_out, int64_t *line7_rows_count);
 
+/* line15_port.c -- Algorithm 2 line 15 (pipeline.hpp:91-103) */
+/* isomorphism.hpp:17-24 as histograms: counts_out[v*16 + s] = #mnfs of size s containing v */
+int po_color_sequences(int m, const uint64_t *mnfs, int nm, int *counts_out);
+/* isomorphism.hpp:162-218: cls_out[v-1] = refined class of vertex v; returns the class count */
+int po_refine_classes(int m, const uint64_t *facets, int k, int *cls_out);
+/* isomorphism.hpp:228-303: the canonical relabeling's facets (ascending) into out;
+ * returns k (or -status); *leaves_out = complete labelings visited */
+int po_canonical_form(int m, const uint64_t *facets, int k, uint64_t *out, long long *leaves_out);
+
 #ifdef __cplusplus
 }
 #endif

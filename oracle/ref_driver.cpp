@@ -32,6 +32,7 @@
 #include "plseeds/charmap.hpp"
 #include "plseeds/complex_io.hpp"
 #include "plseeds/incidence.hpp"
+#include "plseeds/isomorphism.hpp"
 #include "plseeds/kernel_basis.hpp"
 #include "plseeds/pipeline.hpp"
 #include "plseeds/search.hpp"
@@ -219,6 +220,44 @@ int main(int argc, char** argv) {
             if (const char* out = arg_str(argc, argv, "--out")) {
                 std::ofstream os(out, std::ios::binary);
                 write_complexes(os, survivors);
+            }
+            return 0;
+        }
+        if (cmd == "line15") {
+            // Algorithm 2 line 15 as pipeline.hpp:91-103 runs it on a .cplx of
+            // line-13 survivors: canonical_form per complex (isomorphism.hpp:228-303)
+            // and the first-appearance representatives.  --canon writes every
+            // canonical form in input order, --out the representatives in order.
+            const int threads = arg_int(argc, argv, "--threads", 1);
+            std::ifstream in(argv[2]);
+            std::vector<PureComplex> survivors = read_complexes(in, /*embedded=*/true);
+            const auto t0 = Clock::now();
+            std::vector<PureComplex> canon(survivors.size());
+            parallel_for_index(static_cast<long long>(survivors.size()), threads, [&](long long i) {
+                canon[static_cast<std::size_t>(i)] = canonical_form(survivors[static_cast<std::size_t>(i)]);
+            });
+            std::vector<PureComplex> reps;
+            std::set<std::vector<VertexSet>> seen;
+            for (auto& c : canon)
+                if (seen.insert(c.facets).second) reps.push_back(c);
+            std::printf("line13 %zu line15 %zu canon_seconds %.6f threads %d\n", survivors.size(), reps.size(),
+                        since(t0), threads);
+            if (const char* out = arg_str(argc, argv, "--canon")) {
+                std::ofstream os(out, std::ios::binary);
+                write_complexes(os, canon);
+            }
+            if (const char* out = arg_str(argc, argv, "--out")) {
+                std::ofstream os(out, std::ios::binary);
+                write_complexes(os, reps);
+            }
+            return 0;
+        }
+        if (cmd == "classes") {
+            // per complex: refine_classes (isomorphism.hpp:162-218) "v:class ..." for vertices 1..m
+            std::ifstream in(argv[2]);
+            for (const PureComplex& K : read_complexes(in, /*embedded=*/true)) {
+                const auto cls = detail::refine_classes(K, minimal_nonfaces(K));
+                for (int v = 1; v <= K.m; ++v) std::printf("%d%c", cls[static_cast<std::size_t>(v)], v == K.m ? '\n' : ' ');
             }
             return 0;
         }

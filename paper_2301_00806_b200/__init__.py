@@ -124,6 +124,9 @@ class _Complexes(ctypes.Structure):
         ("ms_filter", ctypes.c_double),
         ("h2d_bytes", ctypes.c_int64),
         ("d2h_bytes", ctypes.c_int64),
+        ("line15", ctypes.c_int64),
+        ("ms_canon", ctypes.c_double),
+        ("ms_dedupe", ctypes.c_double),
     ]
 
 
@@ -179,6 +182,12 @@ _SIGS = {
     "wpm_seed_flags": (ctypes.c_int, [_i32, _i32, _i64, ctypes.POINTER(_i64), _u64p, _i32,
                                       ctypes.POINTER(ctypes.c_uint8)]),
     "wpm_pipeline_line13": (ctypes.c_int, [_i32, _i32, _i64, _i32, ctypes.POINTER(_ComplexesP)]),
+    "wpm_plan_line15": (ctypes.c_int, [_PlanP, ctypes.POINTER(_i64)]),
+    "wpm_plan_line15_stats": (ctypes.c_int, [_PlanP, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                             ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "wpm_canonical_forms": (ctypes.c_int, [_i32, _i32, _i64, ctypes.POINTER(_i64), _u64p, _i32, _u64p,
+                                           ctypes.POINTER(ctypes.c_int8)]),
+    "wpm_pipeline_line15": (ctypes.c_int, [_i32, _i32, _i64, _i32, ctypes.POINTER(_ComplexesP)]),
     "wpm_plan_run_kernel_basis": (ctypes.c_int, [_PlanP, ctypes.c_uint64, ctypes.POINTER(_i64)]),
     "wpm_plan_kernel_basis_stats": (ctypes.c_int, [_PlanP, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
@@ -424,8 +433,25 @@ class Plan:
         _check(_lib.wpm_plan_line13_timing(self._h, ctypes.byref(a), ctypes.byref(b)))
         return {"ms_union": a.value, "ms_filter": b.value}
 
+    def line15(self) -> int:
+        """Algorithm 2 line 15 (pipeline.hpp:91-103) on the last line-13
+        result, on the device: canonical_form of every survivor, then one
+        representative per isomorphism class; returns the class count."""
+        a = _i64()
+        _check(_lib.wpm_plan_line15(self._h, ctypes.byref(a)))
+        return int(a.value)
+
+    def line15_stats(self) -> dict:
+        a, b = ctypes.c_double(), ctypes.c_double()
+        c, d = _i64(), _i64()
+        _check(_lib.wpm_plan_line15_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
+                                          ctypes.byref(d)))
+        return {"ms_canon": a.value, "ms_dedupe": b.value, "labelings": int(c.value), "placements": int(d.value)}
+
     def fetch_complexes(self, which: int = 13) -> "Complexes":
-        """The line-7 union (which=7) or the line-13 survivors (which=13)."""
+        """The line-7 union (which=7), the line-13 survivors (13), the
+        canonical form of every survivor in survivor order (14), or the
+        line-15 class representatives in order of first appearance (15)."""
         cp = _ComplexesP()
         _check(_lib.wpm_plan_fetch_complexes(self._h, which, ctypes.byref(cp)))
         return Complexes(cp)
@@ -492,7 +518,8 @@ class Complexes:
     def __init__(self, cp):
         c = cp.contents
         self.m, self.n, self.count = c.m, c.n, c.count
-        self.line7, self.line13 = c.line7, c.line13
+        self.line7, self.line13, self.line15 = c.line7, c.line13, c.line15
+        self.ms_canon, self.ms_dedupe = c.ms_canon, c.ms_dedupe
         self.ms_union, self.ms_filter = c.ms_union, c.ms_filter
         self.h2d_bytes, self.d2h_bytes = c.h2d_bytes, c.d2h_bytes
         self.words = c.words
@@ -557,6 +584,50 @@ def pipeline_line13(n: int, p: int = 4, facet_cap: int = WPM_CAP_UBT, device: in
     cp = _ComplexesP()
     _check(_lib.wpm_pipeline_line13(n, p, facet_cap, device, ctypes.byref(cp)))
     return Complexes(cp)
+
+
+def pipeline_line15(n: int, p: int = 4, facet_cap: int = WPM_CAP_UBT, device: int = 0) -> Complexes:
+    """Algorithm 2 lines 1-15 for one n (pipeline.hpp:52-103), one call: the
+    line-15 class representatives (canonical forms, first-appearance order)."""
+    cp = _ComplexesP()
+    _check(_lib.wpm_pipeline_line15(n, p, facet_cap, device, ctypes.byref(cp)))
+    return Complexes(cp)
+
+
+def _csr(complexes: Sequence[Sequence[int]]):
+    off = np.zeros(len(complexes) + 1, dtype=np.int64)
+    for i, K in enumerate(complexes):
+        off[i + 1] = off[i] + len(K)
+    fac = np.zeros(max(int(off[-1]), 1), dtype=np.uint64)
+    k = 0
+    for K in complexes:
+        for f in K:
+            fac[k] = int(f)
+            k += 1
+    return off, fac
+
+
+def canonical_forms(m: int, n: int, complexes: Sequence[Sequence[int]], device: int = 0,
+                    with_classes: bool = False):
+    """canonical_form (isomorphism.hpp:228-303) of a batch of pure complexes
+    on the device: one ascending facet-mask list per complex; with_classes
+    also returns detail::refine_classes (isomorphism.hpp:162-218) per vertex
+    1..m.  Raises like PureComplex's validation (complex.hpp:37-55)."""
+    off, fac = _csr(complexes)
+    out = np.zeros_like(fac)
+    cls = np.zeros(max(len(complexes) * m, 1), dtype=np.int8)
+    _check(_lib.wpm_canonical_forms(m, n, len(complexes), off.ctypes.data_as(ctypes.POINTER(_i64)),
+                                    fac.ctypes.data_as(_u64p), device, out.ctypes.data_as(_u64p),
+                                    cls.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)) if with_classes else None))
+    forms = [[int(x) for x in out[off[i]:off[i + 1]]] for i in range(len(complexes))]
+    if with_classes:
+        return forms, [[int(x) for x in cls[i * m:(i + 1) * m]] for i in range(len(complexes))]
+    return forms
+
+
+def canonical_form(m: int, n: int, facets: Sequence[int], device: int = 0) -> List[int]:
+    """isomorphism.hpp:228-303 for one complex (device)."""
+    return canonical_forms(m, n, [facets], device)[0]
 
 
 # ----------------------------------------------------------------- the drop-in

@@ -194,6 +194,14 @@ struct wpm_plan {
     long long line7 = -1, line13 = -1;
     int gw = 0;
     float ms_union = 0, ms_filter = 0;
+    // Algorithm 2 line 15 of the last line-13 result (k7_line15.cu)
+    DevBuf<uint32_t> d_l15_rows, d_l15_sidx, d_l15_iota, d_l15_rep;
+    DevBuf<uint8_t> d_l15_first, d_l15_temp;
+    DevBuf<int> d_l15_num;
+    DevBuf<unsigned long long> d_l15_ctl;
+    long long line15 = -1, l15_leaves = 0, l15_steps = 0;
+    int l15_kmax = 0, l15_mnfcap = 0, l15_launches = 0;
+    float ms_canon = 0, ms_dedupe = 0;
     // Algorithm 1 (k6_odometer.cu): the reference's combination space per map
     std::vector<CombinationSpaceHost> spaces;
     DevBuf<OdoMap> d_odo_maps;
@@ -795,7 +803,7 @@ extern "C" int wpm_plan_run(wpm_plan_t* P, int32_t shard_index, int32_t shard_co
     CU(cudaSetDevice(P->device));
     g_alloc_stream = P->stream;
     P->ran = false;
-    P->line7 = P->line13 = -1;
+    P->line7 = P->line13 = P->line15 = -1;
     const int rc = plan_search(P, shard_index, shard_count);
     if (rc) return rc;
     P->ran = true;
@@ -1099,10 +1107,83 @@ extern "C" int wpm_plan_line13_timing(const wpm_plan_t* P, double* ms_union, dou
     return WPM_OK;
 }
 
+// pipeline.hpp:91-103: canonical_form (isomorphism.hpp:228-303) of every
+// line-13 survivor, then one representative per class in order of first
+// appearance -- on the device, on the resident line-13 result
+extern "C" int wpm_plan_line15(wpm_plan_t* P, int64_t* line15_out) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (P->line13 < 0) return fail(WPM_EINVAL, "line 15 needs wpm_plan_line13 first");
+    const int m = P->m, n = P->n;
+    if (m > 15 || n > 11) return fail(WPM_EINVAL, "line 15 on the device needs m <= 15 and n <= 11");
+    CU(cudaSetDevice(P->device));
+    g_alloc_stream = P->stream;
+    const long long cnt = P->line13;
+    const int gw = P->gw;
+    const size_t tdd = l15_dedupe_temp_bytes(std::max<long long>(cnt, 1), gw);
+    if (P->d_l15_rows.ensure((size_t)std::max<long long>(cnt, 1) * gw) || P->d_l15_sidx.ensure(cnt + 1) ||
+        P->d_l15_iota.ensure(cnt + 1) || P->d_l15_rep.ensure(cnt + 1) || P->d_l15_first.ensure(cnt + 1) ||
+        P->d_l15_temp.ensure(tdd) || P->d_l15_num.ensure(2) || P->d_l15_ctl.ensure(4))
+        return fail(WPM_EINTERNAL, "device allocation failed (line 15)");
+    CU(cudaEventRecord(P->ev[0], P->stream));
+    if (l15_max_facets(P->d_l13_rows.p, gw, P->d_l13_sidx.p, cnt, P->d_l15_num.p, P->stream))
+        return fail(WPM_EINTERNAL, "line 15: facet count pass failed");
+    int kmax = 0;
+    CU(cudaMemcpyAsync(&kmax, P->d_l15_num.p, 4, cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaStreamSynchronize(P->stream));
+    // minimal non-faces: ~k for Picard-4 seeds; the kernel flags an overflow
+    // and the launch repeats with twice the room (rare, exact either way)
+    int mnfcap = std::max(64, 2 * kmax);
+    unsigned long long ctl[4] = {0, 0, 0, 0};
+    P->l15_launches = 0;
+    for (;;) {
+        const L15Layout L = l15_layout(m, n, kmax, mnfcap, gw);
+        if (L.P > 2048 || l15_smem_bytes(L) > 227 * 1024)
+            return fail(WPM_EINTERNAL, "line 15: complexes too large for the device layout");
+        ++P->l15_launches;
+        if (l15_launch(L, P->d_l13_rows.p, P->d_l13_sidx.p, nullptr, P->d_unrank.p, nullptr, nullptr, cnt,
+                       P->d_l15_rows.p, nullptr, nullptr, P->d_l15_ctl.p, P->num_sms, P->stream))
+            return fail(WPM_EINTERNAL, std::string("line 15 canonical forms: ") +
+                                           cudaGetErrorString(cudaGetLastError()));
+        CU(cudaMemcpyAsync(ctl, P->d_l15_ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, P->stream));
+        CU(cudaStreamSynchronize(P->stream));
+        if (ctl[1] == 0) break;
+        mnfcap *= 2;
+    }
+    P->l15_kmax = kmax;
+    P->l15_mnfcap = mnfcap;
+    CU(cudaEventRecord(P->ev[1], P->stream));
+    if (l15_dedupe(P->d_l15_rows.p, cnt, gw, P->d_l15_sidx.p, P->d_l15_iota.p, P->d_l15_first.p, P->d_l15_rep.p,
+                   P->d_l15_num.p + 1, P->d_l15_temp.p, P->d_l15_temp.n, P->stream))
+        return fail(WPM_EINTERNAL, std::string("line 15 dedupe: ") + cudaGetErrorString(cudaGetLastError()));
+    CU(cudaEventRecord(P->ev[2], P->stream));
+    int nrep = 0;
+    CU(cudaMemcpyAsync(&nrep, P->d_l15_num.p + 1, 4, cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaStreamSynchronize(P->stream));
+    P->d2h += 4 + 4 + sizeof(ctl);
+    P->line15 = nrep;
+    P->l15_leaves = (long long)ctl[2];
+    P->l15_steps = (long long)ctl[3];
+    CU(cudaEventElapsedTime(&P->ms_canon, P->ev[0], P->ev[1]));
+    CU(cudaEventElapsedTime(&P->ms_dedupe, P->ev[1], P->ev[2]));
+    if (line15_out) *line15_out = P->line15;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_line15_stats(const wpm_plan_t* P, double* ms_canon, double* ms_dedupe, int64_t* labelings,
+                                     int64_t* placements) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (ms_canon) *ms_canon = P->ms_canon;
+    if (ms_dedupe) *ms_dedupe = P->ms_dedupe;
+    if (labelings) *labelings = P->l15_leaves;
+    if (placements) *placements = P->l15_steps;
+    return WPM_OK;
+}
+
 // global bitset rows -> the C-ABI complex list (CSR of 1-based facet masks)
 static wpm_complexes_t* complexes_from_rows(int m, int n, int gw, const std::vector<uint16_t>& unr,
                                             const uint32_t* rows, long long count) {
     auto* C = new wpm_complexes_t();
+    C->line15 = -1;
     C->m = m;
     C->n = n;
     C->count = count;
@@ -1134,15 +1215,19 @@ extern "C" int wpm_plan_fetch_complexes(wpm_plan_t* P, int32_t which, wpm_comple
     *out = nullptr;
     if (!P) return fail(WPM_EINVAL, "null plan");
     if (P->line7 < 0) return fail(WPM_EINVAL, "call wpm_plan_line13 first");
-    if (which != 7 && which != 13) return fail(WPM_EINVAL, "which must be 7 or 13");
+    if (which != 7 && which != 13 && which != 14 && which != 15)
+        return fail(WPM_EINVAL, "which must be 7, 13, 14 or 15");
+    if (which >= 14 && P->line15 < 0) return fail(WPM_EINVAL, "call wpm_plan_line15 first");
     CU(cudaSetDevice(P->device));
     g_alloc_stream = P->stream;
-    const long long count = which == 7 ? P->line7 : P->line13;
-    const uint32_t* idx = which == 7 ? P->d_l13_uidx.p : P->d_l13_sidx.p;
+    const long long count = which == 7 ? P->line7 : which == 15 ? P->line15 : P->line13;
     const int gw = P->gw;
     // the key buffer is free after the union: gather the selected rows there
-    if (l13_gather(P->d_l13_rows.p, gw, idx, count, P->d_l13_keys.p, P->stream))
-        return fail(WPM_EINTERNAL, "gather failed");
+    const int grc = which >= 14 ? l15_gather(P->d_l15_rows.p, gw, which == 15 ? P->d_l15_rep.p : P->d_l15_iota.p,
+                                             count, P->d_l13_keys.p, P->stream)
+                                : l13_gather(P->d_l13_rows.p, gw, which == 7 ? P->d_l13_uidx.p : P->d_l13_sidx.p,
+                                             count, P->d_l13_keys.p, P->stream);
+    if (grc) return fail(WPM_EINTERNAL, "gather failed");
     std::vector<uint32_t> h((size_t)count * gw + 1);
     if (count) CU(cudaMemcpyAsync(h.data(), P->d_l13_keys.p, (size_t)count * gw * 4, cudaMemcpyDeviceToHost,
                                   P->stream));
@@ -1153,6 +1238,9 @@ extern "C" int wpm_plan_fetch_complexes(wpm_plan_t* P, int32_t which, wpm_comple
     C->line13 = P->line13;
     C->ms_union = P->ms_union;
     C->ms_filter = P->ms_filter;
+    C->line15 = P->line15;
+    C->ms_canon = P->ms_canon;
+    C->ms_dedupe = P->ms_dedupe;
     *out = C;
     return WPM_OK;
 }
@@ -1259,6 +1347,108 @@ extern "C" int wpm_pipeline_line13(int32_t n, int32_t p, int64_t facet_cap, int3
     return rc;
 }
 
+// pipeline.hpp:52-103 one-shot for one n: lines 1-13 as above, then the
+// canonical forms and the first-appearance representatives (line 15)
+extern "C" int wpm_pipeline_line15(int32_t n, int32_t p, int64_t facet_cap, int32_t device, wpm_complexes_t** out) {
+    *out = nullptr;
+    wpm_plan_t* P = nullptr;
+    int rc = wpm_plan_create_orbits(n, p, facet_cap, device, &P);
+    if (rc) return rc;
+    int64_t total = 0, l7 = 0, l13 = 0, l15 = 0;
+    rc = wpm_plan_run(P, 0, 1, &total);
+    if (!rc) rc = wpm_plan_line13(P, &l7, &l13);
+    if (!rc) rc = wpm_plan_line15(P, &l15);
+    if (!rc) rc = wpm_plan_fetch_complexes(P, 15, out);
+    if (!rc) {
+        (*out)->h2d_bytes = P->h2d;
+        (*out)->d2h_bytes = P->d2h;
+    }
+    wpm_plan_destroy(P);
+    return rc;
+}
+
+// canonical_form (isomorphism.hpp:228-303) and refine_classes (:162-218) of
+// a batch of pure complexes; PureComplex validation (complex.hpp:37-55)
+extern "C" int wpm_canonical_forms(int32_t m, int32_t n, int64_t count, const int64_t* offsets,
+                                   const uint64_t* facets, int32_t device, uint64_t* canon_out, int8_t* classes_out) {
+    if (m < 1 || m > 15) return fail(WPM_EINVAL, "vertex count out of range (1..15 for canonical forms)");
+    if (n < 1 || n > 11 || n > m) return fail(WPM_EINVAL, "facet size out of range (1..min(11, m))");
+    if (count < 0 || (count > 0 && (!offsets || !canon_out))) return fail(WPM_EINVAL, "bad batch");
+    const uint64_t full = (((uint64_t)1 << m) - 1) << 1;
+    const long long nf = count > 0 ? offsets[count] : 0;
+    std::vector<uint16_t> masks((size_t)nf + 1);
+    int kmax = 1;
+    for (int64_t i = 0; i < count; ++i) {
+        const int64_t a = offsets[i], b = offsets[i + 1];
+        if (b < a || a < 0 || b > nf) return fail(WPM_EINVAL, "offsets not ascending");
+        if (b - a > WPM_MAX_FACETS) return fail(WPM_EINVAL, "complex with more than WPM_MAX_FACETS facets");
+        kmax = std::max<int>(kmax, (int)(b - a));
+        for (int64_t j = a; j < b; ++j) {
+            const uint64_t f = facets[j];
+            if (f & ~full) return fail(WPM_EINVAL, "facet uses a label outside 1..m");
+            if (__builtin_popcountll(f) != n) return fail(WPM_EINVAL, "purity: facet size differs from n");
+            masks[j] = (uint16_t)(f >> 1);
+        }
+        std::sort(masks.begin() + a, masks.begin() + b);  // PureComplex sorts its facets
+        for (int64_t j = a + 1; j < b; ++j)
+            if (masks[j] == masks[j - 1]) return fail(WPM_EINVAL, "duplicate facet");
+    }
+    auto* P = new wpm_plan();
+    int rc = plan_init(P, device);
+    if (rc == WPM_OK && count > 0) {
+        g_alloc_stream = P->stream;
+        DevBuf<uint16_t> dm, dout;
+        DevBuf<long long> doff;
+        DevBuf<int8_t> dcls;
+        DevBuf<unsigned long long> dctl;
+        std::vector<uint16_t> hout((size_t)nf + 1);
+        std::vector<int8_t> hcls;
+        if (dm.ensure(nf + 1) || dout.ensure(nf + 1) || doff.ensure(count + 1) || dctl.ensure(4) ||
+            (classes_out && dcls.ensure((size_t)count * 16))) {
+            rc = fail(WPM_EINTERNAL, "device allocation failed (canonical forms)");
+        } else if (cudaMemcpyAsync(dm.p, masks.data(), (nf + 1) * 2, cudaMemcpyHostToDevice, P->stream) ||
+                   cudaMemcpyAsync(doff.p, offsets, (count + 1) * 8, cudaMemcpyHostToDevice, P->stream)) {
+            rc = fail(WPM_EINTERNAL, "canonical forms: upload failed");
+        } else {
+            int mnfcap = std::max(64, 2 * kmax);
+            for (;;) {
+                const L15Layout L = l15_layout(m, n, kmax, mnfcap, 1);
+                if (L.P > 2048 || l15_smem_bytes(L) > 227 * 1024) {
+                    rc = fail(WPM_EINTERNAL, "canonical forms: complexes too large for the device layout");
+                    break;
+                }
+                unsigned long long ctl[4] = {0, 0, 0, 0};
+                if (l15_launch(L, nullptr, nullptr, nullptr, nullptr, dm.p, doff.p, count, nullptr, dout.p,
+                               classes_out ? dcls.p : nullptr, dctl.p, P->num_sms, P->stream) ||
+                    cudaMemcpyAsync(ctl, dctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, P->stream) ||
+                    cudaStreamSynchronize(P->stream)) {
+                    rc = fail(WPM_EINTERNAL, std::string("canonical forms: ") +
+                                                 cudaGetErrorString(cudaGetLastError()));
+                    break;
+                }
+                if (ctl[1] == 0) break;
+                mnfcap *= 2;
+            }
+            if (rc == WPM_OK) {
+                if (classes_out) hcls.resize((size_t)count * 16);
+                if (cudaMemcpyAsync(hout.data(), dout.p, (nf + 1) * 2, cudaMemcpyDeviceToHost, P->stream) ||
+                    (classes_out && cudaMemcpyAsync(hcls.data(), dcls.p, (size_t)count * 16, cudaMemcpyDeviceToHost,
+                                                    P->stream)) ||
+                    cudaStreamSynchronize(P->stream)) {
+                    rc = fail(WPM_EINTERNAL, "canonical forms: download failed");
+                } else {
+                    for (long long j = 0; j < nf; ++j) canon_out[j] = (uint64_t)hout[j] << 1;
+                    if (classes_out)
+                        for (int64_t i = 0; i < count; ++i)
+                            for (int v = 0; v < m; ++v) classes_out[i * m + v] = hcls[(size_t)i * 16 + v];
+                }
+            }
+        }
+    }
+    wpm_plan_destroy(P);
+    return rc;
+}
+
 // ------------------------------------------------------------------ Algorithm 1 (the reference's search)
 
 // IncidenceMatrix of a universe (incidence.hpp:34-55): ridges ascending, the
@@ -1292,7 +1482,7 @@ extern "C" int wpm_plan_run_kernel_basis(wpm_plan_t* P, uint64_t candidate_cap, 
     CU(cudaSetDevice(P->device));
     g_alloc_stream = P->stream;
     P->ran = false;
-    P->line7 = P->line13 = -1;
+    P->line7 = P->line13 = P->line15 = -1;
     const int K = P->num_maps;
     const int W32 = (P->maxM + 31) / 32;
     const int Wb = odo_words_bucket(W32);

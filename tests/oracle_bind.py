@@ -78,6 +78,8 @@ class Oracle:
         L.po_line13.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _u64p, ctypes.c_int64, ctypes.c_int,
                                 ctypes.POINTER(ctypes.c_int64), _u64p, ctypes.POINTER(ctypes.c_int64)]
         L.po_line13.restype = ctypes.c_int64
+        L.po_refine_classes.argtypes = [ctypes.c_int, _u64p, ctypes.c_int, _i32p]
+        L.po_canonical_form.argtypes = [ctypes.c_int, _u64p, ctypes.c_int, _u64p, ctypes.POINTER(ctypes.c_longlong)]
         L.dfs_enumerate_shard.argtypes = [ctypes.c_int, _u64p, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
                                           ctypes.c_int, ctypes.c_int, ctypes.POINTER(_DfsResult)]
 
@@ -257,3 +259,73 @@ class Oracle:
         if k < 0:
             raise ValueError("line13 failed")
         return int(l7.value), int(k), surv[:k].copy()
+
+    # -- Algorithm 2 line 15 (oracle/line15_port.c)
+    def refine_classes(self, m: int, facets: Sequence[int]) -> List[int]:
+        """isomorphism.hpp:162-218: refined class of vertices 1..m."""
+        f = _arr(facets, np.uint64)
+        cls = np.zeros(m, dtype=np.int32)
+        r = self.lib.po_refine_classes(m, f.ctypes.data_as(_u64p), len(facets), cls.ctypes.data_as(_i32p))
+        if r < 0:
+            raise ValueError("bad complex")
+        return [int(x) for x in cls]
+
+    def canonical_form(self, m: int, facets: Sequence[int]) -> Tuple[List[int], int]:
+        """isomorphism.hpp:228-303: (canonical facets ascending, labelings visited)."""
+        f = _arr(sorted(facets), np.uint64)
+        out = np.zeros(max(len(facets), 1), dtype=np.uint64)
+        leaves = ctypes.c_longlong(0)
+        k = self.lib.po_canonical_form(m, f.ctypes.data_as(_u64p), len(facets), out.ctypes.data_as(_u64p),
+                                       ctypes.byref(leaves))
+        if k < 0:
+            raise ValueError("bad complex")
+        return [int(x) for x in out[:k]], int(leaves.value)
+
+    def line15(self, m: int, n: int, rows: np.ndarray):
+        """pipeline.hpp:91-103 on line-13 survivors given as bitsets over the
+        all-subsets universe: (canonical rows per survivor, first-appearance
+        representative indices)."""
+        all_sub = np.asarray(self.all_subsets_universe(m, n), dtype=np.uint64)
+        r = np.ascontiguousarray(rows, dtype=np.uint64)
+        canon = np.zeros_like(r)
+        seen = {}
+        reps = []
+        for i in range(r.shape[0]):
+            facets = [int(all_sub[j]) for j in _bits_of(r[i])]
+            cf, _ = self.canonical_form(m, facets)
+            idx = np.searchsorted(all_sub, np.asarray(cf, dtype=np.uint64))
+            for j in idx:
+                canon[i, j >> 6] |= np.uint64(1) << np.uint64(j & 63)
+            key = canon[i].tobytes()
+            if key not in seen:
+                seen[key] = i
+                reps.append(i)
+        return canon, reps
+
+
+def _bits_of(row: np.ndarray) -> List[int]:
+    out = []
+    for w, x in enumerate(row.tolist()):
+        while x:
+            b = x & -x
+            out.append(w * 64 + b.bit_length() - 1)
+            x ^= b
+    return out
+
+
+def read_cplx(data: bytes):
+    """complex_io.hpp:41-89 reader: list of (m, n, [facet masks])."""
+    out = []
+    for block in data.decode().strip().split("\n\n"):
+        lines = block.strip().split("\n")
+        if not lines or not lines[0]:
+            continue
+        m, n = map(int, lines[0].split())
+        fs = []
+        for ln in lines[1:]:
+            mask = 0
+            for v in ln.split():
+                mask |= 1 << int(v)
+            fs.append(mask)
+        out.append((m, n, fs))
+    return out
