@@ -204,9 +204,13 @@ int wpm_plan_line13_timing(const wpm_plan_t *plan, double *ms_union, double *ms_
  * appearance.  Needs m <= 15, n <= 11.  *line15 = number of classes. */
 int wpm_plan_line15(wpm_plan_t *plan, int64_t *line15);
 /* device ms of the canonical forms and the dedupe; labelings completed and
- * single-vertex placements of the canonical-labeling searches */
+ * single-vertex placements of the canonical-labeling searches; kernel
+ * launches (> 1: a complex had more minimal non-faces than the first sizing) */
 int wpm_plan_line15_stats(const wpm_plan_t *plan, double *ms_canon, double *ms_dedupe, int64_t *labelings,
-                          int64_t *placements);
+                          int64_t *placements, int32_t *launches);
+/* diagnostics: single-vertex placements of each survivor's canonical-labeling
+ * search (survivor order), at most cap entries; returns the survivor count */
+int64_t wpm_plan_line15_costs(wpm_plan_t *plan, int64_t *out, int64_t cap);
 /* which = 7: the union; which = 13: the survivors of the filters (canonical
  * order); which = 14: the canonical form of every line-13 survivor, in
  * survivor order (the `canon` vector of pipeline.hpp:93-96); which = 15: the

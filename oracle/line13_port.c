@@ -73,8 +73,10 @@ int po_minimal_nonfaces(int m, const uint64_t *facets, int k, uint64_t *out, int
         const uint64_t c = (uint64_t)s << 1;
         int minimal = 1;
         for (uint64_t r = c; r; r &= r - 1) {
+            /* the empty set is not in face_set (faces_by_card erases it,
+             * complex.hpp:185), so a singleton candidate is never minimal */
             const uint64_t sub = c & ~(r & (0 - r));
-            if (sub && !face[sub >> 1]) minimal = 0;
+            if (!sub || !face[sub >> 1]) minimal = 0;
         }
         if (minimal) {
             if (cnt < cap) out[cnt] = c;

@@ -184,7 +184,8 @@ _SIGS = {
     "wpm_pipeline_line13": (ctypes.c_int, [_i32, _i32, _i64, _i32, ctypes.POINTER(_ComplexesP)]),
     "wpm_plan_line15": (ctypes.c_int, [_PlanP, ctypes.POINTER(_i64)]),
     "wpm_plan_line15_stats": (ctypes.c_int, [_PlanP, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
-                                             ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+                                             ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i32)]),
+    "wpm_plan_line15_costs": (_i64, [_PlanP, ctypes.POINTER(_i64), _i64]),
     "wpm_canonical_forms": (ctypes.c_int, [_i32, _i32, _i64, ctypes.POINTER(_i64), _u64p, _i32, _u64p,
                                            ctypes.POINTER(ctypes.c_int8)]),
     "wpm_pipeline_line15": (ctypes.c_int, [_i32, _i32, _i64, _i32, ctypes.POINTER(_ComplexesP)]),
@@ -443,10 +444,20 @@ class Plan:
 
     def line15_stats(self) -> dict:
         a, b = ctypes.c_double(), ctypes.c_double()
-        c, d = _i64(), _i64()
+        c, d, e = _i64(), _i64(), _i32()
         _check(_lib.wpm_plan_line15_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
-                                          ctypes.byref(d)))
-        return {"ms_canon": a.value, "ms_dedupe": b.value, "labelings": int(c.value), "placements": int(d.value)}
+                                          ctypes.byref(d), ctypes.byref(e)))
+        return {"ms_canon": a.value, "ms_dedupe": b.value, "labelings": int(c.value), "placements": int(d.value),
+                "launches": int(e.value)}
+
+    def line15_costs(self) -> np.ndarray:
+        """placements of each line-13 survivor's canonical-labeling search"""
+        n = _lib.wpm_plan_line15_costs(self._h, None, 0)
+        if n < 0:
+            _check(-n)
+        out = np.zeros(max(n, 1), dtype=np.int64)
+        _lib.wpm_plan_line15_costs(self._h, out.ctypes.data_as(ctypes.POINTER(_i64)), n)
+        return out[:n]
 
     def fetch_complexes(self, which: int = 13) -> "Complexes":
         """The line-7 union (which=7), the line-13 survivors (13), the

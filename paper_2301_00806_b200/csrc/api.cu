@@ -198,7 +198,7 @@ struct wpm_plan {
     DevBuf<uint32_t> d_l15_rows, d_l15_sidx, d_l15_iota, d_l15_rep;
     DevBuf<uint8_t> d_l15_first, d_l15_temp;
     DevBuf<int> d_l15_num;
-    DevBuf<unsigned long long> d_l15_ctl;
+    DevBuf<unsigned long long> d_l15_ctl, d_l15_cost;
     long long line15 = -1, l15_leaves = 0, l15_steps = 0;
     int l15_kmax = 0, l15_mnfcap = 0, l15_launches = 0;
     float ms_canon = 0, ms_dedupe = 0;
@@ -1122,7 +1122,8 @@ extern "C" int wpm_plan_line15(wpm_plan_t* P, int64_t* line15_out) {
     const size_t tdd = l15_dedupe_temp_bytes(std::max<long long>(cnt, 1), gw);
     if (P->d_l15_rows.ensure((size_t)std::max<long long>(cnt, 1) * gw) || P->d_l15_sidx.ensure(cnt + 1) ||
         P->d_l15_iota.ensure(cnt + 1) || P->d_l15_rep.ensure(cnt + 1) || P->d_l15_first.ensure(cnt + 1) ||
-        P->d_l15_temp.ensure(tdd) || P->d_l15_num.ensure(2) || P->d_l15_ctl.ensure(4))
+        P->d_l15_temp.ensure(tdd) || P->d_l15_num.ensure(2) || P->d_l15_ctl.ensure(4) ||
+        P->d_l15_cost.ensure(cnt + 1))
         return fail(WPM_EINTERNAL, "device allocation failed (line 15)");
     CU(cudaEventRecord(P->ev[0], P->stream));
     if (l15_max_facets(P->d_l13_rows.p, gw, P->d_l13_sidx.p, cnt, P->d_l15_num.p, P->stream))
@@ -1130,9 +1131,10 @@ extern "C" int wpm_plan_line15(wpm_plan_t* P, int64_t* line15_out) {
     int kmax = 0;
     CU(cudaMemcpyAsync(&kmax, P->d_l15_num.p, 4, cudaMemcpyDeviceToHost, P->stream));
     CU(cudaStreamSynchronize(P->stream));
-    // minimal non-faces: ~k for Picard-4 seeds; the kernel flags an overflow
-    // and the launch repeats with twice the room (rare, exact either way)
-    int mnfcap = std::max(64, 2 * kmax);
+    // minimal non-faces: a few dozen for Picard-4 seeds (<= 64 measured for
+    // n <= 11); the kernel flags an overflow and the launch repeats with
+    // twice the room (exact either way)
+    int mnfcap = 64;
     unsigned long long ctl[4] = {0, 0, 0, 0};
     P->l15_launches = 0;
     for (;;) {
@@ -1141,7 +1143,7 @@ extern "C" int wpm_plan_line15(wpm_plan_t* P, int64_t* line15_out) {
             return fail(WPM_EINTERNAL, "line 15: complexes too large for the device layout");
         ++P->l15_launches;
         if (l15_launch(L, P->d_l13_rows.p, P->d_l13_sidx.p, nullptr, P->d_unrank.p, nullptr, nullptr, cnt,
-                       P->d_l15_rows.p, nullptr, nullptr, P->d_l15_ctl.p, P->num_sms, P->stream))
+                       P->d_l15_rows.p, nullptr, nullptr, P->d_l15_cost.p, P->d_l15_ctl.p, P->num_sms, P->stream))
             return fail(WPM_EINTERNAL, std::string("line 15 canonical forms: ") +
                                            cudaGetErrorString(cudaGetLastError()));
         CU(cudaMemcpyAsync(ctl, P->d_l15_ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, P->stream));
@@ -1169,9 +1171,22 @@ extern "C" int wpm_plan_line15(wpm_plan_t* P, int64_t* line15_out) {
     return WPM_OK;
 }
 
+// per-survivor search cost of the last wpm_plan_line15 (placements), survivor order
+extern "C" int64_t wpm_plan_line15_costs(wpm_plan_t* P, int64_t* out, int64_t cap) {
+    if (!P) return -fail(WPM_EINVAL, "null plan");
+    if (P->line15 < 0) return -fail(WPM_EINVAL, "call wpm_plan_line15 first");
+    const long long n = std::min<long long>(cap, P->line13);
+    if (n > 0 && (cudaMemcpyAsync(out, P->d_l15_cost.p, (size_t)n * 8, cudaMemcpyDeviceToHost, P->stream) !=
+                      cudaSuccess ||
+                  cudaStreamSynchronize(P->stream) != cudaSuccess))
+        return -fail(WPM_EINTERNAL, "line 15 costs: copy failed");
+    return P->line13;
+}
+
 extern "C" int wpm_plan_line15_stats(const wpm_plan_t* P, double* ms_canon, double* ms_dedupe, int64_t* labelings,
-                                     int64_t* placements) {
+                                     int64_t* placements, int32_t* launches) {
     if (!P) return fail(WPM_EINVAL, "null plan");
+    if (launches) *launches = P->l15_launches;
     if (ms_canon) *ms_canon = P->ms_canon;
     if (ms_dedupe) *ms_dedupe = P->ms_dedupe;
     if (labelings) *labelings = P->l15_leaves;
@@ -1410,7 +1425,7 @@ extern "C" int wpm_canonical_forms(int32_t m, int32_t n, int64_t count, const in
                    cudaMemcpyAsync(doff.p, offsets, (count + 1) * 8, cudaMemcpyHostToDevice, P->stream)) {
             rc = fail(WPM_EINTERNAL, "canonical forms: upload failed");
         } else {
-            int mnfcap = std::max(64, 2 * kmax);
+            int mnfcap = 64;
             for (;;) {
                 const L15Layout L = l15_layout(m, n, kmax, mnfcap, 1);
                 if (L.P > 2048 || l15_smem_bytes(L) > 227 * 1024) {
@@ -1419,7 +1434,7 @@ extern "C" int wpm_canonical_forms(int32_t m, int32_t n, int64_t count, const in
                 }
                 unsigned long long ctl[4] = {0, 0, 0, 0};
                 if (l15_launch(L, nullptr, nullptr, nullptr, nullptr, dm.p, doff.p, count, nullptr, dout.p,
-                               classes_out ? dcls.p : nullptr, dctl.p, P->num_sms, P->stream) ||
+                               classes_out ? dcls.p : nullptr, nullptr, dctl.p, P->num_sms, P->stream) ||
                     cudaMemcpyAsync(ctl, dctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, P->stream) ||
                     cudaStreamSynchronize(P->stream)) {
                     rc = fail(WPM_EINTERNAL, std::string("canonical forms: ") +

@@ -51,6 +51,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "wpm_internal.h"
 
@@ -134,6 +135,7 @@ struct L15Out {
     uint32_t* rows;             // row mode: gw words per complex
     uint16_t* masks;            // csr mode: canonical masks at the input offsets
     int8_t* cls;                // optional: refined class per vertex (16 per complex)
+    unsigned long long* cost;   // optional: single-vertex placements per complex
     unsigned long long* ctl;    // [0] ticket, [1] overflow, [2] labelings completed, [3] placements
 };
 
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(32 * L15_WARPS) l15_canon(L15Src src, L15Out o
     int* misc = reinterpret_cast<int*>(base + L.o_misc);
     int* seqoff = misc;                                        // [17]
     uint16_t* clsmask = reinterpret_cast<uint16_t*>(misc + 20);  // [16]
-    int* lo = misc + 28;                                       // [17]
+    uint8_t* clsrange = reinterpret_cast<uint8_t*>(misc + 28);  // [2 * 16] first / last label per class
     uint32_t* rowbuf = reinterpret_cast<uint32_t*>(misc + 48);  // [gw]
 
     const int m = L.m;
@@ -171,6 +173,7 @@ __global__ void __launch_bounds__(32 * L15_WARPS) l15_canon(L15Src src, L15Out o
         if (ci >= count) break;
 
         // ---- 0. the facet list (0-based masks, ascending)
+        unsigned long long c_steps = 0;
         int k = 0;
         if (src.rows) {
             const uint32_t* row = src.rows + (size_t)(src.idx ? src.idx[ci] : ci) * L.gw;
@@ -218,11 +221,16 @@ __global__ void __launch_bounds__(32 * L15_WARPS) l15_canon(L15Src src, L15Out o
             __syncwarp();
         }
 
-        // ---- 2. minimal non-faces: not a face, every one-smaller subset a face
+        // ---- 2. minimal non-faces: not a face, every one-smaller subset a face.
+        // The reference's face set has no empty face (faces_by_card erases it,
+        // complex.hpp:185), so no singleton is ever minimal -- not even a
+        // ghost vertex's (complex.hpp:199-202 candidates fail :210-217)
+        if (lane == 0) fb[0] &= ~1u;
+        __syncwarp();
         const uint32_t valid = m >= 5 ? FULL : ((1u << (1 << m)) - 1u);
         for (int w = lane; w < W; w += 32) {
             const uint32_t f = fb[w];
-            uint32_t x = ~f & valid;
+            uint32_t x = ~f & valid & (w == 0 ? ~1u : FULL);
             for (int b = 0; b < lowb; ++b) x &= (f << (1 << b)) | low_half_mask(b);
             for (int b = 5; b < m; ++b) {
                 const int bit = 1 << (b - 5);
@@ -389,46 +397,89 @@ __global__ void __launch_bounds__(32 * L15_WARPS) l15_canon(L15Src src, L15Out o
         if (out.cls && lane < 16) out.cls[ci * 16 + lane] = lane < m ? (int8_t)rank : (int8_t)-1;
 
         // ---- 4. least relabeled facet list over the class-respecting labelings
-        // slot t (label t, mask bit t) belongs to class slotcls(t)
-        int myslotcls = 0;
+        // (class c owns the c-th consecutive label range, :232-288), by an
+        // exact branch and bound over single placements.  Two placement
+        // orders, both enumerating every such labeling:
+        //  * facet mode: labels 0, 1, ... in turn.  Each facet's final mask
+        //    is at least its placed labels plus, per class, the lowest labels
+        //    that class still has free for the facet's unplaced vertices (a
+        //    facet that is complete is exact).  The final ascending list then
+        //    dominates the ascending list of these bounds elementwise, so if
+        //    the bounds' list is above the best list at their first
+        //    difference, every completion is: prune.  In counts: with x_B =
+        //    the least best mask no bound hits and x_L = the least bound
+        //    value hit more often than the best list has it, prune iff x_B <
+        //    x_L;
+        //  * co-facet mode: labels m-1, m-2, ... in turn, on the co-facets
+        //    [m] \ F.  The facet list ascending is least iff the co-facet
+        //    list descending is greatest (complement reverses the order);
+        //    bounds from above (the highest free labels per class), mirror
+        //    rule with maxima.
+        // Co-facets of a Picard-4 complex have 4 vertices, so their bounds
+        // tighten after 4 placements where facet bounds need ~n.
+        const bool comode = L.mode == 2 || (L.mode == 0 && (m - L.n) <= L.n);
+        int myslotcls = 0;  // lane s: class of the label placed at depth s
         {
+            const int lab = comode ? m - 1 - lane : lane;
             int acc = 0;
             for (int r = 0; r < ncls; ++r) {
                 const int sz = __popc(clsmask[r]);
-                if (lane >= acc && lane < acc + sz) myslotcls = r;
+                if (lab >= acc && lab < acc + sz) myslotcls = r;
+                if (lane == r) {
+                    clsrange[2 * r] = (uint8_t)acc;
+                    clsrange[2 * r + 1] = (uint8_t)(acc + sz - 1);
+                }
                 acc += sz;
             }
         }
+        unsigned long long rankpack = 0;  // 4-bit class of every vertex
+        for (int v = 0; v < m; ++v) rankpack |= (unsigned long long)(__shfl_sync(FULL, rank, v) & 15) << (4 * v);
         for (int w = lane; w < W; w += 32) {
-            fb[w] = 0u;  // current list
+            fb[w] = 0u;  // scratch: bound values of the current node
             mb[w] = 0u;  // best list
         }
         for (int j = lane; j < k; j += 32) rm[j] = 0;
         __syncwarp();
+        uint16_t* bnd = reinterpret_cast<uint16_t*>(base + L.o_bnd);  // per item: its bound at the current node
         bool have_best = false;
         uint32_t taken = 0;
         int t = 0;
-        int my_v = 0;           // lane t: vertex at depth t
+        int my_v = 0;           // lane t: vertex placed at depth t
         uint32_t my_tried = 0;  // lane t: vertices tried at depth t
-        int my_less = 0;        // lane t: branch already below the best at depth t
+        int best_v = -1;        // lane t: vertex at depth t on the best leaf's path
+        int ngen = 0;                 // automorphisms found (lane g holds number g)
+        unsigned long long gen = 0;   // lane g: image of every vertex, 4 bits each
+        uint32_t gen_fix = 0;         // lane g: the vertices it fixes
+        auto item_of = [&](int j) -> uint32_t { return comode ? (vall & ~(uint32_t)fl[j]) : (uint32_t)fl[j]; };
         auto undo = [&](int v, int tt) {
             const uint32_t vb = 1u << v;
-            for (int j = lane; j < k; j += 32) {
-                const uint32_t f = fl[j];
-                if (!(f & vb)) continue;
-                if (!(f & ~taken)) {
-                    const uint32_t x = rm[j];
-                    atomicAnd(&fb[x >> 5], ~(1u << (x & 31)));
-                }
-                rm[j] = (uint16_t)(rm[j] & ~(1u << tt));
-            }
+            const int lab = comode ? m - 1 - tt : tt;
+            for (int j = lane; j < k; j += 32)
+                if (item_of(j) & vb) rm[j] = (uint16_t)(rm[j] & ~(1u << lab));
             taken &= ~vb;
             __syncwarp();
         };
         for (;;) {
             const int scls = __shfl_sync(FULL, myslotcls, t);
             const uint32_t tried = __shfl_sync(FULL, my_tried, t);
-            const uint32_t cand = clsmask[scls] & ~taken & ~tried;
+            uint32_t cand = clsmask[scls] & ~taken & ~tried;
+            if (ngen && tried && cand) {
+                // orbit pruning: a candidate in the orbit of a finished
+                // sibling under the found automorphisms that fix this prefix
+                // pointwise roots an image of that sibling's subtree
+                const bool use = lane < ngen && (taken & ~gen_fix) == 0u;
+                uint32_t orb = tried;
+                for (;;) {
+                    uint32_t img = 0;
+                    if (use)
+                        for (uint32_t x = orb; x; x &= x - 1)
+                            img |= 1u << (uint32_t)((gen >> (4 * (__ffs(x) - 1))) & 15ull);
+                    img = __reduce_or_sync(FULL, img) | orb;
+                    if (img == orb) break;
+                    orb = img;
+                }
+                cand &= ~orb;
+            }
             if (!cand) {
                 if (lane == t) my_tried = 0;
                 if (t == 0) break;
@@ -442,76 +493,136 @@ __global__ void __launch_bounds__(32 * L15_WARPS) l15_canon(L15Src src, L15Out o
                 my_v = v;
             }
             ++n_steps;
-            // place v at label t
+            ++c_steps;
+            const int lab = comode ? m - 1 - t : t;
             taken |= 1u << v;
-            uint32_t x = INF32;  // least new complete mask missing from the best list
+            // place v; bound every item; mark the bound values (dups = hit twice)
+            uint32_t xu = comode ? 0u : INF32;  // extreme bound value the best list lacks or has fewer of
+            bool incomplete = false;
             for (int j = lane; j < k; j += 32) {
-                const uint32_t f = fl[j];
-                if (!((f >> v) & 1u)) continue;
-                const uint32_t r = rm[j] | (1u << t);
-                rm[j] = (uint16_t)r;
-                if (!(f & ~taken)) {
-                    atomicOr(&fb[r >> 5], 1u << (r & 31));
-                    if (have_best && !((mb[r >> 5] >> (r & 31)) & 1u)) x = min(x, r);
+                const uint32_t f = item_of(j);
+                uint32_t r = rm[j];
+                if ((f >> v) & 1u) {
+                    r |= 1u << lab;
+                    rm[j] = (uint16_t)r;
+                }
+                uint32_t free_v = f & ~taken;
+                incomplete |= free_v != 0u;
+                unsigned long long used = 0;  // 4-bit per-class count of free labels taken
+                for (; free_v; free_v &= free_v - 1) {
+                    const int u = __ffs(free_v) - 1;
+                    const int cl = (int)((rankpack >> (4 * u)) & 15ull);
+                    const int c = (int)((used >> (4 * cl)) & 15ull);
+                    used += 1ull << (4 * cl);
+                    if (comode) r |= 1u << (min((int)clsrange[2 * cl + 1], lab - 1) - c);
+                    else r |= 1u << (max((int)clsrange[2 * cl], t + 1) + c);
+                }
+                bnd[j] = (uint16_t)r;
+                const uint32_t old = atomicOr(&fb[r >> 5], 1u << (r & 31));
+                if (have_best) {
+                    const bool dup = (old >> (r & 31)) & 1u;
+                    const bool in_best = (mb[r >> 5] >> (r & 31)) & 1u;
+                    if (dup || !in_best) xu = comode ? max(xu, r + 1u) : min(xu, r);
                 }
             }
             __syncwarp();
-            const int parent_less = t > 0 ? __shfl_sync(FULL, my_less, t - 1) : 0;
-            int less = 1;
-            if (have_best && !parent_less) {
-                x = __reduce_min_sync(FULL, x);
-                uint32_t y = INF32;  // least best mask of this range missing from the current list
-                for (int j = lo[t] + lane; j < lo[t + 1]; j += 32) {
+            const bool leaf = t == m - 1 || (comode && !__any_sync(FULL, incomplete));
+            int verdict = 1;  // -1 prune, 0 equal to the best (leaf), 1 continue / new best
+            if (have_best) {
+                uint32_t xb = comode ? 0u : INF32;  // extreme best value no bound hits
+                for (int j = lane; j < k; j += 32) {
                     const uint32_t b = best[j];
-                    if (!((fb[b >> 5] >> (b & 31)) & 1u)) y = min(y, b);
+                    if (!((fb[b >> 5] >> (b & 31)) & 1u)) xb = comode ? max(xb, b + 1u) : min(xb, b);
                 }
-                y = __reduce_min_sync(FULL, y);
-                if (x == INF32 && y == INF32) less = 0;
-                else if (x < y) less = 1;
-                else less = -1;
+                if (comode) {
+                    xu = __reduce_max_sync(FULL, xu);
+                    xb = __reduce_max_sync(FULL, xb);
+                    verdict = xb > xu ? -1 : (xb == 0u && xu == 0u ? 0 : 1);
+                } else {
+                    xu = __reduce_min_sync(FULL, xu);
+                    xb = __reduce_min_sync(FULL, xb);
+                    verdict = xb < xu ? -1 : (xb == INF32 && xu == INF32 ? 0 : 1);
+                }
             }
-            if (less < 0) {  // above the best: prune
-                undo(v, t);
-                continue;
-            }
-            if (lane == t) my_less = less;
-            if (t == m - 1) {
+            int jump = -1;
+            if (leaf) {
+                // every bound is exact here: a new best iff the list is below the best
                 ++n_leaves;
-                if (less) {  // a new best: copy the current list (bitmap + ascending list)
+                if (verdict == 0) {
+                    // a leaf equal to the best: best^-1 o current is an
+                    // automorphism fixing the common prefix of the two paths
+                    // and mapping this path's vertex at the first differing
+                    // depth d onto the best path's -- so this depth-d branch
+                    // is the image of the (finished) branch that holds the
+                    // best, and nothing under it can be below the best
+                    const uint32_t diff = __ballot_sync(FULL, lane <= t && my_v != best_v);
+                    if (diff) jump = __ffs(diff) - 1;
+                    if (diff && ngen < 32) {  // keep the automorphism: my_v[d] -> best_v[d], identity elsewhere
+                        unsigned long long g = 0;
+                        uint32_t moved = 0;
+                        for (int d = 0; d <= t; ++d) {
+                            const int a = __shfl_sync(FULL, my_v, d), b = __shfl_sync(FULL, best_v, d);
+                            g |= (unsigned long long)b << (4 * a);
+                            if (a != b) moved |= 1u << a;
+                        }
+                        for (uint32_t x = vall & ~taken; x; x &= x - 1) {
+                            const int a = __ffs(x) - 1;
+                            g |= (unsigned long long)a << (4 * a);
+                        }
+                        if (lane == ngen) {
+                            gen = g;
+                            gen_fix = vall & ~moved;
+                        }
+                        ++ngen;
+                    }
+                }
+                if (verdict > 0) {
+                    best_v = lane <= t ? my_v : -1;
+                    for (int w = lane; w < W; w += 32) mb[w] = fb[w];
+                    __syncwarp();
                     int kk = 0;
                     for (int b0 = 0; b0 < W; b0 += 32) {
                         const int w = b0 + lane;
-                        uint32_t y = w < W ? fb[w] : 0u;
-                        if (w < W) mb[w] = y;
+                        uint32_t y = w < W ? mb[w] : 0u;
                         const int c = __popc(y);
                         const int inc = warp_incl_scan(c, lane);
                         int pos = kk + inc - c;
                         for (; y; y &= y - 1) best[pos++] = (uint16_t)(w * 32 + __ffs(y) - 1);
                         kk += __shfl_sync(FULL, inc, 31);
                     }
-                    __syncwarp();
-                    if (lane <= m) {  // lo[t] = #best masks below 2^t
-                        int a = 0, b = k;
-                        const uint32_t key = 1u << lane;
-                        while (a < b) {
-                            const int mid = (a + b) >> 1;
-                            if (best[mid] < key) a = mid + 1;
-                            else b = mid;
-                        }
-                        lo[lane] = a;
-                    }
                     have_best = true;
-                    my_less = 0;  // the path now equals the best
-                    __syncwarp();
                 }
+            }
+            for (int j = lane; j < k; j += 32) {
+                const uint32_t r = bnd[j];
+                atomicAnd(&fb[r >> 5], ~(1u << (r & 31)));
+            }
+            __syncwarp();
+            if (leaf || verdict < 0) {
                 undo(v, t);
+                while (jump >= 0 && t > jump) {
+                    if (lane == t) my_tried = 0;
+                    --t;
+                    undo(__shfl_sync(FULL, my_v, t), t);
+                }
                 continue;
             }
             ++t;
             if (lane == t) my_tried = 0;
         }
+        // best[] holds the ascending list of facet masks (facet mode) or of
+        // co-facet masks (co-facet mode: facet j is the complement of
+        // best[k - 1 - j])
+        if (comode) {
+            __syncwarp();
+            for (int j = lane; j < k; j += 32) rm[j] = (uint16_t)(vall & ~(uint32_t)best[k - 1 - j]);
+            __syncwarp();
+            for (int j = lane; j < k; j += 32) best[j] = rm[j];
+            __syncwarp();
+        }
 
         // ---- output
+        if (out.cost && lane == 0) out.cost[ci] = c_steps;
         if (src.rows) {
             for (int w = lane; w < L.gw; w += 32) rowbuf[w] = 0u;
             __syncwarp();
@@ -610,18 +721,29 @@ L15Layout l15_layout(int m, int n, int kmax, int mnfcap, int gw) {
     L.seqcap = n * L.kmax + (n + 1) * L.mnfcap;
     L.bmw = m >= 5 ? (1 << (m - 5)) : 1;
     L.gw = gw;
+    // placement order: 0 = by shape (co-facets when they are the smaller side),
+    // 1 = facets, 2 = co-facets; WPM_L15_MODE overrides (experiments)
+    L.mode = 0;
+    if (const char* e = std::getenv("WPM_L15_MODE")) L.mode = std::atoi(e);
     auto al = [](int x) { return (x + 15) & ~15; };
-    int o = 0;
-    L.o_keys = o;  o += al(P * 8);
-    L.o_fb = o;    o += al(L.bmw * 4);
-    L.o_mb = o;    o += al(L.bmw * 4);
+    // phase-3 scratch (sort keys, ids, env sequences) overlays the two
+    // bitmaps: the face / non-face bitmaps are dead once the minimal
+    // non-faces are listed, the current / best bitmaps are born after the
+    // classes are refined
+    L.o_fb = 0;
+    L.o_mb = al(L.bmw * 4);
+    const int end4 = L.o_mb + al(L.bmw * 4);
+    L.o_keys = 0;
+    L.o_ids = al(P * 8);
+    L.o_seq = L.o_ids + al(P * 2);
+    const int end3 = L.o_seq + al(L.seqcap * 2);
+    int o = std::max(end3, end4);
     L.o_misc = o;  o += al((48 + std::max(gw, 1)) * 4);
     L.o_fl = o;    o += al(L.kmax * 2);
     L.o_rm = o;    o += al(L.kmax * 2);
     L.o_best = o;  o += al(L.kmax * 2);
+    L.o_bnd = o;   o += al(L.kmax * 2);
     L.o_mnf = o;   o += al(L.mnfcap * 2);
-    L.o_ids = o;   o += al(P * 2);
-    L.o_seq = o;   o += al(L.seqcap * 2);
     L.bytes = o;
     return L;
 }
@@ -630,8 +752,8 @@ size_t l15_smem_bytes(const L15Layout& L) { return (size_t)L.bytes * L15_WARPS; 
 
 int l15_launch(const L15Layout& L, const uint32_t* d_rows, const uint32_t* d_idx, const int* d_num,
                const uint16_t* d_unrank, const uint16_t* d_masks, const long long* d_off, long long count,
-               uint32_t* d_out_rows, uint16_t* d_out_masks, int8_t* d_cls, unsigned long long* d_ctl, int num_sms,
-               cudaStream_t st) {
+               uint32_t* d_out_rows, uint16_t* d_out_masks, int8_t* d_cls, unsigned long long* d_cost,
+               unsigned long long* d_ctl, int num_sms, cudaStream_t st) {
     if (count <= 0) return 0;
     const size_t smem = l15_smem_bytes(L);
     if (smem > 227 * 1024) return 1;
@@ -643,7 +765,7 @@ int l15_launch(const L15Layout& L, const uint32_t* d_rows, const uint32_t* d_idx
         return 1;
     const long long blocks = std::min<long long>((count + L15_WARPS - 1) / L15_WARPS, (long long)num_sms * per_sm);
     L15Src src{d_rows, d_idx, d_num, d_unrank, d_masks, d_off, count};
-    L15Out out{d_out_rows, d_out_masks, d_cls, d_ctl};
+    L15Out out{d_out_rows, d_out_masks, d_cls, d_cost, d_ctl};
     if (cudaMemsetAsync(d_ctl, 0, 4 * sizeof(unsigned long long), st) != cudaSuccess) return 1;
     l15_canon<<<(unsigned)blocks, 32 * L15_WARPS, smem, st>>>(src, out, L, make_binom());
     return cudaGetLastError() == cudaSuccess ? 0 : 1;

@@ -111,8 +111,8 @@ int launch_odometer(const OdoParams& p, int Wb, int num_sms, cudaStream_t st);
 // Algorithm 2 line 15 (k7_line15.cu): canonical forms, one warp per
 // complex; per-warp shared-memory layout (byte offsets) sized on the host
 struct L15Layout {
-    int m, n, kmax, mnfcap, P, seqcap, bmw, gw;
-    int o_fl, o_rm, o_fb, o_mb, o_mnf, o_keys, o_ids, o_seq, o_best, o_misc, bytes;
+    int m, n, kmax, mnfcap, P, seqcap, bmw, gw, mode;
+    int o_fl, o_rm, o_fb, o_mb, o_mnf, o_keys, o_ids, o_seq, o_best, o_bnd, o_misc, bytes;
 };
 L15Layout l15_layout(int m, int n, int kmax, int mnfcap, int gw);
 size_t l15_smem_bytes(const L15Layout& L);
@@ -124,8 +124,8 @@ int l15_max_facets(const uint32_t* d_rows, int gw, const uint32_t* d_idx, long l
 // ticket, overflow count (> 0: rerun with a larger mnfcap), labelings, placements
 int l15_launch(const L15Layout& L, const uint32_t* d_rows, const uint32_t* d_idx, const int* d_num,
                const uint16_t* d_unrank, const uint16_t* d_masks, const long long* d_off, long long count,
-               uint32_t* d_out_rows, uint16_t* d_out_masks, int8_t* d_cls, unsigned long long* d_ctl, int num_sms,
-               cudaStream_t st);
+               uint32_t* d_out_rows, uint16_t* d_out_masks, int8_t* d_cls, unsigned long long* d_cost,
+               unsigned long long* d_ctl, int num_sms, cudaStream_t st);
 size_t l15_dedupe_temp_bytes(long long count, int gw);
 int l15_dedupe(const uint32_t* d_rows, long long count, int gw, uint32_t* d_sidx, uint32_t* d_iota, uint8_t* d_first,
                uint32_t* d_rep, int* d_nrep, void* d_temp, size_t temp_bytes, cudaStream_t st);
