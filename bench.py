@@ -359,7 +359,10 @@ def sweep_per_n(wpm, dev, flush, g, ns=range(2, 12), reps=3, alg1_max_n=8):
     call with host buffers; parity of counts and nodes against the golden
     file.  Also Algorithm 2 lines 7 / 13 (union + support + seedness filter,
     pipeline.hpp:58-89) on each run's resident result: device ms and counts
-    against golden.json["line13"]; and, for n <= alg1_max_n, the reference's
+    against golden.json["line13"]; line 15 (canonical forms + class dedupe,
+    pipeline.hpp:91-103) likewise against golden.json["line15"] (the
+    reference for n <= 7, the paper's counts for n = 8..10); and, for
+    n <= alg1_max_n, the reference's
     own algorithm (kernel basis + every combination-space leaf on the GPU):
     the reference's work unit (leaves) per second, apples to apples."""
     import torch
@@ -368,7 +371,7 @@ def sweep_per_n(wpm, dev, flush, g, ns=range(2, 12), reps=3, alg1_max_n=8):
     for n in ns:
         with wpm.Plan.orbits(n, device=dev) as p:
             p.run()
-            runs, l13 = [], []
+            runs, l13, l15 = [], [], []
             for _ in range(reps):
                 flush.zero_()
                 torch.cuda.synchronize(dev)
@@ -379,12 +382,20 @@ def sweep_per_n(wpm, dev, flush, g, ns=range(2, 12), reps=3, alg1_max_n=8):
                 lines = p.line13()
                 lt = p.line13_timing()
                 l13.append((lt["ms_union"] + lt["ms_filter"], lt["ms_union"], lt["ms_filter"], lines))
+                # Algorithm 2 line 15 on the resident survivors (k7_line15.cu)
+                c15 = p.line15()
+                s15 = p.line15_stats()
+                l15.append((s15["ms_canon"] + s15["ms_dedupe"], s15["ms_canon"], s15["ms_dedupe"], c15,
+                            s15["placements"]))
             total = p.fetch().total
         runs.sort()
         ms, ms_search, ms_sort, nodes = runs[len(runs) // 2]
         l13.sort()
         ms13, ms_union, ms_filter, (line7, line13) = l13[len(l13) // 2]
         want13 = g.get("line13", {}).get(str(n), {})
+        l15.sort()
+        ms15, ms_canon, ms_dedupe, line15, placements = l15[len(l15) // 2]
+        want15 = g.get("line15", {}).get(str(n), {})
         want = g["dfs"][str(n)]
         alg1 = None
         if n <= alg1_max_n:
@@ -424,6 +435,10 @@ def sweep_per_n(wpm, dev, flush, g, ns=range(2, 12), reps=3, alg1_max_n=8):
                      "line13": {"line7": line7, "line13": line13, "ms": round(ms13, 3), "ms_union": round(ms_union, 3),
                                 "ms_filter": round(ms_filter, 3),
                                 "parity_ok": (line7, line13) == (want13.get("line7"), want13.get("line13"))},
+                     "line15": {"line15": line15, "ms": round(ms15, 3), "ms_canon": round(ms_canon, 3),
+                                "ms_dedupe": round(ms_dedupe, 3), "placements": placements,
+                                "ref_canon_s": want15.get("ref_canon_s"), "ref_threads": want15.get("threads"),
+                                "parity_ok": None if "line15" not in want15 else line15 == want15["line15"]},
                      "alg1": alg1})
         del r
     return rows
