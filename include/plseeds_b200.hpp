@@ -18,6 +18,8 @@
 //      write_complex(es)    complex_io.hpp:21-39
 //      pipeline_line13      pipeline.hpp:52-89 lines 1-13 (union, support, is_seed on the GPU)
 //      is_seed              classify.hpp:51-53 (batch, on the GPU)
+//      canonical_form       isomorphism.hpp:228-303 (batch, on the GPU)
+//      pipeline_line15      pipeline.hpp:52-103 lines 1-15 (+ canonical forms, class dedupe)
 //      purity_error, cap_exceeded_error, format_error   errors.hpp:10-32
 //
 // 2. Inside a program that already includes the reference headers
@@ -352,6 +354,62 @@ inline std::vector<char> is_seed(const std::vector<PureComplex>& list, int devic
 }
 inline bool is_seed(const PureComplex& K, int device = 0) { return is_seed(std::vector<PureComplex>{K}, device)[0]; }
 
+// ---- Algorithm 2 line 15 (pipeline.hpp:91-103) on the device
+
+// canonical_form (isomorphism.hpp:228-303) over a batch; m <= 15, n <= 11
+inline std::vector<PureComplex> canonical_form(const std::vector<PureComplex>& list, int device = 0) {
+    std::vector<PureComplex> out(list.size());
+    std::size_t i = 0;
+    while (i < list.size()) {  // one call per run of equal (m, n)
+        std::size_t j = i;
+        std::vector<std::int64_t> off{0};
+        std::vector<std::uint64_t> fac;
+        while (j < list.size() && list[j].m == list[i].m && list[j].n == list[i].n) {
+            for (const auto& f : list[j].facets) fac.push_back(f.bits);
+            off.push_back(static_cast<std::int64_t>(fac.size()));
+            ++j;
+        }
+        std::vector<std::uint64_t> canon(fac.size() + 1);
+        check(wpm_canonical_forms(list[i].m, list[i].n, static_cast<std::int64_t>(j - i), off.data(), fac.data(),
+                                  device, canon.data(), nullptr));
+        for (std::size_t k = i; k < j; ++k) {
+            PureComplex K;
+            K.m = list[k].m;
+            K.n = list[k].n;
+            for (std::int64_t q = off[k - i]; q < off[k - i + 1]; ++q) K.facets.emplace_back(canon[q]);
+            out[k] = std::move(K);
+        }
+        i = j;
+    }
+    return out;
+}
+inline PureComplex canonical_form(const PureComplex& K, int device = 0) {
+    return canonical_form(std::vector<PureComplex>{K}, device)[0];
+}
+
+// PipelineResult's line7 / line13 / line15 (pipeline.hpp:23-30) and the
+// line-15 representatives (canonical forms, order of first appearance:
+// the `reps` of pipeline.hpp:91-101)
+struct Line15Result {
+    long long line7 = 0, line13 = 0, line15 = 0;
+    std::vector<PureComplex> reps;
+    double ms_canon = 0, ms_dedupe = 0;
+};
+
+// lines 1-15 of pipeline(n, db) (pipeline.hpp:52-103): every orbit map, UBT cap
+inline Line15Result pipeline_line15(int n, int p = 4, int device = 0, std::int64_t facet_cap = WPM_CAP_UBT) {
+    detail::Complexes C;
+    check(wpm_pipeline_line15(n, p, facet_cap, device, &C.c));
+    Line15Result r;
+    r.line7 = C.c->line7;
+    r.line13 = C.c->line13;
+    r.line15 = C.c->line15;
+    r.ms_canon = C.c->ms_canon;
+    r.ms_dedupe = C.c->ms_dedupe;
+    r.reps = detail::complexes_of(C.c);
+    return r;
+}
+
 }  // namespace plseeds_b200
 
 // ---------------------------------------------------------------------------
@@ -455,6 +513,59 @@ struct Line13Result {
     long long line7 = 0, line13 = 0;
     std::vector<PureComplex> survivors;  // pipeline.hpp:74-89, in order
 };
+
+namespace detail {
+inline std::vector<PureComplex> to_ref(const std::vector<plseeds_b200::PureComplex>& in, bool embedded) {
+    std::vector<PureComplex> out;
+    out.reserve(in.size());
+    for (const auto& K : in) {
+        std::vector<VertexSet> fs;
+        fs.reserve(K.facets.size());
+        for (const auto& f : K.facets) fs.emplace_back(f.bits);
+        out.emplace_back(K.m, K.n, std::move(fs), embedded);
+    }
+    return out;
+}
+}  // namespace detail
+
+// canonical_form(K) (isomorphism.hpp:228-303) for a batch, on the device
+inline std::vector<PureComplex> canonical_form(const std::vector<PureComplex>& list, int device = 0) {
+    std::vector<plseeds_b200::PureComplex> in;
+    in.reserve(list.size());
+    for (const auto& K : list) {
+        plseeds_b200::PureComplex k;
+        k.m = K.m;
+        k.n = K.n;
+        for (const auto& f : K.facets) k.facets.emplace_back(f.bits);
+        in.push_back(std::move(k));
+    }
+    const auto canon = plseeds_b200::canonical_form(in, device);
+    std::vector<PureComplex> out;
+    out.reserve(canon.size());
+    for (std::size_t i = 0; i < canon.size(); ++i) {
+        std::vector<VertexSet> fs;
+        fs.reserve(canon[i].facets.size());
+        for (const auto& f : canon[i].facets) fs.emplace_back(f.bits);
+        out.emplace_back(list[i].m, list[i].n, std::move(fs), list[i].embedded);  // isomorphism.hpp:302
+    }
+    return out;
+}
+
+struct Line15Result {
+    long long line7 = 0, line13 = 0, line15 = 0;
+    std::vector<PureComplex> reps;  // pipeline.hpp:91-101, first-appearance order
+};
+
+// lines 1-15 of pipeline(n, db) (pipeline.hpp:52-103) with the reference's types
+inline Line15Result pipeline_line15(int n, int device = 0) {
+    const auto r = plseeds_b200::pipeline_line15(n, 4, device);
+    Line15Result out;
+    out.line7 = r.line7;
+    out.line13 = r.line13;
+    out.line15 = r.line15;
+    out.reps = detail::to_ref(r.reps, false);
+    return out;
+}
 
 // lines 1-13 of pipeline(n, db) (pipeline.hpp:52-89) with the reference's types
 inline Line13Result pipeline_line13(int n, int device = 0) {

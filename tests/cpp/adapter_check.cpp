@@ -16,6 +16,7 @@
 #include "plseeds/classify.hpp"
 #include "plseeds/pipeline.hpp"
 #include "plseeds/search.hpp"
+#include "plseeds/isomorphism.hpp"
 #include "plseeds_b200.hpp"
 
 using namespace plseeds;
@@ -132,6 +133,41 @@ int main() {
         for (std::size_t i = 0; i < cat.size(); ++i)
             if ((got[i] != 0) != is_seed(cat[i])) {
                 std::printf("MISMATCH is_seed catalog %zu\n", i);
+                ++failures;
+            }
+        ++jobs;
+    }
+    // Algorithm 2 line 15 (pipeline.hpp:91-103): the reference's canonical
+    // forms and first-appearance representatives, n = 2..4
+    for (int n = 2; n <= 4; ++n) {
+        const auto l13 = b200::pipeline_line13(n);
+        std::vector<PureComplex> reps;
+        std::set<std::vector<VertexSet>> seen;
+        for (const auto& K : l13.survivors) {
+            auto c = canonical_form(K);
+            if (seen.insert(c.facets).second) reps.push_back(std::move(c));
+        }
+        const auto got = b200::pipeline_line15(n);
+        if (got.line15 != (long long)reps.size() || !(got.reps == reps)) {
+            std::printf("MISMATCH line15 n=%d: reference %zu, b200 %lld\n", n, reps.size(), got.line15);
+            ++failures;
+        }
+        const auto canon = b200::canonical_form(l13.survivors);
+        for (std::size_t i = 0; i < canon.size(); ++i)
+            if (!(canon[i] == canonical_form(l13.survivors[i]))) {
+                std::printf("MISMATCH canonical_form n=%d survivor %zu\n", n, i);
+                ++failures;
+                break;
+            }
+        ++jobs;
+    }
+    {  // canonical_form on catalog complexes with large automorphism groups
+        const std::vector<PureComplex> cat = {s0(), square(), hexagon(), octahedron(), pentagon(),
+                                              suspension(pentagon()), suspension(octahedron()), wedge(square(), 1)};
+        const auto got = b200::canonical_form(cat);
+        for (std::size_t i = 0; i < cat.size(); ++i)
+            if (!(got[i] == canonical_form(cat[i]))) {
+                std::printf("MISMATCH canonical_form catalog %zu\n", i);
                 ++failures;
             }
         ++jobs;
