@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <unordered_map>
 #include <chrono>
@@ -228,49 +229,140 @@ extern "C" int64_t wpm_cyclic_facet_bound(int32_t n) { return cyclic_bound(n); }
 // (column permutation) orbit of injective [M; I_p]; representative = the
 // lexicographically least sorted row list over the p! bit shuffles; the
 // representatives sorted; identity rows appended.
+// idcm_orbits (charmap.hpp:212-281): one representative per S_n x S_p orbit
+// of injective dual matrices [M; I_p] -- the lex-min sorted row list over the
+// p! column permutations (:237-249), representatives in sorted order
+// (:268), identity rows appended (:277).  A row set is a bitmask over the
+// 2^p vectors; for sets of equal size the sorted-list order is "the set
+// holding the lowest element of the symmetric difference is smaller", and a
+// column permutation acts on a mask through per-byte lookup tables built
+// once per p (0.35 ms -> ~0.03 ms per call at n = 5).
+namespace {
+struct OrbitTables {
+    int p = 0, words = 0;                       // mask words of 64 bits over 2^p vectors
+    std::vector<std::vector<uint32_t>> img;     // per permutation: image of every vector
+    std::vector<uint64_t> byte_img;             // [perm][chunk][byte][word] -> image mask words
+};
+inline bool set_less(const uint64_t* a, const uint64_t* b, int words) {
+    for (int w = 0; w < words; ++w) {
+        const uint64_t x = a[w] ^ b[w];
+        if (x) return (a[w] & (x & (0 - x))) != 0;
+    }
+    return false;
+}
+const OrbitTables& orbit_tables(int p) {
+    static std::mutex mu;
+    static std::map<int, OrbitTables> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(p);
+    if (it != cache.end()) return it->second;
+    OrbitTables T;
+    T.p = p;
+    const int nv = 1 << p;
+    T.words = (nv + 63) / 64;
+    std::vector<int> perm(p);
+    std::iota(perm.begin(), perm.end(), 0);
+    do {
+        std::vector<uint32_t> im(nv, 0);
+        for (int v = 0; v < nv; ++v)
+            for (int b = 0; b < p; ++b)
+                if ((v >> b) & 1) im[v] |= 1u << perm[b];
+        T.img.push_back(std::move(im));
+    } while (std::next_permutation(perm.begin(), perm.end()));
+    const int chunks = (nv + 7) / 8;
+    if (p > 5) return cache.emplace(p, std::move(T)).first->second;  // tables would be too big: direct images
+    T.byte_img.assign(T.img.size() * chunks * 256 * T.words, 0);
+    for (size_t q = 0; q < T.img.size(); ++q)
+        for (int c = 0; c < chunks; ++c)
+            for (int x = 0; x < 256; ++x) {
+                uint64_t* dst = &T.byte_img[(((q * chunks) + c) * 256 + x) * T.words];
+                for (int bit = 0; bit < 8; ++bit) {
+                    const int v = c * 8 + bit;
+                    if (v < nv && ((x >> bit) & 1)) dst[T.img[q][v] >> 6] |= 1ull << (T.img[q][v] & 63);
+                }
+            }
+    return cache.emplace(p, std::move(T)).first->second;
+}
+}  // namespace
+
 extern "C" int32_t wpm_idcm_orbits(int32_t n, int32_t p, uint32_t* rows_out, int32_t cap) {
     if (n < 1 || p < 1 || p > 8) return -fail(WPM_EINVAL, "unsupported (n, p)");
     if (n + p > (1 << p) - 1) return -fail(WPM_EINVAL, "no injective dual matrix: m exceeds 2^p - 1");
-    std::vector<uint32_t> pool;
+    std::vector<uint32_t> pool;  // the non-unit nonzero vectors (rows of M)
     for (uint32_t v = 1; v < (1u << p); ++v)
         if (v & (v - 1)) pool.push_back(v);
     if (n > (int)pool.size()) return -fail(WPM_EINVAL, "no injective dual matrix: m exceeds 2^p - 1");
-    std::vector<int> perm(p);
-    std::iota(perm.begin(), perm.end(), 0);
-    std::vector<std::vector<uint32_t>> shuffles;  // shuffles[q][v] = image of v
-    do {
-        std::vector<uint32_t> img(1u << p, 0);
-        for (uint32_t v = 0; v < (1u << p); ++v)
-            for (int b = 0; b < p; ++b)
-                if ((v >> b) & 1u) img[v] |= 1u << perm[b];
-        shuffles.push_back(std::move(img));
-    } while (std::next_permutation(perm.begin(), perm.end()));
-    std::set<std::vector<uint32_t>> reps;
+    const OrbitTables& T = orbit_tables(p);
+    const int W = T.words, chunks = ((1 << p) + 7) / 8;
+    std::vector<uint64_t> reps;  // W words per representative
     std::vector<int> idx(n);
     std::iota(idx.begin(), idx.end(), 0);
-    std::vector<uint32_t> cur(n), best(n);
+    std::vector<uint64_t> cur(W), img(W), best(W);
     const int P = (int)pool.size();
-    for (;;) {
-        bool first = true;
-        for (const auto& img : shuffles) {
-            for (int i = 0; i < n; ++i) cur[i] = img[pool[idx[i]]];
-            std::sort(cur.begin(), cur.end());
-            if (first || cur < best) best = cur;
-            first = false;
+    if (W == 1 && !T.byte_img.empty()) {  // p <= 5: one-word masks, straight-line minimum
+        const size_t Q = T.img.size();
+        const uint64_t* tab = T.byte_img.data();
+        for (;;) {
+            uint64_t c = 0;
+            for (int i = 0; i < n; ++i) c |= 1ull << pool[idx[i]];
+            uint64_t bm = 0;
+            for (size_t q = 0; q < Q; ++q) {
+                uint64_t im = 0;
+                for (int ch = 0; ch < chunks; ++ch) im |= tab[((q * chunks) + ch) * 256 + ((c >> (8 * ch)) & 0xFFu)];
+                const uint64_t x = im ^ bm;
+                if (q == 0 || (im & x & (0 - x))) bm = im;
+            }
+            reps.push_back(bm);
+            int pos = n - 1;
+            while (pos >= 0 && idx[pos] == P - (n - pos)) --pos;
+            if (pos < 0) break;
+            ++idx[pos];
+            for (int i = pos + 1; i < n; ++i) idx[i] = idx[i - 1] + 1;
         }
-        reps.insert(best);
+    } else
+    for (;;) {
+        std::fill(cur.begin(), cur.end(), 0ull);
+        for (int i = 0; i < n; ++i) cur[pool[idx[i]] >> 6] |= 1ull << (pool[idx[i]] & 63);
+        for (size_t q = 0; q < T.img.size(); ++q) {
+            std::fill(img.begin(), img.end(), 0ull);
+            if (T.byte_img.empty()) {
+                for (int i = 0; i < n; ++i) {
+                    const uint32_t y = T.img[q][pool[idx[i]]];
+                    img[y >> 6] |= 1ull << (y & 63);
+                }
+            } else {
+                for (int c = 0; c < chunks; ++c) {
+                    const unsigned x = (unsigned)((cur[(c * 8) >> 6] >> ((c * 8) & 63)) & 0xFFu);
+                    if (!x) continue;
+                    const uint64_t* src = &T.byte_img[(((q * chunks) + c) * 256 + x) * W];
+                    for (int w = 0; w < W; ++w) img[w] |= src[w];
+                }
+            }
+            if (q == 0 || set_less(img.data(), best.data(), W)) best = img;
+        }
+        reps.insert(reps.end(), best.begin(), best.end());
         int pos = n - 1;
         while (pos >= 0 && idx[pos] == P - (n - pos)) --pos;
         if (pos < 0) break;
         ++idx[pos];
         for (int i = pos + 1; i < n; ++i) idx[i] = idx[i - 1] + 1;
     }
+    // sort + unique the representatives (std::set order, :268)
+    const size_t R = reps.size() / W;
+    std::vector<size_t> order(R);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(),
+              [&](size_t a, size_t b) { return set_less(&reps[a * W], &reps[b * W], W); });
     const int m = n + p;
     int k = 0;
-    for (const auto& r : reps) {
+    for (size_t r = 0; r < R; ++r) {
+        const uint64_t* x = &reps[order[r] * W];
+        if (r > 0 && std::equal(x, x + W, &reps[order[r - 1] * W])) continue;
         if (k < cap && rows_out) {
-            for (int i = 0; i < n; ++i) rows_out[(size_t)k * m + i] = r[i];
-            for (int i = 0; i < p; ++i) rows_out[(size_t)k * m + n + i] = 1u << i;
+            int i = 0;
+            for (int w = 0; w < W; ++w)
+                for (uint64_t y = x[w]; y; y &= y - 1) rows_out[(size_t)k * m + i++] = (uint32_t)(w * 64 + __builtin_ctzll(y));
+            for (int j = 0; j < p; ++j) rows_out[(size_t)k * m + n + j] = 1u << j;
         }
         ++k;
     }
@@ -619,6 +711,7 @@ extern "C" int32_t wpm_plan_incidence(wpm_plan_t* P, int32_t map, uint64_t* ridg
 static int plan_sort(wpm_plan* P);
 
 static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
+    Trace tr;
     const int K = P->num_maps;
     // root tasks: (f, map) f-major so the largest subtrees start first;
     // pinned universes get one ENTRY task
@@ -659,6 +752,7 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         P->d_task_map.ensure(ntasks + 1) || P->d_task_f.ensure(ntasks + 1) || P->d_task_kind.ensure(ntasks + 1) ||
         P->d_out_ctl.ensure(4) || P->d_per_map.ensure(K))
         return fail(WPM_EINTERNAL, "device allocation failed (queue)");
+    tr.mark("  run: tasks + queue alloc");
     if (P->has_pins) {
         if (P->d_pin_in.ensure(P->mw) || P->d_pin_out.ensure(P->mw))
             return fail(WPM_EINTERNAL, "device allocation failed (pins)");
@@ -666,12 +760,15 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         CU(cudaMemcpyAsync(P->d_pin_out.p, P->pin_out.data(), P->mw * 4, cudaMemcpyHostToDevice, P->stream));
     }
     if (P->out_cap == 0) {
-        // first run: size the row buffer from free memory (a rerun is only
-        // needed if the WPM count exceeds it; the count is then known)
+        // first run: 2^21 rows covers every Picard-4 n (the most WPMs of any
+        // n is 1.72 M, n = 8); a larger result reruns once with the exact
+        // count.  (Sizing from free memory asked the pool for GBs per plan,
+        // and a pool that had to map them again cost tens of ms per call.)
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
         const unsigned long long row = (unsigned long long)P->rw * 4 * 3;  // keys + sort temp + sorted rows
-        P->out_cap = std::min<unsigned long long>(std::max<unsigned long long>(fr / 16 / row, 1ull << 20), 1ull << 26);
+        P->out_cap = std::min<unsigned long long>(std::max<unsigned long long>(fr / 16 / row, 1ull << 16), 1ull << 21);
+        if (const char* e = std::getenv("WPM_OUT_CAP")) P->out_cap = std::max(1ull, std::strtoull(e, nullptr, 10));
     }
     CU(cudaEventRecord(P->ev[4], P->stream));
     // frame stack sized for the branch depths the search reaches in practice
@@ -727,6 +824,7 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         // O(N) per donated task) -- measured sweep in DESIGN.md
         sp.check_every = P->maxN <= 256 ? 16 : 32;
         if (const char* e = std::getenv("WPM_CHECK_EVERY")) sp.check_every = std::max(1, std::atoi(e));
+        tr.mark("  run: output alloc, H2D, seed");
         CU(cudaEventRecord(P->ev[0], P->stream));
         if (ntasks > 0 && !launch_k3_search(sp, P->num_sms, P->stream, &P->warps))
             return fail(WPM_EINTERNAL, std::string("kernel 3 launch: ") + cudaGetErrorString(cudaGetLastError()));
@@ -734,7 +832,9 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         unsigned long long octl[4], qc[8];
         CU(cudaMemcpyAsync(octl, P->d_out_ctl.p, 32, cudaMemcpyDeviceToHost, P->stream));
         CU(cudaMemcpyAsync(qc, P->d_qctl.p, sizeof(qc), cudaMemcpyDeviceToHost, P->stream));
+        tr.mark("  run: k3 launch");
         CU(cudaStreamSynchronize(P->stream));
+        tr.mark("  run: k3 sync");
         P->h2d += (long long)sizeof(ctl);
         P->d2h += 32 + (long long)sizeof(qc);
         P->total = (long long)octl[0];
@@ -760,6 +860,7 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
 // canonical sort of the key rows in d_out_keys (P->total of them), per-map
 // counts from the group boundaries; shared by the DFS and the odometer runs
 static int plan_sort(wpm_plan* P) {
+    Trace tr;
     const int K = P->num_maps;
     const long long total = P->total;
     const size_t tb = canon_sort_temp_bytes(std::max<long long>(total, 1), P->w32);
@@ -773,11 +874,13 @@ static int plan_sort(wpm_plan* P) {
                         P->d_temp.n, (long long*)P->d_per_map.p, P->d_out_ctl.p + 1, P->stream))
         return fail(WPM_EINTERNAL, std::string("canonical sort: ") + cudaGetErrorString(cudaGetLastError()));
     CU(cudaEventRecord(P->ev[3], P->stream));
+    tr.mark("  sort: alloc + launch");
     unsigned long long dups = 0;
     std::vector<long long> first(K);
     CU(cudaMemcpyAsync(&dups, P->d_out_ctl.p + 1, 8, cudaMemcpyDeviceToHost, P->stream));
     CU(cudaMemcpyAsync(first.data(), P->d_per_map.p, K * 8, cudaMemcpyDeviceToHost, P->stream));
     CU(cudaStreamSynchronize(P->stream));
+    tr.mark("  sort: sync");
     P->d2h += 8 + 8LL * K;
     P->dups = (long long)dups;
     // per-map counts from the group boundaries of the sorted map ids

@@ -88,6 +88,15 @@ struct LC {
     static constexpr int FRAMES = TRAIL + a16(2 * MP);     // uint2 per branch frame
     static constexpr int SCRATCH = FRAMES + a16(8 * (DMAX + 2));  // closing-ridge list
     static constexpr int BYTES = SCRATCH + 64;
+    // CTAs per SM the register budget is cut for: 10 (48 registers, no
+    // spills) up to the n = 8 shapes -- measured +1.5 / +5 / +6 % nodes/s
+    // at n = 5 / 6 / 8 over 8 CTAs (64 registers) -- and 8 for the larger
+    // shapes, whose shared state caps residency anyway (n = 11: -3 % at 10)
+#ifdef K3_MIN_BLOCKS
+    static constexpr int MIN_BLOCKS = K3_MIN_BLOCKS;
+#else
+    static constexpr int MIN_BLOCKS = NMAX <= 720 ? 10 : 8;
+#endif
 };
 
 // size classes (max ridges, max facets, frame capacity): the exact shapes of
@@ -667,7 +676,7 @@ __device__ __forceinline__ void try_donate(WS<C>& w, const MapView& mp, const Se
 }
 
 template <class C>
-__global__ void __launch_bounds__(128, 8) k3_search(const __grid_constant__ SearchParams p) {
+__global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_constant__ SearchParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WS<C> w;

@@ -137,3 +137,14 @@ def test_job_validation_errors(wpm):
         wpm.enumerate_wpm(wpm.SearchJob(4, 2, [0b1100, 0b0110]))  # not canonical order
     with pytest.raises(ValueError):
         wpm.enumerate_wpm(wpm.SearchJob(4, 2, [0b0110], properties=[wpm.AffineProperty([2], 3)]))
+
+
+def test_idcm_orbits_host_matches_goldens(wpm, oracle, golden):
+    """wpm_idcm_orbits (host C++, table-driven) = the reference's orbit
+    representatives (charmap.hpp:212-281), every Picard-4 n, and the oracle
+    for Picard 3 and 5."""
+    for n in range(2, 12):
+        got = [d.rows for d in wpm.idcm_orbits(n, 4)]
+        assert got == golden["orbits"][str(n)], n
+    for n, p in ((2, 3), (3, 3), (4, 3), (2, 5), (3, 5)):  # the oracle returns <= 64 orbits
+        assert [d.rows for d in wpm.idcm_orbits(n, p)] == oracle.idcm_orbits(n, p), (n, p)

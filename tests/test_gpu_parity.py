@@ -313,3 +313,13 @@ def test_cpp_adapter_vs_reference():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 mismatches" in r.stdout
+
+
+def test_output_overflow_reruns_exactly(wpm, golden, monkeypatch):
+    """The row buffer starts at 2^21 rows; a result larger than the buffer
+    reruns once with the exact count (forced here with a 1000-row buffer)."""
+    monkeypatch.setenv("WPM_OUT_CAP", "1000")
+    with wpm.Plan.orbits(4) as p:
+        assert p.run() == golden["dfs"]["4"]["sum"]
+        res = p.fetch()
+    assert res.duplicates == 0 and res.total == golden["dfs"]["4"]["sum"]
