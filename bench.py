@@ -304,6 +304,7 @@ def main():
     if world == 1 and args.per_n:
         plan.close()
         per_n = sweep_per_n(wpm, dev, flush, g)
+        synthetic = sweep_synthetic(wpm, dev, flush, g)
         plan = None
 
     if rank == 0:
@@ -332,6 +333,7 @@ def main():
         }
         if per_n is not None:
             line["per_n"] = per_n
+            line["synthetic"] = synthetic
             row = next((r for r in per_n if r["n"] == n), None)
             if row and row.get("alg1"):
                 # the same algorithm on both sides: the reference's leaves per
@@ -441,6 +443,39 @@ def sweep_per_n(wpm, dev, flush, g, ns=range(2, 12), reps=3, alg1_max_n=8):
                                 "parity_ok": None if "line15" not in want15 else line15 == want15["line15"]},
                      "alg1": alg1})
         del r
+    return rows
+
+
+def sweep_synthetic(wpm, dev, flush, g, densities=(0.75, 0.78, 0.80, 0.85, 0.90, 1.0), seed=1,
+                    budget=2_000_000_000):
+    """BASELINE configs[4]: synthetic candidate-facet sets, (m, n) = (15, 11),
+    cap 252, density sweep.  Full enumeration where it
+    is checkable (parity vs golden.json["synthetic"]); above d = 0.80 a
+    node-budgeted stress run (truncated = True: nodes/s and divergence only)."""
+    import torch
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import catalog as C
+
+    want = {(c["seed"], round(c["d"], 4)): c for c in g.get("synthetic", {}).get("cases", [])}
+    rows = []
+    for d in densities:
+        u = C.synthetic_universe(seed, d)
+        with wpm.Plan.universes(15, 11, [u], facet_cap=252, device=dev) as p:
+            if d > 0.80:
+                p.set_node_budget(budget)
+            p.run()
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            total = p.run()
+            st, tm = p.stats(), p.timing()
+            trunc = p.truncated()
+        w = want.get((seed, round(d, 4)))
+        rows.append({"d": d, "seed": seed, "M": len(u), "wpms": total, "nodes": st["nodes"],
+                     "ms_search": round(st["ms_search"], 3), "ms_step": round(tm["ms_total"], 3),
+                     "nodes_per_s": st["nodes"] / (st["ms_search"] * 1e-3) if st["ms_search"] else None,
+                     "truncated": trunc,
+                     "parity_ok": None if w is None or trunc else (total == w["wpms"] and st["nodes"] == w["nodes"])})
     return rows
 
 

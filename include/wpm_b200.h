@@ -153,6 +153,12 @@ int32_t wpm_plan_incidence(wpm_plan_t *plan, int32_t map, uint64_t *ridges_out, 
 /* Run the search + canonical sort on the device; results stay resident.
  * Returns status; *total_out = number of WPMs. */
 int wpm_plan_run(wpm_plan_t *plan, int32_t shard_index, int32_t shard_count, int64_t *total_out);
+/* Search-node budget of the following runs (0 = none, the default).  A run
+ * that reaches it stops early: its rows are valid WPMs but not all of them,
+ * and wpm_plan_truncated() returns 1 -- for throughput / divergence stress on
+ * universes whose full enumeration is out of reach (BASELINE configs[4]). */
+int wpm_plan_set_node_budget(wpm_plan_t *plan, int64_t budget);
+int wpm_plan_truncated(const wpm_plan_t *plan);
 /* Copy the last run's results to the host. */
 int wpm_plan_fetch(wpm_plan_t *plan, wpm_result_t **out);
 /* Device-side timing of the last run (ms) and node count, without a fetch. */

@@ -185,6 +185,8 @@ _SIGS = {
     "wpm_plan_line15": (ctypes.c_int, [_PlanP, ctypes.POINTER(_i64)]),
     "wpm_plan_line15_stats": (ctypes.c_int, [_PlanP, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                              ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i32)]),
+    "wpm_plan_set_node_budget": (ctypes.c_int, [_PlanP, _i64]),
+    "wpm_plan_truncated": (ctypes.c_int, [_PlanP]),
     "wpm_plan_line15_costs": (_i64, [_PlanP, ctypes.POINTER(_i64), _i64]),
     "wpm_canonical_forms": (ctypes.c_int, [_i32, _i32, _i64, ctypes.POINTER(_i64), _u64p, _i32, _u64p,
                                            ctypes.POINTER(ctypes.c_int8)]),
@@ -433,6 +435,14 @@ class Plan:
         a, b = ctypes.c_double(), ctypes.c_double()
         _check(_lib.wpm_plan_line13_timing(self._h, ctypes.byref(a), ctypes.byref(b)))
         return {"ms_union": a.value, "ms_filter": b.value}
+
+    def set_node_budget(self, budget: int) -> None:
+        """Stop later runs after `budget` search nodes (0 = enumerate all);
+        a stopped run has .truncated() True (stress runs, BASELINE configs[4])."""
+        _check(_lib.wpm_plan_set_node_budget(self._h, int(budget)))
+
+    def truncated(self) -> bool:
+        return bool(_lib.wpm_plan_truncated(self._h))
 
     def line15(self) -> int:
         """Algorithm 2 line 15 (pipeline.hpp:91-103) on the last line-13

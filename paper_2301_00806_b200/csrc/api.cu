@@ -179,6 +179,8 @@ struct wpm_plan {
     unsigned long long out_cap = 0;
     // last run
     long long total = 0, nodes = 0, tasks = 0, dups = 0, reruns = 0;
+    unsigned long long node_budget = 0;  // 0 = enumerate everything
+    bool truncated = false;              // the last run stopped at the node budget
     std::vector<unsigned long long> per_map;
     float ms_search = 0, ms_sort = 0, ms_total = 0;
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -810,6 +812,7 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         sp.per_map = P->d_per_map.p;
         sp.out_cap = P->out_cap;
         sp.rw = P->rw;
+        sp.node_budget = P->node_budget;
         if (launch_seed_tasks(sp, ntasks, P->d_task_map.p, P->d_task_f.p, P->d_task_kind.p,
                               P->has_pins ? P->d_pin_in.p : nullptr, P->has_pins ? P->d_pin_out.p : nullptr,
                               P->stream))
@@ -845,10 +848,15 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
             std::fprintf(stderr, "[wpm] warp clocks: busy %.1f%%  waiting %.1f%%  final wait %.1f%%  (tasks %llu)\n",
                          100.0 * qc[5] / all, 100.0 * qc[6] / all, 100.0 * qc[7] / all, qc[3]);
         }
+        P->truncated = octl[3] != 0;
         if (octl[2]) {  // frame stack overflowed: redo with the full-depth layout
             full_depth = true;
             ++P->reruns;
             continue;
+        }
+        if (P->truncated) {  // a budgeted stress run: keep what fits, no rerun
+            P->total = std::min<long long>(P->total, (long long)P->out_cap);
+            break;
         }
         if (octl[0] <= P->out_cap) break;
         ++P->reruns;
@@ -913,6 +921,18 @@ extern "C" int wpm_plan_run(wpm_plan_t* P, int32_t shard_index, int32_t shard_co
     if (total_out) *total_out = P->total;
     return WPM_OK;
 }
+
+// search-node budget of the following runs (0 = none): a run that reaches it
+// stops early and reports truncated = 1 -- a throughput / divergence stress
+// on universes whose full enumeration is out of reach, not an enumeration
+extern "C" int wpm_plan_set_node_budget(wpm_plan_t* P, int64_t budget) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (budget < 0) return fail(WPM_EINVAL, "negative node budget");
+    P->node_budget = (unsigned long long)budget;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_truncated(const wpm_plan_t* P) { return P && P->truncated ? 1 : 0; }
 
 extern "C" int wpm_plan_stats(const wpm_plan_t* P, double* ms_search, double* ms_sort, int64_t* nodes,
                               int64_t* tasks) {

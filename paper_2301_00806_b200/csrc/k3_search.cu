@@ -729,6 +729,11 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
         const unsigned long long slot = (unsigned long long)t % (unsigned long long)p.qcap;
         __syncwarp();
         __threadfence();
+        if (p.node_budget && ld_relaxed_u64(&p.out_ctl[3])) {  // budget spent: drain the queue
+            if (lane == 0) atomicAdd(&p.qctl[2], (unsigned long long)-1ll);
+            __syncwarp();
+            continue;
+        }
         const uint32_t* rec = p.qrec + slot * (unsigned long long)p.recw;
         const uint32_t h0 = __ldcg(rec), h1 = __ldcg(rec + 1), h2 = __ldcg(rec + 2);
         const int map = (int)(h0 & 0xFFFFu);
@@ -772,6 +777,7 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
         // ---- the DFS over branch frames
         unsigned long long qword = ld_relaxed_u64(&p.qctl[0]);  // prefetched queue state
         unsigned long long next_check = nodes + (unsigned)p.check_every;
+        unsigned long long flushed = nodes;  // node-budget mode: count already in qctl[1]
         while (w.depth > 0) {
             const uint2 fr = w.frames()[w.depth - 1];
             int npos = 0;
@@ -822,6 +828,16 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
                 const long long queued = (long long)(qword >> 32) - (long long)(qword & 0xFFFFFFFFull);
                 if (queued < (long long)p.hungry) try_donate(w, mp, p, lane);
                 qword = ld_relaxed_u64(&p.qctl[0]);  // consumed at the next check
+                if (p.node_budget) {
+                    int stop = 0;
+                    if (lane == 0) {
+                        const unsigned long long d = nodes - flushed;
+                        if (atomicAdd(&p.qctl[1], d) + d >= p.node_budget) atomicExch(&p.out_ctl[3], 1ull);
+                        stop = ld_relaxed_u64(&p.out_ctl[3]) != 0ull;
+                    }
+                    flushed = nodes;
+                    if (__shfl_sync(FULL, stop, 0)) break;  // abandon the task (a truncated run)
+                }
             }
         }
         // task finished

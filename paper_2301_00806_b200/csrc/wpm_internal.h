@@ -39,6 +39,10 @@ struct SearchParams {
     unsigned long long* per_map;  // scratch: first row per map (after the sort)
     unsigned long long out_cap;
     int rw;                     // key row words = key_words_for(w32) + 1
+    // node budget (0 = none): warps flush their node counts into qctl[1]
+    // at every queue check and stop once the total reaches it (out_ctl[3]
+    // = 1: the run is truncated -- a throughput stress, not an enumeration)
+    unsigned long long node_budget;
 };
 
 // seeds root tasks (map, f) in queue order; required/forbidden lists for ENTRY tasks

@@ -100,3 +100,23 @@ def relabel(K: Complex, perm: List[int]) -> Complex:
                 g |= 1 << perm[v]
         out.append(g)
     return m, n, sorted(out)
+
+
+# ---- BASELINE configs[4]: synthetic candidate-facet sets
+M64 = (1 << 64) - 1
+
+
+def splitmix64(x: int) -> int:
+    z = (x + 0x9E3779B97F4A7C15) & M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def synthetic_universe(seed: int, density: float, m: int = 15, n: int = 11) -> List[int]:
+    """Facet j of the all-subsets universe of (m, n) (ascending masks,
+    catalog.hpp:112-120) is kept iff splitmix64(seed ^ j) * 2^-64 < density."""
+    thr = int(density * (1 << 64))
+    allf = [mask(*c) for c in combinations(range(1, m + 1), n)]
+    allf.sort()
+    return [f for j, f in enumerate(allf) if splitmix64(seed ^ j) < thr]
