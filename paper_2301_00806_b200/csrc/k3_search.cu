@@ -705,8 +705,8 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
                     t = (long long)tk;
                     break;
                 }
-                if (*pend == 0ull) {
-                    t = -2;
+                if (*pend == 0ull || (p.node_budget && ld_relaxed_u64(&p.out_ctl[3]))) {
+                    t = -2;  // no task left anywhere, or the node budget is spent
                     break;
                 }
                 __nanosleep(backoff);
@@ -729,10 +729,10 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
         const unsigned long long slot = (unsigned long long)t % (unsigned long long)p.qcap;
         __syncwarp();
         __threadfence();
-        if (p.node_budget && ld_relaxed_u64(&p.out_ctl[3])) {  // budget spent: drain the queue
-            if (lane == 0) atomicAdd(&p.qctl[2], (unsigned long long)-1ll);
-            __syncwarp();
-            continue;
+        if (p.node_budget) {  // budget spent: leave the queue as is (one read, warp-uniform)
+            int spent = 0;
+            if (lane == 0) spent = ld_relaxed_u64(&p.out_ctl[3]) != 0ull;
+            if (__shfl_sync(FULL, spent, 0)) break;
         }
         const uint32_t* rec = p.qrec + slot * (unsigned long long)p.recw;
         const uint32_t h0 = __ldcg(rec), h1 = __ldcg(rec + 1), h2 = __ldcg(rec + 2);
