@@ -819,7 +819,9 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
             return fail(WPM_EINTERNAL, "seed launch failed");
         const int est_warps = P->num_sms * 16;
         sp.hungry = std::max(64, est_warps / 2);
+        sp.backoff_min = 32;
         sp.backoff_max = 8192;
+        if (const char* e = std::getenv("WPM_BACKOFF_MIN")) sp.backoff_min = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("WPM_HUNGRY")) sp.hungry = std::atoi(e);
         if (const char* e = std::getenv("WPM_BACKOFF_MAX")) sp.backoff_max = std::max(32, std::atoi(e));
         // donation checks: every 16 nodes for small tables (cheap task

@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
             const unsigned long long tk = atomicAdd(&p.qctl[0], 1ull) & 0xFFFFFFFFull;
             volatile unsigned long long* rdy = p.qready + (tk % (unsigned long long)p.qcap);
             volatile unsigned long long* pend = p.qctl + 2;
-            unsigned backoff = 32;
+            unsigned backoff = (unsigned)p.backoff_min;
             for (;;) {
                 if (*rdy == tk + 1ull) {
                     t = (long long)tk;

@@ -141,7 +141,7 @@ struct L15Out {
 
 namespace {
 
-__global__ void __launch_bounds__(32 * L15_WARPS) l15_canon(L15Src src, L15Out out, L15Layout L, Binom B) {
+__global__ void __launch_bounds__(32 * L15_WARPS, 8) l15_canon(L15Src src, L15Out out, L15Layout L, Binom B) {
     extern __shared__ __align__(16) unsigned char l15_smem[];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* base = l15_smem + (size_t)wib * L.bytes;

@@ -31,6 +31,7 @@ struct SearchParams {
     unsigned long long* qctl;  // [0] tail << 32 | head, [2] pending, [3] tasks done, [4] nodes
     int qcap, recw, mw;
     int hungry;                 // donate while queued tasks < hungry
+    int backoff_min;            // ns, idle warps' first polling sleep
     int backoff_max;            // ns, idle warps' polling backoff cap
     int check_every;            // search nodes between looks at the queue word (donation check)
     // output: one key row per WPM = kw bitset words (zero padded) + the map id
