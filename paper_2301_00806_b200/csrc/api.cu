@@ -829,6 +829,8 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         // O(N) per donated task) -- measured sweep in DESIGN.md
         sp.check_every = P->maxN <= 256 ? 16 : 32;
         if (const char* e = std::getenv("WPM_CHECK_EVERY")) sp.check_every = std::max(1, std::atoi(e));
+        sp.donate_max = 1;
+        if (const char* e = std::getenv("WPM_DONATE_MAX")) sp.donate_max = std::max(1, std::atoi(e));
         tr.mark("  run: output alloc, H2D, seed");
         CU(cudaEventRecord(P->ev[0], P->stream));
         if (ntasks > 0 && !launch_k3_search(sp, P->num_sms, P->stream, &P->warps))

@@ -602,7 +602,7 @@ __device__ __forceinline__ bool load_state(WS<C>& w, const MapView& mp, const ui
 // frame's state = the current state minus every decision on the trail at or
 // after mk (`late`), with its in-progress child excluded.
 template <class C>
-__device__ __forceinline__ void try_donate(WS<C>& w, const MapView& mp, const SearchParams& p, int lane) {
+__device__ __forceinline__ bool try_donate(WS<C>& w, const MapView& mp, const SearchParams& p, int lane) {
     const int M = mp.M, mw = (M + 31) >> 5;
     uint32_t* late = w.late();
     const uint8_t* fst = w.fst();
@@ -671,8 +671,9 @@ __device__ __forceinline__ void try_donate(WS<C>& w, const MapView& mp, const Se
             w.frames()[d].x = ridge | (POS_DONE << 16);  // exhausted here
         }
         __syncwarp();
-        return;
+        return true;
     }
+    return false;
 }
 
 template <class C>
@@ -826,7 +827,13 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
                 next_check = nodes + (unsigned)p.check_every;
                 // waiting warps <=> the head ticket ran ahead of the tail
                 const long long queued = (long long)(qword >> 32) - (long long)(qword & 0xFFFFFFFFull);
-                if (queued < (long long)p.hungry) try_donate(w, mp, p, lane);
+                if (queued < (long long)p.hungry) {
+                    // warps are waiting (head ran past tail): hand out up to
+                    // donate_max frames at once, shallowest first
+                    const int k = queued < 0 ? p.donate_max : 1;
+                    for (int i = 0; i < k; ++i)
+                        if (!try_donate(w, mp, p, lane)) break;
+                }
                 qword = ld_relaxed_u64(&p.qctl[0]);  // consumed at the next check
                 if (p.node_budget) {
                     int stop = 0;

@@ -34,6 +34,7 @@ struct SearchParams {
     int backoff_min;            // ns, idle warps' first polling sleep
     int backoff_max;            // ns, idle warps' polling backoff cap
     int check_every;            // search nodes between looks at the queue word (donation check)
+    int donate_max;             // frames donated per check while warps wait
     // output: one key row per WPM = kw bitset words (zero padded) + the map id
     uint32_t* out_keys;         // out_cap * rw
     unsigned long long* out_ctl;  // [0] count, [1] duplicates (after the sort)

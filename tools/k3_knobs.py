@@ -11,10 +11,10 @@ import paper_2301_00806_b200 as wpm  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 grid = {
-    "WPM_BACKOFF_MIN": ["", "128", "512", "2048"],
-    "WPM_HUNGRY": ["", "256", "1024"],
-    "WPM_CHECK_EVERY": ["", "32"],
-    "WPM_BACKOFF_MAX": ["", "2048", "32768"],
+    "WPM_DONATE_MAX": ["", "2", "4", "8"],
+    "WPM_HUNGRY": ["", "256"],
+    "WPM_CHECK_EVERY": ["", "8", "32"],
+    "WPM_BACKOFF_MIN": ["", "512"],
 }
 with wpm.Plan.orbits(n) as p:
     p.run()
