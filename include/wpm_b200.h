@@ -211,9 +211,10 @@ int wpm_plan_line13_timing(const wpm_plan_t *plan, double *ms_union, double *ms_
 int wpm_plan_line15(wpm_plan_t *plan, int64_t *line15);
 /* device ms of the canonical forms and the dedupe; labelings completed and
  * single-vertex placements of the canonical-labeling searches; kernel
- * launches (> 1: a complex had more minimal non-faces than the first sizing) */
+ * launches (> 1: a complex had more minimal non-faces than the first sizing);
+ * survivors whose canonical form was confirmed from the isomorphism cache */
 int wpm_plan_line15_stats(const wpm_plan_t *plan, double *ms_canon, double *ms_dedupe, int64_t *labelings,
-                          int64_t *placements, int32_t *launches);
+                          int64_t *placements, int32_t *launches, int64_t *cache_hits);
 /* diagnostics: single-vertex placements of each survivor's canonical-labeling
  * search (survivor order), at most cap entries; returns the survivor count */
 int64_t wpm_plan_line15_costs(wpm_plan_t *plan, int64_t *out, int64_t cap);

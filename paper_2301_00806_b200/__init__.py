@@ -184,7 +184,8 @@ _SIGS = {
     "wpm_pipeline_line13": (ctypes.c_int, [_i32, _i32, _i64, _i32, ctypes.POINTER(_ComplexesP)]),
     "wpm_plan_line15": (ctypes.c_int, [_PlanP, ctypes.POINTER(_i64)]),
     "wpm_plan_line15_stats": (ctypes.c_int, [_PlanP, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
-                                             ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i32)]),
+                                             ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i32),
+                                             ctypes.POINTER(_i64)]),
     "wpm_plan_set_node_budget": (ctypes.c_int, [_PlanP, _i64]),
     "wpm_plan_truncated": (ctypes.c_int, [_PlanP]),
     "wpm_plan_line15_costs": (_i64, [_PlanP, ctypes.POINTER(_i64), _i64]),
@@ -454,11 +455,11 @@ class Plan:
 
     def line15_stats(self) -> dict:
         a, b = ctypes.c_double(), ctypes.c_double()
-        c, d, e = _i64(), _i64(), _i32()
+        c, d, e, h = _i64(), _i64(), _i32(), _i64()
         _check(_lib.wpm_plan_line15_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
-                                          ctypes.byref(d), ctypes.byref(e)))
+                                          ctypes.byref(d), ctypes.byref(e), ctypes.byref(h)))
         return {"ms_canon": a.value, "ms_dedupe": b.value, "labelings": int(c.value), "placements": int(d.value),
-                "launches": int(e.value)}
+                "launches": int(e.value), "cache_hits": int(h.value)}
 
     def line15_costs(self) -> np.ndarray:
         """placements of each line-13 survivor's canonical-labeling search"""

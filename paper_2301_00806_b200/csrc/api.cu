@@ -201,7 +201,9 @@ struct wpm_plan {
     DevBuf<uint32_t> d_l15_rows, d_l15_sidx, d_l15_iota, d_l15_rep;
     DevBuf<uint8_t> d_l15_first, d_l15_temp;
     DevBuf<int> d_l15_num;
-    DevBuf<unsigned long long> d_l15_ctl, d_l15_cost;
+    DevBuf<unsigned long long> d_l15_ctl, d_l15_cost, d_l15_ckey;
+    DevBuf<uint16_t> d_l15_cdata;
+    long long l15_hits = 0;
     long long line15 = -1, l15_leaves = 0, l15_steps = 0;
     int l15_kmax = 0, l15_mnfcap = 0, l15_launches = 0;
     float ms_canon = 0, ms_dedupe = 0;
@@ -1249,7 +1251,7 @@ extern "C" int wpm_plan_line15(wpm_plan_t* P, int64_t* line15_out) {
     const size_t tdd = l15_dedupe_temp_bytes(std::max<long long>(cnt, 1), gw);
     if (P->d_l15_rows.ensure((size_t)std::max<long long>(cnt, 1) * gw) || P->d_l15_sidx.ensure(cnt + 1) ||
         P->d_l15_iota.ensure(cnt + 1) || P->d_l15_rep.ensure(cnt + 1) || P->d_l15_first.ensure(cnt + 1) ||
-        P->d_l15_temp.ensure(tdd) || P->d_l15_num.ensure(2) || P->d_l15_ctl.ensure(4) ||
+        P->d_l15_temp.ensure(tdd) || P->d_l15_num.ensure(2) || P->d_l15_ctl.ensure(5) ||
         P->d_l15_cost.ensure(cnt + 1))
         return fail(WPM_EINTERNAL, "device allocation failed (line 15)");
     CU(cudaEventRecord(P->ev[0], P->stream));
@@ -1262,15 +1264,23 @@ extern "C" int wpm_plan_line15(wpm_plan_t* P, int64_t* line15_out) {
     // n <= 11); the kernel flags an overflow and the launch repeats with
     // twice the room (exact either way)
     int mnfcap = 64;
-    unsigned long long ctl[4] = {0, 0, 0, 0};
+    unsigned long long ctl[5] = {0, 0, 0, 0, 0};
     P->l15_launches = 0;
+    // canonical-form cache: isomorphic survivors after the first confirm a
+    // cached form instead of searching (WPM_L15_CACHE=0 disables)
+    const int cslots = 1 << 14;
+    const bool use_cache = !(std::getenv("WPM_L15_CACHE") && std::atoi(std::getenv("WPM_L15_CACHE")) == 0);
+    if (use_cache && (P->d_l15_ckey.ensure(cslots) || P->d_l15_cdata.ensure((size_t)cslots * (kmax + 1))))
+        return fail(WPM_EINTERNAL, "device allocation failed (line 15 cache)");
     for (;;) {
         const L15Layout L = l15_layout(m, n, kmax, mnfcap, gw);
         if (L.P > 2048 || l15_smem_bytes(L) > 227 * 1024)
             return fail(WPM_EINTERNAL, "line 15: complexes too large for the device layout");
         ++P->l15_launches;
         if (l15_launch(L, P->d_l13_rows.p, P->d_l13_sidx.p, nullptr, P->d_unrank.p, nullptr, nullptr, cnt,
-                       P->d_l15_rows.p, nullptr, nullptr, P->d_l15_cost.p, P->d_l15_ctl.p, P->num_sms, P->stream))
+                       P->d_l15_rows.p, nullptr, nullptr, P->d_l15_cost.p, P->d_l15_ctl.p,
+                       use_cache ? P->d_l15_ckey.p : nullptr, use_cache ? P->d_l15_cdata.p : nullptr, cslots,
+                       P->num_sms, P->stream))
             return fail(WPM_EINTERNAL, std::string("line 15 canonical forms: ") +
                                            cudaGetErrorString(cudaGetLastError()));
         CU(cudaMemcpyAsync(ctl, P->d_l15_ctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, P->stream));
@@ -1292,6 +1302,7 @@ extern "C" int wpm_plan_line15(wpm_plan_t* P, int64_t* line15_out) {
     P->line15 = nrep;
     P->l15_leaves = (long long)ctl[2];
     P->l15_steps = (long long)ctl[3];
+    P->l15_hits = (long long)ctl[4];
     CU(cudaEventElapsedTime(&P->ms_canon, P->ev[0], P->ev[1]));
     CU(cudaEventElapsedTime(&P->ms_dedupe, P->ev[1], P->ev[2]));
     if (line15_out) *line15_out = P->line15;
@@ -1311,8 +1322,9 @@ extern "C" int64_t wpm_plan_line15_costs(wpm_plan_t* P, int64_t* out, int64_t ca
 }
 
 extern "C" int wpm_plan_line15_stats(const wpm_plan_t* P, double* ms_canon, double* ms_dedupe, int64_t* labelings,
-                                     int64_t* placements, int32_t* launches) {
+                                     int64_t* placements, int32_t* launches, int64_t* cache_hits) {
     if (!P) return fail(WPM_EINVAL, "null plan");
+    if (cache_hits) *cache_hits = P->l15_hits;
     if (launches) *launches = P->l15_launches;
     if (ms_canon) *ms_canon = P->ms_canon;
     if (ms_dedupe) *ms_dedupe = P->ms_dedupe;
@@ -1542,10 +1554,11 @@ extern "C" int wpm_canonical_forms(int32_t m, int32_t n, int64_t count, const in
         DevBuf<uint16_t> dm, dout;
         DevBuf<long long> doff;
         DevBuf<int8_t> dcls;
-        DevBuf<unsigned long long> dctl;
+        DevBuf<unsigned long long> dctl, ckey;
+        DevBuf<uint16_t> cdata;
         std::vector<uint16_t> hout((size_t)nf + 1);
         std::vector<int8_t> hcls;
-        if (dm.ensure(nf + 1) || dout.ensure(nf + 1) || doff.ensure(count + 1) || dctl.ensure(4) ||
+        if (dm.ensure(nf + 1) || dout.ensure(nf + 1) || doff.ensure(count + 1) || dctl.ensure(5) ||
             (classes_out && dcls.ensure((size_t)count * 16))) {
             rc = fail(WPM_EINTERNAL, "device allocation failed (canonical forms)");
         } else if (cudaMemcpyAsync(dm.p, masks.data(), (nf + 1) * 2, cudaMemcpyHostToDevice, P->stream) ||
@@ -1559,9 +1572,12 @@ extern "C" int wpm_canonical_forms(int32_t m, int32_t n, int64_t count, const in
                     rc = fail(WPM_EINTERNAL, "canonical forms: complexes too large for the device layout");
                     break;
                 }
-                unsigned long long ctl[4] = {0, 0, 0, 0};
-                if (l15_launch(L, nullptr, nullptr, nullptr, nullptr, dm.p, doff.p, count, nullptr, dout.p,
-                               classes_out ? dcls.p : nullptr, nullptr, dctl.p, P->num_sms, P->stream) ||
+                unsigned long long ctl[5] = {0, 0, 0, 0, 0};
+                const int cslots = 1 << 12;
+                if ((!ckey.p && (ckey.ensure(cslots) || cdata.ensure((size_t)cslots * (kmax + 1)))) ||
+                    l15_launch(L, nullptr, nullptr, nullptr, nullptr, dm.p, doff.p, count, nullptr, dout.p,
+                               classes_out ? dcls.p : nullptr, nullptr, dctl.p, ckey.p, cdata.p, cslots,
+                               P->num_sms, P->stream) ||
                     cudaMemcpyAsync(ctl, dctl.p, sizeof(ctl), cudaMemcpyDeviceToHost, P->stream) ||
                     cudaStreamSynchronize(P->stream)) {
                     rc = fail(WPM_EINTERNAL, std::string("canonical forms: ") +

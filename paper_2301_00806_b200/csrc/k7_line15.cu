@@ -105,6 +105,12 @@ __device__ void warp_bitonic(unsigned long long* a, int P, int lane) {
     }
 }
 
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {  // splitmix64 finalizer
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
 // sorted ranks of the vertices of `s` as nibbles from bit `top` downward
 __device__ __forceinline__ unsigned long long rank_nibbles(uint32_t s, const uint16_t* clsmask, int ncls, int top) {
     unsigned long long code = 0;
@@ -136,7 +142,14 @@ struct L15Out {
     uint16_t* masks;            // csr mode: canonical masks at the input offsets
     int8_t* cls;                // optional: refined class per vertex (16 per complex)
     unsigned long long* cost;   // optional: single-vertex placements per complex
-    unsigned long long* ctl;    // [0] ticket, [1] overflow, [2] labelings completed, [3] placements
+    unsigned long long* ctl;    // [0] ticket, [1] overflow, [2] labelings completed, [3] placements,
+                                // [4] cache hits (canonical form confirmed from a cached one)
+    // canonical-form cache (optional): write-once slots keyed by an
+    // isomorphism-invariant hash; slot data = k, then the canonical facets
+    unsigned long long* cache_key;
+    uint16_t* cache_data;
+    int cache_slots;            // power of two
+    int cache_stride;           // uint16 per slot (>= kmax + 1)
 };
 
 namespace {
@@ -395,7 +408,19 @@ __global__ void __launch_bounds__(32 * L15_WARPS, 8) l15_canon(L15Src src, L15Ou
             __syncwarp();
         }
         if (out.cls && lane < 16) out.cls[ci * 16 + lane] = lane < m ? (int8_t)rank : (int8_t)-1;
+        // isomorphism-invariant key: the last round's sorted entry codes
+        // (ranks are class ids, item indices masked off) and the classes
+        unsigned long long hkey = 0;
+        if (out.cache_key) {
+            for (int q = lane; q < ni; q += 32) hkey += mix64((keys[q] >> 11) ^ ((unsigned long long)q << 52));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) hkey += __shfl_xor_sync(FULL, hkey, o);
+            hkey = mix64(hkey ^ ((unsigned long long)k << 32) ^ ((unsigned long long)ncls << 48) ^
+                         (unsigned long long)m) | (1ull << 63);
+        }
 
+        bool no_seed = false;
+    phase4:
         // ---- 4. least relabeled facet list over the class-respecting labelings
         // (class c owns the c-th consecutive label range, :232-288), by an
         // exact branch and bound over single placements.  Two placement
@@ -451,6 +476,41 @@ __global__ void __launch_bounds__(32 * L15_WARPS, 8) l15_canon(L15Src src, L15Ou
         unsigned long long gen = 0;   // lane g: image of every vertex, 4 bits each
         uint32_t gen_fix = 0;         // lane g: the vertices it fixes
         auto item_of = [&](int j) -> uint32_t { return comode ? (vall & ~(uint32_t)fl[j]) : (uint32_t)fl[j]; };
+        // a cached canonical form with the same invariant key seeds the
+        // best.  A leaf equal to it proves K is isomorphic to the cached
+        // complex (the leaf IS the cached list), so the search stops there:
+        // its minimum is the cached one.  If the seed is not reachable
+        // (not isomorphic), either a real leaf beats it or nothing survives
+        // and the search reruns unseeded.
+        const unsigned cslot = out.cache_key ? (unsigned)(hkey & (unsigned long long)(out.cache_slots - 1)) : 0u;
+        bool seeded = false, found = false, real_best = false;
+        // seed only where a fresh search is expensive: the labelings of the
+        // class structure (prod of class-size factorials) exceed 7!; below
+        // that the fresh search (with its automorphism pruning) measured
+        // cheaper than confirming a cached form
+        double labelings_bound = 1.0;
+        for (int r = 0; r < ncls; ++r)
+            for (int q = 2; q <= __popc(clsmask[r]); ++q) labelings_bound *= q;
+        if (out.cache_key && !no_seed && labelings_bound > 5040.0) {
+            unsigned long long ck = 0;
+            if (lane == 0) ck = *(volatile unsigned long long*)(out.cache_key + cslot);
+            ck = __shfl_sync(FULL, ck, 0);
+            if (ck == hkey) {
+                __threadfence();
+                const uint16_t* cd = out.cache_data + (size_t)cslot * out.cache_stride;
+                if ((int)__ldcg(cd) == k) {
+                    for (int j = lane; j < k; j += 32) {
+                        // facet list ascending -> item list ascending
+                        const uint32_t f = __ldcg(cd + 1 + (comode ? k - 1 - j : j));
+                        const uint32_t it = comode ? (vall & ~f) : f;
+                        best[j] = (uint16_t)it;
+                        atomicOr(&mb[it >> 5], 1u << (it & 31));
+                    }
+                    __syncwarp();
+                    seeded = have_best = true;
+                }
+            }
+        }
         auto undo = [&](int v, int tt) {
             const uint32_t vb = 1u << v;
             const int lab = comode ? m - 1 - tt : tt;
@@ -545,6 +605,11 @@ __global__ void __launch_bounds__(32 * L15_WARPS, 8) l15_canon(L15Src src, L15Ou
                 }
             }
             int jump = -1;
+            if (leaf && verdict == 0 && seeded && !real_best) {
+                ++n_leaves;
+                found = true;  // K is isomorphic to the cached complex
+                break;
+            }
             if (leaf) {
                 // every bound is exact here: a new best iff the list is below the best
                 ++n_leaves;
@@ -577,6 +642,7 @@ __global__ void __launch_bounds__(32 * L15_WARPS, 8) l15_canon(L15Src src, L15Ou
                     }
                 }
                 if (verdict > 0) {
+                    real_best = true;
                     best_v = lane <= t ? my_v : -1;
                     for (int w = lane; w < W; w += 32) mb[w] = fb[w];
                     __syncwarp();
@@ -610,6 +676,11 @@ __global__ void __launch_bounds__(32 * L15_WARPS, 8) l15_canon(L15Src src, L15Ou
             ++t;
             if (lane == t) my_tried = 0;
         }
+        if (seeded && !found && !real_best) {  // the seed was out of reach: search again, unseeded
+            no_seed = true;
+            goto phase4;
+        }
+        if (found && lane == 0) atomicAdd(out.ctl + 4, 1ull);
         // best[] holds the ascending list of facet masks (facet mode) or of
         // co-facet masks (co-facet mode: facet j is the complement of
         // best[k - 1 - j])
@@ -619,6 +690,19 @@ __global__ void __launch_bounds__(32 * L15_WARPS, 8) l15_canon(L15Src src, L15Ou
             __syncwarp();
             for (int j = lane; j < k; j += 32) best[j] = rm[j];
             __syncwarp();
+        }
+        if (out.cache_key && !found && k + 1 <= out.cache_stride) {
+            // publish this canonical form (write-once slot: claim, fill, release)
+            int claimed = 0;
+            if (lane == 0) claimed = atomicCAS(out.cache_key + cslot, 0ull, 1ull) == 0ull;
+            if (__shfl_sync(FULL, claimed, 0)) {
+                uint16_t* cd = out.cache_data + (size_t)cslot * out.cache_stride;
+                for (int j = lane; j < k; j += 32) cd[1 + j] = best[j];
+                if (lane == 0) cd[0] = (uint16_t)k;
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) atomicExch(out.cache_key + cslot, hkey);
+            }
         }
 
         // ---- output
@@ -753,7 +837,8 @@ size_t l15_smem_bytes(const L15Layout& L) { return (size_t)L.bytes * L15_WARPS; 
 int l15_launch(const L15Layout& L, const uint32_t* d_rows, const uint32_t* d_idx, const int* d_num,
                const uint16_t* d_unrank, const uint16_t* d_masks, const long long* d_off, long long count,
                uint32_t* d_out_rows, uint16_t* d_out_masks, int8_t* d_cls, unsigned long long* d_cost,
-               unsigned long long* d_ctl, int num_sms, cudaStream_t st) {
+               unsigned long long* d_ctl, unsigned long long* d_cache_key, uint16_t* d_cache_data, int cache_slots,
+               int num_sms, cudaStream_t st) {
     if (count <= 0) return 0;
     const size_t smem = l15_smem_bytes(L);
     if (smem > 227 * 1024) return 1;
@@ -765,8 +850,12 @@ int l15_launch(const L15Layout& L, const uint32_t* d_rows, const uint32_t* d_idx
         return 1;
     const long long blocks = std::min<long long>((count + L15_WARPS - 1) / L15_WARPS, (long long)num_sms * per_sm);
     L15Src src{d_rows, d_idx, d_num, d_unrank, d_masks, d_off, count};
-    L15Out out{d_out_rows, d_out_masks, d_cls, d_cost, d_ctl};
-    if (cudaMemsetAsync(d_ctl, 0, 4 * sizeof(unsigned long long), st) != cudaSuccess) return 1;
+    L15Out out{d_out_rows, d_out_masks, d_cls, d_cost, d_ctl, d_cache_key, d_cache_data, cache_slots,
+               L.kmax + 1};
+    if (cudaMemsetAsync(d_ctl, 0, 5 * sizeof(unsigned long long), st) != cudaSuccess) return 1;
+    if (d_cache_key &&
+        cudaMemsetAsync(d_cache_key, 0, (size_t)cache_slots * sizeof(unsigned long long), st) != cudaSuccess)
+        return 1;
     l15_canon<<<(unsigned)blocks, 32 * L15_WARPS, smem, st>>>(src, out, L, make_binom());
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }

@@ -127,11 +127,14 @@ int l15_max_facets(const uint32_t* d_rows, int gw, const uint32_t* d_idx, long l
                    cudaStream_t st);
 // row mode (d_rows != null: complexes = rows[idx[i]], gw words, count from
 // *d_num if given) or CSR mode (0-based masks ascending, offsets); d_ctl[4]:
-// ticket, overflow count (> 0: rerun with a larger mnfcap), labelings, placements
+// ticket, overflow count (> 0: rerun with a larger mnfcap), labelings, placements, cache hits;
+// d_cache_key (cache_slots, a power of two; null = no cache) + d_cache_data
+// (cache_slots * (kmax + 1) uint16): the canonical-form cache
 int l15_launch(const L15Layout& L, const uint32_t* d_rows, const uint32_t* d_idx, const int* d_num,
                const uint16_t* d_unrank, const uint16_t* d_masks, const long long* d_off, long long count,
                uint32_t* d_out_rows, uint16_t* d_out_masks, int8_t* d_cls, unsigned long long* d_cost,
-               unsigned long long* d_ctl, int num_sms, cudaStream_t st);
+               unsigned long long* d_ctl, unsigned long long* d_cache_key, uint16_t* d_cache_data, int cache_slots,
+               int num_sms, cudaStream_t st);
 size_t l15_dedupe_temp_bytes(long long count, int gw);
 int l15_dedupe(const uint32_t* d_rows, long long count, int gw, uint32_t* d_sidx, uint32_t* d_iota, uint8_t* d_first,
                uint32_t* d_rep, int* d_nrep, void* d_temp, size_t temp_bytes, cudaStream_t st);
