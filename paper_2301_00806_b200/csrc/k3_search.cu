@@ -86,7 +86,8 @@ struct LC {
     static constexpr int LATE = INB + a16(4 * MW + 4);     // donation scratch
     static constexpr int TRAIL = LATE + a16(4 * MW + 4);   // uint16 per decision (bit 15: include)
     static constexpr int FRAMES = TRAIL + a16(2 * MP);     // uint2 per branch frame
-    static constexpr int SCRATCH = FRAMES + a16(8 * (DMAX + 2));  // closing-ridge list
+    static constexpr int NOPEN = FRAMES + a16(8 * (DMAX + 2));    // uint16 per frame: open ridges at its mark
+    static constexpr int SCRATCH = NOPEN + a16(2 * (DMAX + 2));   // closing-ridge list
     static constexpr int BYTES = SCRATCH + 64;
     // CTAs per SM the register budget is cut for: 10 (48 registers, no
     // spills) up to the n = 8 shapes -- measured +1.5 / +5 / +6 % nodes/s
@@ -126,7 +127,8 @@ template <class C>
 struct WS {
     uint8_t* base;  // generic pointer to the warp's region (shared)
     uint32_t sb;    // the same as a 32-bit shared-window address
-    int size, nopen, ndead, tl, depth;
+    int size, nopen, tl, depth;
+    int ndead;  // nonzero iff some open ridge has no undecided candidate (a dead state is always abandoned)
     __device__ __forceinline__ uint8_t* rs() const { return base + C::RS; }
     __device__ __forceinline__ uint8_t* fst() const { return base + C::FST; }
     __device__ __forceinline__ uint32_t* open() const { return reinterpret_cast<uint32_t*>(base + C::OPEN); }
@@ -135,6 +137,7 @@ struct WS {
     __device__ __forceinline__ uint32_t* late() const { return reinterpret_cast<uint32_t*>(base + C::LATE); }
     __device__ __forceinline__ uint16_t* trail() const { return reinterpret_cast<uint16_t*>(base + C::TRAIL); }
     __device__ __forceinline__ uint2* frames() const { return reinterpret_cast<uint2*>(base + C::FRAMES); }
+    __device__ __forceinline__ uint16_t* nopen_at() const { return reinterpret_cast<uint16_t*>(base + C::NOPEN); }
     __device__ __forceinline__ uint16_t* scratch() const { return reinterpret_cast<uint16_t*>(base + C::SCRATCH); }
     // shared-window addresses for the PTX helpers
     __device__ __forceinline__ uint32_t a_rs_word(int r) const { return sb + C::RS + (r & ~3); }
@@ -210,7 +213,7 @@ __device__ __forceinline__ void apply_exclusions(WS<C>& w, const MapView& mp, in
         const unsigned ob = (atom_add_if(w.a_rs_word(r), 0u - (4u << sh), act) >> sh) & 0xFFu;
         // (1,1) -> (1,0): dead and leaves the forced set; (1,2) -> (1,1): enters it
         red_xor_if(w.a_b1(r), 1u << (r & 31), act && (ob == 5u || ob == 9u));
-        w.ndead += __popc(__ballot_sync(FULL, act && ob == 5u));
+        w.ndead |= (int)__any_sync(FULL, act && ob == 5u);
     }
 }
 
@@ -224,7 +227,7 @@ __device__ __forceinline__ void exclude_one(WS<C>& w, const MapView& mp, int g, 
     const unsigned sh = (r & 3) * 8;
     const unsigned ob = (atom_add_if(w.a_rs_word(r), 0u - (4u << sh), act) >> sh) & 0xFFu;
     red_xor_if(w.a_b1(r), 1u << (r & 31), act && (ob == 5u || ob == 9u));
-    w.ndead += __popc(__ballot_sync(FULL, act && ob == 5u));
+    w.ndead |= (int)__any_sync(FULL, act && ob == 5u);
     w.tl += 1;
     __syncwarp();
 }
@@ -306,12 +309,16 @@ __device__ __forceinline__ void include_facet(WS<C>& w, const MapView& mp, int f
 // a-1), so the final bytes do not depend on the order the inverse deltas are
 // applied in.  All (decision, ridge) pairs are flattened over the 32 lanes and
 // applied with shared atomics; each atomic returns the exact old byte, so the
-// open / forced / dead transitions it reports are exact and their sum
-// telescopes to the right totals and bitsets whatever the interleaving.
+// open / forced bit flips it reports are exact whatever the interleaving.
+// The tallies need no per-pair vote: every mark is taken at a live node
+// (ndead == 0; a frame is pushed only when nothing is dead and a sibling
+// exclusion that kills a ridge retires its open frame), so the state after
+// the undo has ndead = 0 and the open count the caller saved at the mark.
 template <class C>
-__device__ __forceinline__ void undo_to(WS<C>& w, const MapView& mp, int mark, int lane) {
+__device__ __forceinline__ void undo_to(WS<C>& w, const MapView& mp, int mark, int nopen_mark, int lane) {
     const int lo = mark, hi = w.tl;
     if (hi <= lo) return;
+#ifndef K3_UNDO_ONEPASS
     for (int e0 = lo; e0 < hi; e0 += 32) {
         const int e = e0 + lane;
         const bool act = e < hi;
@@ -322,26 +329,31 @@ __device__ __forceinline__ void undo_to(WS<C>& w, const MapView& mp, int mark, i
         red_and_if(w.a_inb(g), ~(1u << (g & 31)), inc);
         w.size -= __popc(__ballot_sync(FULL, inc));
     }
+#endif
     const int sh_l = mp.lpf_shift, k = lane & ((1 << sh_l) - 1), per = 32 >> sh_l;
     for (int e0 = lo; e0 < hi; e0 += per) {
         const int e = e0 + (lane >> sh_l);
         const bool act = e < hi && k < mp.n;
         const unsigned t = act ? (unsigned)w.trail()[e] : 0u;
         const int g = (int)(t & 0x7FFFu);
+#ifdef K3_UNDO_ONEPASS
+        // the decision's own status / IN bit / size, by its k = 0 lane
+        const bool lead = act && k == 0, inc = lead && (t & TR_INC);
+        st_u8_if(w.a_fst(g), FU, lead);
+        red_and_if(w.a_inb(g), ~(1u << (g & 31)), inc);
+        w.size -= __popc(__ballot_sync(FULL, inc));
+#endif
         const int r = act ? __ldg(mp.fr + g * mp.fs + k) : 0;
         const unsigned delta = (t & TR_INC) ? 3u : 4u;  // (c-1, a+1) or (a+1)
         const unsigned sh = (r & 3) * 8;
         const unsigned ob = (atom_add_if(w.a_rs_word(r), delta << sh, act) >> sh) & 0xFFu;
         const unsigned nb = ob + delta;
-        const bool o0 = act && (ob & 3u) == 1u, o1 = act && (nb & 3u) == 1u;
-        const bool f0 = ob == 5u, f1 = nb == 5u;                // (1,1): forced
-        const bool z0 = act && ob == 1u, z1 = act && nb == 1u;  // (1,0): dead
         const unsigned bit = 1u << (r & 31);
-        red_xor_if(w.a_open(r), bit, o0 != o1);
-        red_xor_if(w.a_b1(r), bit, act && f0 != f1);
-        w.nopen += __popc(__ballot_sync(FULL, o1 && !o0)) - __popc(__ballot_sync(FULL, o0 && !o1));
-        w.ndead += __popc(__ballot_sync(FULL, z1 && !z0)) - __popc(__ballot_sync(FULL, z0 && !z1));
+        red_xor_if(w.a_open(r), bit, act && (((ob & 3u) == 1u) != ((nb & 3u) == 1u)));
+        red_xor_if(w.a_b1(r), bit, act && ((ob == 5u) != (nb == 5u)));
     }
+    w.nopen = nopen_mark;
+    w.ndead = 0;
     w.tl = mark;
     __syncwarp();
 }
@@ -380,7 +392,7 @@ __device__ void debug_check(const WS<C>& w, const MapView& mp, int lane, int whe
     size = (int)__reduce_add_sync(FULL, (unsigned)size);
     bad = (int)__reduce_or_sync(FULL, (unsigned)bad);
     if (nopen != w.nopen) bad |= 16;
-    if (ndead != w.ndead) bad |= 32;
+    if ((ndead != 0) != (w.ndead != 0)) bad |= 32;
     if (size != w.size) bad |= 64;
     if (bad) {
         if (lane == 0)
@@ -789,7 +801,7 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
                 w.depth -= 1;
                 if (w.depth > 0) {
                     const uint2 pf = w.frames()[w.depth - 1];
-                    undo_to(w, mp, (int)(pf.y >> 16), lane);
+                    undo_to(w, mp, (int)(pf.y >> 16), (int)w.nopen_at()[w.depth - 1], lane);
                     DEBUG_CHECK(w, mp, lane, 3);
                     exclude_one(w, mp, (int)(pf.y & 0xFFFFu), lane);
                     DEBUG_CHECK(w, mp, lane, 4);
@@ -800,10 +812,12 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
                 }
                 continue;
             }
-            const int cm = w.tl;
-            if (lane == 0)
+            const int cm = w.tl, om = w.nopen;
+            if (lane == 0) {
                 w.frames()[w.depth - 1] =
                     make_uint2((fr.x & 0xFFFFu) | ((uint32_t)npos << 16), (uint32_t)c | ((uint32_t)cm << 16));
+                w.nopen_at()[w.depth - 1] = (uint16_t)om;
+            }
             __syncwarp();
             const Probe pr = probe_facet(w, mp, c, lane);
             ++nodes;
@@ -814,7 +828,7 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
                 pushed = descend(w, mp, p, nodes, lane);
             }
             if (!pushed) {
-                undo_to(w, mp, cm, lane);
+                undo_to(w, mp, cm, om, lane);
                 DEBUG_CHECK(w, mp, lane, 6);
                 exclude_one(w, mp, c, lane);
                 DEBUG_CHECK(w, mp, lane, 7);
@@ -903,6 +917,9 @@ int launch_class(const SearchParams& p, int num_sms, cudaStream_t st, int* warps
     const size_t smem = (size_t)C::BYTES * wpb;
     if (cudaFuncSetAttribute(k3_search<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return 0;
+    // experiment knob: the L1 / shared split (percent of the max shared carveout)
+    if (const char* e = std::getenv("WPM_CARVEOUT"))
+        cudaFuncSetAttribute(k3_search<C>, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e));
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_search<C>, 32 * wpb, smem) != cudaSuccess ||
         per_sm < 1)
