@@ -318,7 +318,6 @@ template <class C>
 __device__ __forceinline__ void undo_to(WS<C>& w, const MapView& mp, int mark, int nopen_mark, int lane) {
     const int lo = mark, hi = w.tl;
     if (hi <= lo) return;
-#ifndef K3_UNDO_ONEPASS
     for (int e0 = lo; e0 < hi; e0 += 32) {
         const int e = e0 + lane;
         const bool act = e < hi;
@@ -329,20 +328,12 @@ __device__ __forceinline__ void undo_to(WS<C>& w, const MapView& mp, int mark, i
         red_and_if(w.a_inb(g), ~(1u << (g & 31)), inc);
         w.size -= __popc(__ballot_sync(FULL, inc));
     }
-#endif
     const int sh_l = mp.lpf_shift, k = lane & ((1 << sh_l) - 1), per = 32 >> sh_l;
     for (int e0 = lo; e0 < hi; e0 += per) {
         const int e = e0 + (lane >> sh_l);
         const bool act = e < hi && k < mp.n;
         const unsigned t = act ? (unsigned)w.trail()[e] : 0u;
         const int g = (int)(t & 0x7FFFu);
-#ifdef K3_UNDO_ONEPASS
-        // the decision's own status / IN bit / size, by its k = 0 lane
-        const bool lead = act && k == 0, inc = lead && (t & TR_INC);
-        st_u8_if(w.a_fst(g), FU, lead);
-        red_and_if(w.a_inb(g), ~(1u << (g & 31)), inc);
-        w.size -= __popc(__ballot_sync(FULL, inc));
-#endif
         const int r = act ? __ldg(mp.fr + g * mp.fs + k) : 0;
         const unsigned delta = (t & TR_INC) ? 3u : 4u;  // (c-1, a+1) or (a+1)
         const unsigned sh = (r & 3) * 8;
