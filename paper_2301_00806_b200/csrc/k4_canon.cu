@@ -9,9 +9,10 @@
 //
 // Kernel 3 emits each WPM as a fixed-width key row -- W uint32 words of the
 // characteristic bitset (zero padded, W a bucket >= the plan's width)
-// followed by the map id.  Narrow rows (W = 4, M <= 128, i.e. n <= 5) are
+// followed by the map id.  Narrow rows (W <= 4, M <= 128, i.e. n <= 5) are
 // merge-sorted (CUB) as keys themselves: no indirection, comparisons in
-// registers.  Wider rows merge-sort row indices instead, the comparator
+// registers.  W is the exact word count there (n = 5 has M <= 88: 16-byte
+// keys instead of 20).  Wider rows merge-sort row indices instead, the comparator
 // reading the rows from L2 (moving 36-132 B keys through every merge pass
 // measured 2-4x slower).  A split/gather pass then writes the canonical rows
 // (the C-ABI width) and map ids, records per-map group boundaries and counts
@@ -138,10 +139,13 @@ __global__ void gather_rows(const uint32_t* __restrict__ keys, int rw, const uin
     }
 }
 
-constexpr int KEY_SORT_MAX_WORDS = 4;  // row-key sort up to 4 bitset words (M <= 128)
 
 int key_words_for(int w32) {
-    static const int buckets[] = {4, 8, 16, 24, 32, 48, 64};
+#ifdef WPM_KEY_FINE
+    static const int buckets[] = {1, 2, 3, 4, 5, 6, 8, 16, 24, 32, 48, 64};
+#else
+    static const int buckets[] = {1, 2, 3, 4, 8, 16, 24, 32, 48, 64};
+#endif
     for (int b : buckets)
         if (w32 <= b) return b;
     return -1;
@@ -166,9 +170,20 @@ static int sort_w(uint32_t* d_keys, long long count, int w32, uint32_t* d_sorted
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+#ifdef WPM_KEY_FINE
+#define WPM_KEY_FINE_CASES(CALL) \
+    case 5: CALL(5);             \
+    case 6: CALL(6);
+#else
+#define WPM_KEY_FINE_CASES(CALL)
+#endif
 #define WPM_KEY_DISPATCH(KW, CALL) \
     switch (KW) {                  \
+        case 1: CALL(1);           \
+        case 2: CALL(2);           \
+        case 3: CALL(3);           \
         case 4: CALL(4);           \
+        WPM_KEY_FINE_CASES(CALL)   \
         case 8: CALL(8);           \
         case 16: CALL(16);         \
         case 24: CALL(24);         \
@@ -181,7 +196,17 @@ static int sort_w(uint32_t* d_keys, long long count, int w32, uint32_t* d_sorted
 // temp = merge-sort scratch (+ the index array on the wide-row path)
 size_t canon_sort_temp_bytes(long long count, int w32) {
     const int kw = key_words_for(w32);
-    if (kw <= KEY_SORT_MAX_WORDS) return temp_bytes_w<KEY_SORT_MAX_WORDS>(count);
+    switch (kw) {
+        case 1: return temp_bytes_w<1>(count);
+        case 2: return temp_bytes_w<2>(count);
+        case 3: return temp_bytes_w<3>(count);
+        case 4: return temp_bytes_w<4>(count);
+#ifdef WPM_KEY_DIRECT6
+        case 5: return temp_bytes_w<5>(count);
+        case 6: return temp_bytes_w<6>(count);
+#endif
+        default: break;
+    }
     size_t bytes = 0;
     cub::DeviceMergeSort::SortKeys(nullptr, bytes, (uint32_t*)nullptr, (int)count, IdxLess{nullptr, kw + 1, w32});
     return bytes + ((size_t)count * 4 + 256);
@@ -192,9 +217,17 @@ int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sort
                     cudaStream_t st) {
     if (count <= 0) return 0;
     const int kw = key_words_for(w32);
-    if (kw <= KEY_SORT_MAX_WORDS)
-        return sort_w<KEY_SORT_MAX_WORDS>(d_keys, count, w32, d_sorted_bits, d_sorted_map, d_temp, temp_bytes,
-                                          d_first_row, d_dups, st);
+#define SW(W)                                                                                                  \
+    case W:                                                                                                    \
+        return sort_w<W>(d_keys, count, w32, d_sorted_bits, d_sorted_map, d_temp, temp_bytes, d_first_row, d_dups, st);
+    switch (kw) {
+        SW(1) SW(2) SW(3) SW(4)
+#ifdef WPM_KEY_DIRECT6
+        SW(5) SW(6)
+#endif
+        default: break;
+    }
+#undef SW
     const size_t idx_bytes = (size_t)count * 4 + 256;
     uint32_t* idx = reinterpret_cast<uint32_t*>(d_temp);
     void* sort_temp = static_cast<uint8_t*>(d_temp) + idx_bytes;
