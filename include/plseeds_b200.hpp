@@ -14,7 +14,7 @@
 //      AffineProperty, ubt_property, cyclic_facet_bound   affine_property.hpp:16-54
 //      SearchJob            search.hpp:46-55 (+ required/forbidden pins, device)
 //      enumerate_wpm        search.hpp:141-258 (kernels 2-3 + canonical sort)
-//      enumerate_orbits     the per-orbit loop of pipeline.hpp:383-397, one launch
+//      enumerate_orbits     the per-orbit loop of pipeline.hpp:58-72, one launch
 //      write_complex(es)    complex_io.hpp:21-39
 //      pipeline_line13      pipeline.hpp:52-89 lines 1-13 (union, support, is_seed on the GPU)
 //      is_seed              classify.hpp:51-53 (batch, on the GPU)
@@ -251,7 +251,7 @@ inline std::vector<PureComplex> enumerate_wpm(const SearchJob& job) {
     return detail::complexes_of(R.r, 0, job.m, job.n, job.facets);
 }
 
-// the Algorithm-2 per-orbit loop (pipeline.hpp:383-397) for one n in one launch:
+// the Algorithm-2 per-orbit loop (pipeline.hpp:58-72) for one n in one launch:
 // element i = enumerate_wpm over matroid_universe(idcm_orbits(n, p)[i]) with the UBT cap
 inline std::vector<std::vector<PureComplex>> enumerate_orbits(int n, int p = 4, int device = 0,
                                                               std::int64_t facet_cap = WPM_CAP_UBT) {
@@ -419,13 +419,17 @@ namespace plseeds {
 namespace b200 {
 
 // Drop-in for plseeds::enumerate_wpm(job).  Honours job.basis exactly: the
-// reference enumerates base + span(free generators) (search.hpp:152-153,
-// combination_space :81-104).  A facet on which every free generator vanishes
-// is fixed to its base bit; those pins go to the device search, and each
-// result is kept iff K xor base lies in the span of the free generators (a
-// no-op for bases produced by apply_link_constraints, whose solution set is
-// exactly the pinned WPMs).  The candidate cap throws cap_exceeded_error like
-// the reference (search.hpp:147-150).
+// reference enumerates base + one candidate per block of
+// combination_space(kb) (search.hpp:81-104, :152-153) -- at most two
+// generators of each induced block, any subset of the free singletons
+// (g >= covered), nothing else.  A facet on which every usable generator
+// vanishes is fixed to its base bit; those pins go to the device search.
+// Every device WPM K is then written in coordinates, K xor base = sum of
+// x_g gens[g] (the generators are independent, so x is unique), and kept iff
+// x exists and obeys the combination-space rules -- for bases produced by
+// convenient_basis / apply_link_constraints this keeps every WPM; for a
+// hand-made basis it drops exactly the K the reference cannot reach.  The
+// candidate cap throws cap_exceeded_error like the reference (search.hpp:147-150).
 inline std::vector<PureComplex> enumerate_wpm(const SearchJob& job) {
     const KernelBasis& kb = job.basis;
     const std::uint64_t space = combination_space(kb).size_saturated();
@@ -433,15 +437,26 @@ inline std::vector<PureComplex> enumerate_wpm(const SearchJob& job) {
         throw cap_exceeded_error("combination space of " + std::to_string(space) + " candidates exceeds cap " +
                                  std::to_string(job.candidate_cap));
     const int M = static_cast<int>(job.facets.size());
+    const int s = kb.s();
     const int first_free = kb.pinned_ones + kb.pinned_zeros;
+    // usable generators and their block (search.hpp:85-103): block id, or -1
+    // for a free singleton; unusable ones (pinned, or skipped by `covered`) -2
+    std::vector<int> block_of(static_cast<std::size_t>(s), -2);
+    int covered = first_free;
+    for (std::size_t b = 0; b < kb.blocks.size(); ++b) {
+        for (int i = 0; i < kb.blocks[b].width; ++i) block_of[static_cast<std::size_t>(kb.blocks[b].offset + i)] = static_cast<int>(b);
+        covered = std::max(covered, kb.blocks[b].offset + kb.blocks[b].width);
+    }
+    for (int g = covered; g < s; ++g) block_of[static_cast<std::size_t>(g)] = -1;
     BitVec base(M);
     for (int g = 0; g < kb.pinned_ones; ++g) base ^= kb.gens[static_cast<std::size_t>(g)];
     std::vector<int> req, forb;
-    if (first_free > 0) {
+    {
         BitVec any_free(M);
-        for (int g = first_free; g < kb.s(); ++g)
-            for (std::size_t w = 0; w < any_free.words.size(); ++w)
-                any_free.words[w] |= kb.gens[static_cast<std::size_t>(g)].words[w];
+        for (int g = 0; g < s; ++g)
+            if (block_of[static_cast<std::size_t>(g)] >= -1)
+                for (std::size_t w = 0; w < any_free.words.size(); ++w)
+                    any_free.words[w] |= kb.gens[static_cast<std::size_t>(g)].words[w];
         for (int j = 0; j < M; ++j)
             if (!any_free.test(j)) (base.test(j) ? req : forb).push_back(j);
     }
@@ -452,32 +467,59 @@ inline std::vector<PureComplex> enumerate_wpm(const SearchJob& job) {
     for (const auto& g : job.properties) j.properties.push_back({g.weights, g.constant});
     j.required = req;
     j.forbidden = forb;
-    // echelon of the free generators for the affine-span filter
+    j.progress = job.progress;
+    // reduced echelon of the usable generators, each row remembering which
+    // generators it sums (coordinate bookkeeping)
+    const std::size_t sw = (static_cast<std::size_t>(s) + 63) / 64;
     std::vector<BitVec> ech;
+    std::vector<std::vector<std::uint64_t>> comb;
     std::vector<int> lead;
-    for (int g = first_free; g < kb.s(); ++g) {
+    for (int g = 0; g < s; ++g) {
+        if (block_of[static_cast<std::size_t>(g)] < -1) continue;
         BitVec v = kb.gens[static_cast<std::size_t>(g)];
+        std::vector<std::uint64_t> c(sw, 0);
+        c[static_cast<std::size_t>(g) / 64] |= std::uint64_t{1} << (g % 64);
         for (std::size_t i = 0; i < ech.size(); ++i)
-            if (v.test(lead[i])) v ^= ech[i];
+            if (v.test(lead[i])) {
+                v ^= ech[i];
+                for (std::size_t w = 0; w < sw; ++w) c[w] ^= comb[i][w];
+            }
         int l = -1;
         for (int b = 0; b < M && l < 0; ++b)
             if (v.test(b)) l = b;
-        if (l < 0) continue;
+        if (l < 0) continue;  // dependent generator: not a basis; its span is still covered
         for (std::size_t i = 0; i < ech.size(); ++i)
-            if (ech[i].test(l)) ech[i] ^= v;
-        ech.push_back(v);
+            if (ech[i].test(l)) {
+                ech[i] ^= v;
+                for (std::size_t w = 0; w < sw; ++w) comb[i][w] ^= c[w];
+            }
+        ech.push_back(std::move(v));
+        comb.push_back(std::move(c));
         lead.push_back(l);
     }
     std::vector<PureComplex> out;
+    std::vector<int> per_block(kb.blocks.size());
     for (auto& K : plseeds_b200::enumerate_wpm(j)) {
         BitVec x = base;
         for (const auto& f : K.facets) {
             const auto it = std::lower_bound(job.facets.begin(), job.facets.end(), VertexSet(f.bits));
             x.flip(static_cast<int>(it - job.facets.begin()));
         }
+        std::vector<std::uint64_t> coords(sw, 0);
         for (std::size_t i = 0; i < ech.size(); ++i)
-            if (x.test(lead[i])) x ^= ech[i];
-        if (x.any()) continue;
+            if (x.test(lead[i])) {
+                x ^= ech[i];
+                for (std::size_t w = 0; w < sw; ++w) coords[w] ^= comb[i][w];
+            }
+        if (x.any()) continue;  // not in base + span
+        std::fill(per_block.begin(), per_block.end(), 0);
+        bool ok = true;
+        for (int g = 0; g < s && ok; ++g) {
+            if (!((coords[static_cast<std::size_t>(g) / 64] >> (g % 64)) & 1u)) continue;
+            const int b = block_of[static_cast<std::size_t>(g)];
+            if (b >= 0) ok = ++per_block[static_cast<std::size_t>(b)] <= 2;  // {0, singles, pairs}
+        }
+        if (!ok) continue;
         std::vector<VertexSet> fs;
         for (const auto& f : K.facets) fs.emplace_back(f.bits);
         out.emplace_back(job.m, job.n, std::move(fs), /*embedded=*/true);

@@ -9,7 +9,7 @@
  *   wpm_idcm_orbits         <- idcm_orbits(n, p)            include/plseeds/charmap.hpp:212-281
  *   wpm_charmap_of_dcm      <- charmap_of_dcm(d)            include/plseeds/charmap.hpp:155-204
  *   wpm_cyclic_facet_bound  <- cyclic_facet_bound(n)        include/plseeds/affine_property.hpp:35-45
- *   wpm_plan_create_orbits  <- the per-orbit loop prelude   include/plseeds/pipeline.hpp:379-392
+ *   wpm_plan_create_orbits  <- the per-orbit loop prelude   include/plseeds/pipeline.hpp:54-66
  *                              matroid_universe (pipeline.hpp:33-35) = binary_matroid
  *                              (charmap.hpp:117-141) on the GPU (kernel 1), then
  *                              incidence_matrix (incidence.hpp:34-55) on the GPU (kernel 2)
@@ -23,6 +23,9 @@
  *   wpm_write_cplx          <- write_complexes(os, list)       include/plseeds/complex_io.hpp:21-39
  *   wpm_plan_run_kernel_basis <- enumerate_wpm's own algorithm (kernel basis + combination-space
  *                              odometer, search.hpp:141-258) with every leaf on the GPU
+ *   wpm_plan_run_kernel_basis_prefix <- the per-item odometer (search.hpp:204-243) of one outer prefix
+ *   wpm_plan_verify         <- is_weak_pseudomanifold_direct (complex.hpp:224-233) on every row, plus
+ *                              coordinates in the reference basis (test_gf2.cpp:15-50 style)
  *   wpm_plan_line13         <- Algorithm 2 lines 7 and 13      include/plseeds/pipeline.hpp:58-89
  *                              (std::set union of the per-orbit lists; support == full(m),
  *                              complex.hpp:64-70; is_seed, classify.hpp:51-53)
@@ -197,6 +200,28 @@ int wpm_plan_kernel_basis_stats(const wpm_plan_t *plan, int64_t *leaves, int64_t
 /* combination_space(basis).size_saturated(), kernel dimension s and induced
  * blocks of map `map` (after wpm_plan_run_kernel_basis) */
 int wpm_plan_combination_space(const wpm_plan_t *plan, int32_t map, uint64_t *space, int32_t *s, int32_t *blocks);
+/* Algorithm 1 over ONE map with the first nfixed blocks of its combination
+ * space (widest first, search.hpp:168-170) fixed to candidates
+ * cand[0..nfixed) (0 = none, 1..w = single generator, then the pairs, the
+ * order of search.hpp:88-93): the reference's inner odometer over the
+ * remaining blocks.  The result (same layout as wpm_plan_run; other maps
+ * empty) is every reference-reachable WPM whose coordinates start with that
+ * prefix -- the two-sided completeness check of SURVEY 8(c)(3). */
+int wpm_plan_run_kernel_basis_prefix(wpm_plan_t *plan, int32_t map, int32_t nfixed, const int32_t *cand,
+                                     uint64_t candidate_cap, int64_t *total_out);
+/* widths of map `map`'s combination-space blocks, widest first (1 = free
+ * singleton; block b owns usable generators [sum of widths before b, + w));
+ * returns the block count (writes at most cap) or -status */
+int32_t wpm_plan_space_blocks(wpm_plan_t *plan, int32_t map, int32_t *widths, int32_t cap);
+/* Device verification of the last run (kernel 8): *unsound = rows that fail
+ * the direct WPM test (complex.hpp:224-233: every ridge in 0 or 2 facets),
+ * are empty, leave the universe or exceed the cap.  With reach != 0 also
+ * *unreachable = rows whose coordinates in the reference's convenient basis
+ * (kernel_basis.hpp:84-235) do not exist or use > 2 generators of an induced
+ * block -- rows enumerate_wpm could not produce; coords_out
+ * (optional, one per row, canonical order) receives the coordinates, bit g =
+ * usable generator g in block order.  Needs <= 64 usable generators. */
+int wpm_plan_verify(wpm_plan_t *plan, int32_t reach, int64_t *unsound, int64_t *unreachable, uint64_t *coords_out);
 /* Algorithm 2 lines 7 and 13 on the last run's results (pipeline.hpp:58-89),
  * on the device: the union of every map's WPMs as labeled complexes (line 7,
  * exact duplicates across maps removed), then full support and is_seed

@@ -195,6 +195,10 @@ _SIGS = {
     "wpm_plan_run_kernel_basis": (ctypes.c_int, [_PlanP, ctypes.c_uint64, ctypes.POINTER(_i64)]),
     "wpm_plan_kernel_basis_stats": (ctypes.c_int, [_PlanP, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "wpm_plan_run_kernel_basis_prefix": (ctypes.c_int, [_PlanP, _i32, _i32, _i32p, ctypes.c_uint64,
+                                                        ctypes.POINTER(_i64)]),
+    "wpm_plan_space_blocks": (_i32, [_PlanP, _i32, _i32p, _i32]),
+    "wpm_plan_verify": (ctypes.c_int, [_PlanP, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _u64p]),
     "wpm_plan_combination_space": (ctypes.c_int, [_PlanP, _i32, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(_i32),
                                                   ctypes.POINTER(_i32)]),
 }
@@ -413,6 +417,35 @@ class Plan:
         tot = _i64()
         _check(_lib.wpm_plan_run_kernel_basis(self._h, ctypes.c_uint64(candidate_cap), ctypes.byref(tot)))
         return int(tot.value)
+
+    def run_kernel_basis_prefix(self, map_index: int, cand: Sequence[int], candidate_cap: int = (1 << 64) - 1) -> int:
+        """Algorithm 1 over one map with its first len(cand) blocks fixed to
+        the given candidates (the reference's inner odometer over the rest)."""
+        arr, ap = _i32a(list(cand) or [0])
+        tot = _i64()
+        _check(_lib.wpm_plan_run_kernel_basis_prefix(self._h, map_index, len(cand), ap, ctypes.c_uint64(candidate_cap),
+                                                     ctypes.byref(tot)))
+        return int(tot.value)
+
+    def space_blocks(self, map_index: int) -> List[int]:
+        """Widths of the map's combination-space blocks, widest first."""
+        buf = np.zeros(4096, dtype=np.int32)
+        k = int(_lib.wpm_plan_space_blocks(self._h, map_index, buf.ctypes.data_as(_i32p), len(buf)))
+        if k < 0:
+            _check(-k)
+        return [int(x) for x in buf[:k]]
+
+    def verify(self, reach: bool = False, coords: bool = False):
+        """Kernel 8 on the last run: (unsound rows, unreachable rows or -1,
+        coordinates per row or None)."""
+        a, b = _i64(), _i64()
+        out = np.zeros(max(self.stats_total(), 1), dtype=np.uint64) if coords else None
+        _check(_lib.wpm_plan_verify(self._h, 1 if reach else 0, ctypes.byref(a), ctypes.byref(b),
+                                    out.ctypes.data_as(_u64p) if coords else None))
+        return int(a.value), int(b.value), (out[: self.stats_total()] if coords else None)
+
+    def stats_total(self) -> int:
+        return int(self.device_result()[2])
 
     def kernel_basis_stats(self) -> dict:
         a, b, c, d = _i64(), _i64(), ctypes.c_double(), ctypes.c_double()

@@ -4,7 +4,7 @@
 // charmap_of_dcm (charmap.hpp:155-204) in C++, then everything
 // data-parallel on the device: kernel 1 (universes), kernel 2 (incidence),
 // kernel 3 (search), the canonical sort.  The per-orbit sequential loop of
-// pipeline.hpp:383-397 becomes ONE persistent launch over every map's search
+// pipeline.hpp:58-72 becomes ONE persistent launch over every map's search
 // tree; job.threads / parallel_for_index (parallel.hpp:27-54) becomes the
 // device work queue.  There is no CPU fallback: no device, no result.
 #include <cuda_runtime.h>
@@ -214,7 +214,8 @@ struct wpm_plan {
     DevBuf<uint32_t> d_odo_words;
     DevBuf<unsigned long long> d_odo_ctl;
     long long leaves = 0, checked = 0;
-    double ms_prep = 0;
+    double ms_prep = 0, ms_basis = 0;
+    bool spaces_ok = false;
 };
 
 // ------------------------------------------------------------------ host
@@ -1635,18 +1636,12 @@ static void host_incidence(const std::vector<uint32_t>& facets, HostIncidence* A
 // enumerate_wpm exactly as the reference runs it (search.hpp:141-258): the
 // kernel basis on the host (kbasis.cpp), every leaf of the combination space
 // on the device (k6_odometer.cu), then the same canonical sort
-extern "C" int wpm_plan_run_kernel_basis(wpm_plan_t* P, uint64_t candidate_cap, int64_t* total_out) {
-    if (!P) return fail(WPM_EINVAL, "null plan");
-    CU(cudaSetDevice(P->device));
-    g_alloc_stream = P->stream;
-    P->ran = false;
-    P->line7 = P->line13 = P->line15 = -1;
+// the reference's basis and combination space of every map (kbasis.cpp),
+// built once per plan (the maps and pins are fixed)
+static int ensure_spaces(wpm_plan* P) {
+    if (P->spaces_ok) return WPM_OK;
     const int K = P->num_maps;
-    const int W32 = (P->maxM + 31) / 32;
-    const int Wb = odo_words_bucket(W32);
-    if (Wb < 0) return fail(WPM_EINVAL, "the odometer supports universes of at most 1024 facets");
     const auto t0 = std::chrono::steady_clock::now();
-    // ---- the reference's basis and combination space, per map
     P->spaces.assign(K, {});
     for (int i = 0; i < K; ++i) {
         const MapDesc& d = P->desc[i];
@@ -1662,10 +1657,97 @@ extern "C" int wpm_plan_run_kernel_basis(wpm_plan_t* P, uint64_t candidate_cap, 
                 if ((P->pin_out[(size_t)i * P->mw + (j >> 5)] >> (j & 31)) & 1u) forb.push_back(j);
             }
         if (build_space(A, req, forb, &P->spaces[i])) return fail(WPM_EINFEASIBLE, "link constraints are infeasible");
-        if (P->spaces[i].space > candidate_cap)  // search.hpp:147-150
-            return fail(WPM_ECAP, "combination space of " + std::to_string(P->spaces[i].space) +
-                                      " candidates exceeds cap " + std::to_string(candidate_cap));
     }
+    P->ms_basis = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    P->spaces_ok = true;
+    return WPM_OK;
+}
+
+static int run_odometer(wpm_plan* P, const std::vector<CombinationSpaceHost>& spaces, double ms_prep0,
+                        int64_t* total_out);
+
+extern "C" int wpm_plan_run_kernel_basis(wpm_plan_t* P, uint64_t candidate_cap, int64_t* total_out) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    CU(cudaSetDevice(P->device));
+    g_alloc_stream = P->stream;
+    const bool fresh = !P->spaces_ok;
+    const int rc = ensure_spaces(P);
+    if (rc) return rc;
+    for (const auto& cs : P->spaces)
+        if (cs.space > candidate_cap)  // search.hpp:147-150
+            return fail(WPM_ECAP, "combination space of " + std::to_string(cs.space) + " candidates exceeds cap " +
+                                      std::to_string(candidate_cap));
+    return run_odometer(P, P->spaces, fresh ? P->ms_basis : 0.0, total_out);
+}
+
+// Algorithm 1 over one map with the first `nfixed` blocks (widest first,
+// search.hpp:168-170) fixed to candidates cand[0..nfixed): the reference's
+// per-item odometer (search.hpp:204-243) over the remaining blocks from
+// base' = base ^ the fixed candidates' deltas.  The accepted set is every
+// reference-reachable WPM whose coordinates share that prefix.
+extern "C" int wpm_plan_run_kernel_basis_prefix(wpm_plan_t* P, int32_t map, int32_t nfixed, const int32_t* cand,
+                                                uint64_t candidate_cap, int64_t* total_out) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (map < 0 || map >= P->num_maps) return fail(WPM_EINVAL, "bad map index");
+    CU(cudaSetDevice(P->device));
+    g_alloc_stream = P->stream;
+    const int rc = ensure_spaces(P);
+    if (rc) return rc;
+    const CombinationSpaceHost& cs = P->spaces[map];
+    const int nb = (int)cs.ncand.size();
+    if (nfixed < 0 || nfixed > nb) return fail(WPM_EINVAL, "prefix longer than the block list");
+    std::vector<CombinationSpaceHost> sp(P->num_maps);
+    for (auto& x : sp) x.space = 0;  // every other map: no leaves
+    CombinationSpaceHost& r = sp[map];
+    r.s = cs.s;
+    r.induced_blocks = cs.induced_blocks;
+    r.W32 = cs.W32;
+    r.base = cs.base;
+    size_t first = 0;
+    for (int b = 0; b < nfixed; ++b) {
+        if (cand[b] < 0 || cand[b] >= cs.ncand[b]) return fail(WPM_EINVAL, "prefix candidate out of range");
+        const uint32_t* d = cs.deltas.data() + (first + (size_t)cand[b]) * cs.W32;
+        for (int w = 0; w < cs.W32; ++w) r.base[w] ^= d[w];
+        first += (size_t)cs.ncand[b];
+    }
+    r.ncand.assign(cs.ncand.begin() + nfixed, cs.ncand.end());
+    r.deltas.assign(cs.deltas.begin() + (long)(first * cs.W32), cs.deltas.end());
+    unsigned long long space = 1;
+    bool sat = false;
+    for (int c : r.ncand) {
+        if (!sat && space > ~0ull / (unsigned long long)c) sat = true;
+        if (!sat) space *= (unsigned long long)c;
+    }
+    r.space = sat ? ~0ull : space;
+    if (r.space > candidate_cap)
+        return fail(WPM_ECAP, "prefix space of " + std::to_string(r.space) + " candidates exceeds cap " +
+                                  std::to_string(candidate_cap));
+    return run_odometer(P, sp, 0.0, total_out);
+}
+
+// blocks of map `map`'s combination space, widest first: widths[b] generators
+// each (1 = a free singleton; candidates = 1 + w + w(w-1)/2); returns the block
+// count (writes at most cap) or -status
+extern "C" int32_t wpm_plan_space_blocks(wpm_plan_t* P, int32_t map, int32_t* widths, int32_t cap) {
+    if (!P || map < 0 || map >= P->num_maps) return -fail(WPM_EINVAL, "bad map index");
+    if (cudaSetDevice(P->device) != cudaSuccess) return -fail(WPM_EINTERNAL, "cudaSetDevice failed");
+    g_alloc_stream = P->stream;
+    const int rc = ensure_spaces(P);
+    if (rc) return -rc;
+    const auto& w = P->spaces[map].width;
+    for (int b = 0; b < (int)w.size() && b < cap; ++b) widths[b] = w[b];
+    return (int32_t)w.size();
+}
+
+static int run_odometer(wpm_plan* P, const std::vector<CombinationSpaceHost>& spaces, double ms_prep0,
+                        int64_t* total_out) {
+    P->ran = false;
+    P->line7 = P->line13 = P->line15 = -1;
+    const int K = P->num_maps;
+    const int W32 = (P->maxM + 31) / 32;
+    const int Wb = odo_words_bucket(W32);
+    if (Wb < 0) return fail(WPM_EINVAL, "the odometer supports universes of at most 1024 facets");
+    const auto t0 = std::chrono::steady_clock::now();
     // ---- device tables: vectors at stride Wb (zero padded)
     std::vector<OdoMap> om(K);
     std::vector<int> blk;  // ncand entries, then (after nblk) first-candidate entries
@@ -1678,7 +1760,7 @@ extern "C" int wpm_plan_run_kernel_basis(wpm_plan_t* P, uint64_t candidate_cap, 
     // 128 / 512 / 2048 / 8192 at n = 7: 311 / 139 / 78 / 72 / 83 / 109 ms) --
     // and at most 64K leaves of inner loop per lane
     unsigned long long all_leaves = 0;
-    for (const auto& cs : P->spaces) all_leaves += cs.space;
+    for (const auto& cs : spaces) all_leaves += cs.space;
     const unsigned long long lanes = (unsigned long long)P->num_sms * 64 * 32;
     long long per_lane = 512;
     if (const char* e = std::getenv("WPM_ODO_PER_LANE")) per_lane = std::max(1, std::atoi(e));
@@ -1688,7 +1770,7 @@ extern "C" int wpm_plan_run_kernel_basis(wpm_plan_t* P, uint64_t candidate_cap, 
         for (int w = 0; w < Wb; ++w) words.push_back(w < W32 ? v[w] : 0u);
     };
     for (int i = 0; i < K; ++i) {
-        const CombinationSpaceHost& cs = P->spaces[i];
+        const CombinationSpaceHost& cs = spaces[i];
         const int nb = (int)cs.ncand.size();
         OdoMap& o = om[i];
         o.map = i;
@@ -1751,7 +1833,7 @@ extern "C" int wpm_plan_run_kernel_basis(wpm_plan_t* P, uint64_t candidate_cap, 
         CU(cudaMemcpyAsync(P->d_odo_blk.p, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice, P->stream));
     CU(cudaMemcpyAsync(P->d_odo_words.p, words.data(), words.size() * 4, cudaMemcpyHostToDevice, P->stream));
     P->h2d += (long long)(sizeof(OdoMap) * K + blk.size() * 4 + words.size() * 4);
-    P->ms_prep = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    P->ms_prep = ms_prep0 + std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (P->out_cap == 0) {
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
@@ -1803,6 +1885,141 @@ extern "C" int wpm_plan_run_kernel_basis(wpm_plan_t* P, uint64_t candidate_cap, 
     if (rc) return rc;
     P->ran = true;
     if (total_out) *total_out = P->total;
+    return WPM_OK;
+}
+
+// ------------------------------------------------------------------ verification (k8_verify.cu)
+
+namespace {
+// pivots P (one facet per usable generator) with G|_P invertible, and the
+// inverse's columns: x_i = parity(invcol[i] & y|_P)
+bool solve_pivots(const std::vector<uint32_t>& gens, int s, int W32, std::vector<int32_t>* piv,
+                  std::vector<unsigned long long>* invcol) {
+    std::vector<std::vector<uint32_t>> r(s);
+    for (int i = 0; i < s; ++i) r[i].assign(gens.begin() + (long)i * W32, gens.begin() + (long)(i + 1) * W32);
+    std::vector<unsigned long long> comb(s);  // which generators each reduced row sums
+    for (int i = 0; i < s; ++i) comb[i] = 1ull << i;
+    piv->assign(s, -1);
+    for (int i = 0; i < s; ++i) {
+        int f = -1;
+        for (int w = 0; w < W32 && f < 0; ++w)
+            if (r[i][w]) f = w * 32 + __builtin_ctz(r[i][w]);
+        if (f < 0) return false;  // dependent generators
+        (*piv)[i] = f;
+        for (int j = 0; j < s; ++j)
+            if (j != i && ((r[j][f >> 5] >> (f & 31)) & 1u)) {
+                for (int w = 0; w < W32; ++w) r[j][w] ^= r[i][w];
+                comb[j] ^= comb[i];
+            }
+    }
+    // reduced row i = sum over comb[i] of g, and has a 1 at pivot i and 0 at
+    // every other pivot: y|_P = x A  =>  x_k = sum_i y_{P_i} [k in comb[i]]
+    invcol->assign(s, 0ull);
+    for (int i = 0; i < s; ++i)
+        for (int k = 0; k < s; ++k)
+            if ((comb[i] >> k) & 1ull) (*invcol)[k] |= 1ull << i;
+    return true;
+}
+}  // namespace
+
+// Soundness of every row of the last run (the direct WPM test on the device)
+// and, with reach != 0, reachability in the reference's combination space:
+// coordinates in its usable generators, <= 2 per induced block
+// (SURVEY 8(c)(1)-(2)).  coords_out (optional): one uint64 per row, canonical
+// order -- bit g = generator g of the block order (wpm_plan_space_blocks).
+extern "C" int wpm_plan_verify(wpm_plan_t* P, int32_t reach, int64_t* unsound, int64_t* unreachable,
+                               uint64_t* coords_out) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (!P->ran) return fail(WPM_EINVAL, "verify needs a completed run");
+    CU(cudaSetDevice(P->device));
+    g_alloc_stream = P->stream;
+    const int K = P->num_maps;
+    std::vector<VerifyMap> vm(K);
+    std::vector<uint32_t> words;
+    std::vector<int32_t> ints;
+    std::vector<unsigned long long> u64s;
+    if (reach) {
+        const int rc = ensure_spaces(P);
+        if (rc) return rc;
+    }
+    for (int i = 0; i < K; ++i) {
+        const MapDesc& d = P->desc[i];
+        VerifyMap& v = vm[i];
+        v.M = d.M;
+        v.N = d.N;
+        v.n = d.n;
+        v.cap = d.cap;
+        v.fs = d.fr_stride;
+        v.fr_off = d.fr_off;
+        v.s = -1;
+        v.nblk = 0;
+        if (!reach) continue;
+        const CombinationSpaceHost& cs = P->spaces[i];
+        int s = 0;
+        for (int w : cs.width) s += w;
+        if (s > 64) return fail(WPM_EINVAL, "reachability needs at most 64 usable generators");
+        std::vector<int32_t> piv;
+        std::vector<unsigned long long> inv;
+        if (!solve_pivots(cs.gens, s, cs.W32, &piv, &inv)) return fail(WPM_EINTERNAL, "dependent kernel generators");
+        v.s = s;
+        v.W32 = cs.W32;
+        v.gens_off = (uint32_t)words.size();
+        words.insert(words.end(), cs.gens.begin(), cs.gens.end());
+        v.base_off = (uint32_t)words.size();
+        words.insert(words.end(), cs.base.begin(), cs.base.end());
+        words.resize(words.size() + 64, 0u);  // rows are read up to w32 words
+        v.piv_off = (uint32_t)ints.size();
+        ints.insert(ints.end(), piv.begin(), piv.end());
+        v.inv_off = (uint32_t)u64s.size();
+        u64s.insert(u64s.end(), inv.begin(), inv.end());
+        v.blk_off = (uint32_t)u64s.size();
+        int lo = 0;
+        for (int w : cs.width) {
+            if (w >= 2) {
+                u64s.push_back((w == 64 ? ~0ull : ((1ull << w) - 1ull)) << lo);
+                ++v.nblk;
+            }
+            lo += w;
+        }
+    }
+    DevBuf<VerifyMap> d_vm;
+    DevBuf<uint32_t> d_words;
+    DevBuf<int32_t> d_ints;
+    DevBuf<unsigned long long> d_u64, d_ctl, d_coords;
+    if (d_vm.ensure(K) || d_words.ensure(words.size() + 1) || d_ints.ensure(ints.size() + 1) ||
+        d_u64.ensure(u64s.size() + 1) || d_ctl.ensure(4) || d_coords.ensure((size_t)std::max<long long>(P->total, 1)))
+        return fail(WPM_EINTERNAL, "device allocation failed (verify)");
+    CU(cudaMemcpyAsync(d_vm.p, vm.data(), K * sizeof(VerifyMap), cudaMemcpyHostToDevice, P->stream));
+    if (!words.empty())
+        CU(cudaMemcpyAsync(d_words.p, words.data(), words.size() * 4, cudaMemcpyHostToDevice, P->stream));
+    if (!ints.empty()) CU(cudaMemcpyAsync(d_ints.p, ints.data(), ints.size() * 4, cudaMemcpyHostToDevice, P->stream));
+    if (!u64s.empty())
+        CU(cudaMemcpyAsync(d_u64.p, u64s.data(), u64s.size() * 8, cudaMemcpyHostToDevice, P->stream));
+    CU(cudaMemsetAsync(d_ctl.p, 0, 32, P->stream));
+    VerifyParams vp{};
+    vp.maps = d_vm.p;
+    vp.fr = P->d_fr.p;
+    vp.words = d_words.p;
+    vp.ints = d_ints.p;
+    vp.u64s = d_u64.p;
+    vp.rows = P->d_sorted_bits.p;
+    vp.row_map = P->d_sorted_map.p;
+    vp.count = P->total;
+    vp.w32 = P->w32;
+    vp.cnt_words = (P->maxN + 3) / 4 + 1;
+    vp.reach = reach ? 1 : 0;
+    vp.coords = d_coords.p;
+    vp.flags = nullptr;
+    vp.ctl = d_ctl.p;
+    if (launch_k8_verify(vp, P->num_sms, P->stream))
+        return fail(WPM_EINTERNAL, std::string("verify launch: ") + cudaGetErrorString(cudaGetLastError()));
+    unsigned long long ctl[4];
+    CU(cudaMemcpyAsync(ctl, d_ctl.p, 32, cudaMemcpyDeviceToHost, P->stream));
+    if (coords_out && P->total > 0)
+        CU(cudaMemcpyAsync(coords_out, d_coords.p, (size_t)P->total * 8, cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaStreamSynchronize(P->stream));
+    if (unsound) *unsound = (int64_t)ctl[0];
+    if (unreachable) *unreachable = reach ? (int64_t)(ctl[1] + ctl[2]) : -1;
     return WPM_OK;
 }
 

@@ -7,7 +7,7 @@
 // canonical ridge order (ascending bitmask).  A second shared table maps the
 // colex rank of an n-subset to its facet index, so the candidate facets of a
 // ridge r are {r + v : v not in r} looked up directly -- ascending v gives
-// ascending facet masks, the reference's parent order (incidence.hpp:300).
+// ascending facet masks, the reference's parent order (incidence.hpp:47-52).
 // fr[f] lists f's ridges ascending: dropping a higher vertex gives a smaller
 // mask, so vertices are walked high to low.
 #include <cstdint>

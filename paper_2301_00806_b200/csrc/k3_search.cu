@@ -486,7 +486,7 @@ __device__ __forceinline__ bool descend(WS<C>& w, const MapView& mp, const Searc
         if (w.ndead) return false;
         uint32_t ridge;
         if (w.nopen == 0) {
-            if (w.size > 0) emit(w, mp, p, lane);
+            if (w.size > 0 && w.size <= mp.cap) emit(w, mp, p, lane);  // count_cap at the leaf, search.hpp:218-220
             if (w.size + mp.n + 1 > mp.cap) return false;
             ridge = CLOSED_FRAME;
         } else {

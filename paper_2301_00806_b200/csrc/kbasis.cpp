@@ -272,11 +272,13 @@ int build_space(const HostIncidence& A, const std::vector<int>& required, const 
     // combination_space (search.hpp:81-104): each induced block {0, singles,
     // pairs}, then every uncovered generator as a free {0, g}
     std::vector<std::vector<Vec>> blocks;
+    std::vector<std::vector<int>> bgens;  // the generators of each block
     const Vec zero(base.size(), 0);
     int covered = kb.ones + kb.zeros;
     for (auto [off, wd] : kb.blocks) {
         std::vector<Vec> c{zero};
-        for (int i = 0; i < wd; ++i) c.push_back(kb.gens[off + i]);
+        std::vector<int> gi;
+        for (int i = 0; i < wd; ++i) c.push_back(kb.gens[off + i]), gi.push_back(off + i);
         for (int i = 0; i < wd; ++i)
             for (int j = i + 1; j < wd; ++j) {
                 Vec d = kb.gens[off + i];
@@ -284,11 +286,22 @@ int build_space(const HostIncidence& A, const std::vector<int>& required, const 
                 c.push_back(std::move(d));
             }
         blocks.push_back(std::move(c));
+        bgens.push_back(std::move(gi));
         covered = std::max(covered, off + wd);
     }
-    for (int g = covered; g < (int)kb.gens.size(); ++g) blocks.push_back({zero, kb.gens[g]});
+    for (int g = covered; g < (int)kb.gens.size(); ++g) blocks.push_back({zero, kb.gens[g]}), bgens.push_back({g});
     // widest blocks outermost (search.hpp:168-170, stable)
-    std::stable_sort(blocks.begin(), blocks.end(), [](const auto& a, const auto& b) { return a.size() > b.size(); });
+    std::vector<int> order(blocks.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return blocks[a].size() > blocks[b].size(); });
+    {
+        std::vector<std::vector<Vec>> sb;
+        std::vector<std::vector<int>> sg;
+        for (int i : order) sb.push_back(std::move(blocks[i])), sg.push_back(std::move(bgens[i]));
+        blocks = std::move(sb);
+        bgens = std::move(sg);
+    }
     unsigned long long space = 1;
     bool sat = false;
     for (auto& b : blocks) {
@@ -305,6 +318,16 @@ int build_space(const HostIncidence& A, const std::vector<int>& required, const 
     to32(base, out->base.data());
     out->ncand.clear();
     out->deltas.clear();
+    out->width.clear();
+    out->gens.clear();
+    for (auto& gi : bgens) {
+        out->width.push_back((int)gi.size());
+        for (int g : gi) {
+            const size_t at = out->gens.size();
+            out->gens.resize(at + W32);
+            to32(kb.gens[g], out->gens.data() + at);
+        }
+    }
     for (auto& b : blocks) {
         out->ncand.push_back((int)b.size());
         for (auto& d : b) {

@@ -21,6 +21,13 @@ struct CombinationSpaceHost {
     std::vector<uint32_t> base;   // XOR of the pinned-in generators
     std::vector<int> ncand;       // candidates per block, widest block first
     std::vector<uint32_t> deltas; // sum(ncand) * W32: XOR mask per candidate (candidate 0 = none)
+    // coordinates: the usable generators (every generator of a block or free
+    // singleton, i.e. everything but the pinned ones) in block order -- block b
+    // of the sorted list owns gens [lo_b, lo_b + width_b), lo_b = sum of the
+    // widths before it; its candidates are none, the singles, then the pairs
+    // (i < j), in deltas order (search.hpp:88-93)
+    std::vector<int> width;       // per block (1 = free singleton)
+    std::vector<uint32_t> gens;   // usable generators * W32
 };
 
 // gf2_kernel -> convenient_basis -> apply_link_constraints -> combination

@@ -141,6 +141,35 @@ int l15_dedupe(const uint32_t* d_rows, long long count, int gw, uint32_t* d_sidx
 int l15_gather(const uint32_t* d_rows, int gw, const uint32_t* d_idx, long long count, uint32_t* d_out,
                cudaStream_t st);
 
+// verification of a result (k8_verify.cu): soundness of every row and, with
+// reach, its coordinates in the reference basis
+struct VerifyMap {
+    int32_t M, N, n, cap, fs, W32;
+    uint32_t fr_off;
+    int32_t s;          // usable generators; -1 = no reachability data
+    uint32_t gens_off;  // s * W32 words (words)
+    uint32_t base_off;  // W32 words (words)
+    uint32_t piv_off;   // s pivot facets (ints)
+    uint32_t inv_off;   // s inverse columns (u64s)
+    uint32_t blk_off;   // nblk induced-block generator masks (u64s)
+    int32_t nblk;
+};
+struct VerifyParams {
+    const VerifyMap* maps;
+    const uint16_t* fr;
+    const uint32_t* words;
+    const int32_t* ints;
+    const unsigned long long* u64s;
+    const uint32_t* rows;
+    const uint16_t* row_map;
+    long long count;
+    int w32, cnt_words, reach;
+    unsigned long long* coords;  // optional, one per row
+    uint8_t* flags;              // optional: bit 0 unsound, 1 outside the span, 2 > 2 generators in a block
+    unsigned long long* ctl;     // [0..2] rows with flag bit 0 / 1 / 2
+};
+int launch_k8_verify(const VerifyParams& p, int num_sms, cudaStream_t st);
+
 // INT32 lane-op issue peak (LOP3 + IADD3 chains over every SM), ops/s
 int int_peak_measure(int device, double* ops_per_s);
 
