@@ -137,6 +137,7 @@ struct SearchJob {
     std::uint64_t candidate_cap = std::uint64_t{1} << 48;  // no combination space on the device
     std::function<void(long long, long long)> progress;
     int device = 0;
+    std::vector<std::int32_t> devices;  // several GPUs for one job (threads -> GPUs); empty = `device`
 };
 
 inline std::vector<DualCharMatrix> idcm_orbits(int n, int p) {
@@ -245,10 +246,22 @@ inline std::vector<PureComplex> enumerate_wpm(const SearchJob& job) {
     j.forbidden = job.forbidden.data();
     j.num_forbidden = static_cast<std::int32_t>(job.forbidden.size());
     j.device = job.device;
+    // SearchJob::progress (search.hpp:54): forwarded from the C-ABI's calls
+    auto relay = [](std::int64_t done, std::int64_t total, void* user) {
+        (*static_cast<const std::function<void(long long, long long)>*>(user))(done, total);
+    };
+    if (job.progress) {
+        j.progress = relay;
+        j.progress_user = const_cast<std::function<void(long long, long long)>*>(&job.progress);
+    }
+    j.devices = job.devices.empty() ? nullptr : job.devices.data();
+    j.num_devices = static_cast<std::int32_t>(job.devices.size());
     detail::Result R;
     check(wpm_enumerate(&j, &R.r));
-    if (job.progress) job.progress(1, 1);
-    return detail::complexes_of(R.r, 0, job.m, job.n, job.facets);
+    // result bits index the universe in canonical (ascending) order
+    std::vector<VertexSet> sorted = job.facets;
+    std::sort(sorted.begin(), sorted.end());
+    return detail::complexes_of(R.r, 0, job.m, job.n, sorted);
 }
 
 // the Algorithm-2 per-orbit loop (pipeline.hpp:58-72) for one n in one launch:
@@ -497,13 +510,18 @@ inline std::vector<PureComplex> enumerate_wpm(const SearchJob& job) {
         comb.push_back(std::move(c));
         lead.push_back(l);
     }
+    // facet mask -> index in job.facets (the universe may be in any order)
+    std::vector<std::pair<std::uint64_t, int>> index;
+    index.reserve(job.facets.size());
+    for (int i = 0; i < M; ++i) index.emplace_back(job.facets[static_cast<std::size_t>(i)].bits, i);
+    std::sort(index.begin(), index.end());
     std::vector<PureComplex> out;
     std::vector<int> per_block(kb.blocks.size());
     for (auto& K : plseeds_b200::enumerate_wpm(j)) {
         BitVec x = base;
         for (const auto& f : K.facets) {
-            const auto it = std::lower_bound(job.facets.begin(), job.facets.end(), VertexSet(f.bits));
-            x.flip(static_cast<int>(it - job.facets.begin()));
+            const auto it = std::lower_bound(index.begin(), index.end(), std::make_pair(f.bits, -1));
+            x.flip(it->second);
         }
         std::vector<std::uint64_t> coords(sw, 0);
         for (std::size_t i = 0; i < ech.size(); ++i)

@@ -19,7 +19,9 @@
  *   wpm_plan_run            <- enumerate_wpm(const SearchJob&)  search.hpp:141-258 (kernel 3,
  *                              the ridge-driven DFS) + the canonical merge/sort (:247-257)
  *   wpm_plan_fetch / wpm_result_*  <- std::vector<PureComplex> return value (search.hpp:141)
- *   wpm_enumerate           <- enumerate_wpm(job) one-shot     search.hpp:141-258
+ *   wpm_enumerate           <- enumerate_wpm(job) one-shot     search.hpp:141-258 (job.progress,
+ *                              job.threads -> devices: wpm_job_t.progress / .devices)
+ *   wpm_plan_set_devices ... wpm_plan_run_claim <- parallel_for_index (parallel.hpp:27-54) across GPUs
  *   wpm_write_cplx          <- write_complexes(os, list)       include/plseeds/complex_io.hpp:21-39
  *   wpm_plan_run_kernel_basis <- enumerate_wpm's own algorithm (kernel basis + combination-space
  *                              odometer, search.hpp:141-258) with every leaf on the GPU
@@ -84,8 +86,19 @@ typedef struct {
     const int32_t *forbidden;    /* facet indices pinned out of every K */
     int32_t num_forbidden;
     int32_t device;              /* CUDA ordinal */
-    int32_t shard_index;         /* root-branch partition for multi-GPU runs: */
-    int32_t shard_count;         /* this rank takes root tasks t with t % count == index (0/1 = all) */
+    int32_t shard_index;         /* static root-task partition (a rank's share without a shared */
+    int32_t shard_count;         /* frontier): root tasks t with t % count == index (0/1 = all) */
+    /* SearchJob::progress (search.hpp:54, called per outer item :244): called
+     * from the calling thread while the search runs with (root tasks
+     * finished, root tasks), monotone, the last call done == total; NULL = none */
+    void (*progress)(int64_t done, int64_t total, void *user);
+    void *progress_user;
+    /* SearchJob::threads (search.hpp:52) becomes GPUs: devices[0..num_devices)
+     * run one job (num_devices <= 1: `device` alone) -- the tree is split
+     * below the root and every GPU claims frontier records through one shared
+     * counter (wpm_plan_set_devices) */
+    const int32_t *devices;
+    int32_t num_devices;
 } wpm_job_t;
 
 /* enumeration output: WPMs of every map of the plan, grouped by map, each
@@ -142,8 +155,11 @@ int wpm_plan_create_orbits(int32_t n, int32_t p, int64_t facet_cap, int32_t devi
 int wpm_plan_create_charmaps(int32_t n, int32_t m, int32_t num_maps, const uint32_t *cols,
                              int64_t facet_cap, int32_t device, wpm_plan_t **out);
 /* Explicit universes (SearchJob.facets), one per map; facet_counts[i] masks
- * each, concatenated in `facets`.  required/forbidden apply to map 0 only
- * (pass num_maps == 1 with pins). */
+ * each, concatenated in `facets`, in any order (like the reference's
+ * incidence_matrix, incidence.hpp:34-55): the plan keeps each universe in
+ * canonical (ascending) order -- results and wpm_plan_universe index that
+ * order; required/forbidden index the caller's order and apply to map 0 only
+ * (pass num_maps == 1 with pins).  Duplicate facets -> 2. */
 int wpm_plan_create_universes(int32_t m, int32_t n, int32_t num_maps, const int32_t *facet_counts,
                               const uint64_t *facets, int64_t facet_cap, const int32_t *required,
                               int32_t num_required, const int32_t *forbidden, int32_t num_forbidden,
@@ -173,6 +189,43 @@ int wpm_plan_timing(const wpm_plan_t *plan, double *ms_total, int32_t *warps);
  * uint64 word; uint16 map ids) in canonical order, valid until the next run. */
 int wpm_plan_device_result(const wpm_plan_t *plan, const uint32_t **bits32, const uint16_t **map_ids,
                            int64_t *count, int32_t *words32);
+
+/* ---------------------------------------------------------------- multi-GPU
+ * One job on several GPUs of one process (SearchJob::threads ->
+ * parallel_for_index, parallel.hpp:27-54, becomes GPUs): devices[0] must be
+ * the plan's device; the others get plans of the same maps.  wpm_plan_run
+ * then splits the search tree below the root on devices[0] (split rounds
+ * until the frontier has >= 512 records per GPU), copies the frontier to
+ * every GPU, and each GPU's kernel 3 pulls records through one claim counter
+ * in devices[0]'s HBM (peer atomics over NVLink) and shares them further by
+ * donation; the rows are gathered into devices[0] (peer copies) and sorted
+ * canonically there.  No GPU waits for another.  ndev <= 1 detaches. */
+int wpm_plan_set_devices(wpm_plan_t *plan, const int32_t *devices, int32_t ndev);
+int wpm_plan_create_orbits_multi(int32_t n, int32_t p, int64_t facet_cap, const int32_t *devices, int32_t ndev,
+                                 wpm_plan_t **out);
+/* per device of the last multi-GPU run: kernel-3 ms and search nodes; returns the device count */
+int wpm_plan_device_stats(const wpm_plan_t *plan, int32_t cap, double *ms_out, int64_t *nodes_out);
+/* split below the root before the search: first split depth (branch frames;
+ * 0 = off for single-GPU runs, multi-GPU runs default to 3) */
+int wpm_plan_set_split(wpm_plan_t *plan, int32_t depth);
+/* progress callback of the following runs (see wpm_job_t.progress); NULL = off */
+int wpm_plan_set_progress(wpm_plan_t *plan, void (*fn)(int64_t done, int64_t total, void *user), void *user);
+/* The same protocol across processes (one per GPU): rank 0 calls
+ * wpm_plan_split (rows and nodes above the frontier stay in its plan) and
+ * broadcasts the frontier records (wpm_plan_frontier: a device pointer,
+ * count x recw uint32); the other ranks wpm_plan_load_frontier them.  A
+ * claim counter made by rank 0 (wpm_claim_counter_create, 64-byte CUDA IPC
+ * handle) is opened by the others (wpm_claim_counter_open); every rank then
+ * wpm_plan_run_claim-s and the canonical rows are gathered to rank 0
+ * (wpm_canonical_sort_device there). */
+int wpm_plan_split(wpm_plan_t *plan, int32_t depth, int64_t target, int64_t *count);
+int wpm_plan_frontier(const wpm_plan_t *plan, const uint32_t **recs, int64_t *count, int32_t *recw);
+int wpm_plan_load_frontier(wpm_plan_t *plan, const uint32_t *recs, int64_t count);
+int wpm_claim_counter_create(int32_t device, void **counter, uint8_t *ipc_handle /* 64 bytes, optional */);
+int wpm_claim_counter_open(int32_t device, const uint8_t *ipc_handle, void **counter);
+int wpm_claim_counter_reset(int32_t device, void *counter);
+int wpm_claim_counter_close(int32_t device, void *counter, int32_t opened);
+int wpm_plan_run_claim(wpm_plan_t *plan, void *counter, int64_t *total_out);
 
 /* Canonical sort of rows that already live on `device` (e.g. shards gathered
  * over NCCL): orders (map id, canonical WPM order) into out_bits/out_map and

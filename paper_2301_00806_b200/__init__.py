@@ -106,7 +106,15 @@ class _Job(ctypes.Structure):
         ("device", ctypes.c_int32),
         ("shard_index", ctypes.c_int32),
         ("shard_count", ctypes.c_int32),
+        ("progress", ctypes.c_void_p),
+        ("progress_user", ctypes.c_void_p),
+        ("devices", _i32p),
+        ("num_devices", ctypes.c_int32),
     ]
+
+
+# progress(done, total, user) -- SearchJob::progress (search.hpp:54)
+_PROGRESS = ctypes.CFUNCTYPE(None, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p)
 
 
 class _Complexes(ctypes.Structure):
@@ -195,6 +203,20 @@ _SIGS = {
     "wpm_plan_run_kernel_basis": (ctypes.c_int, [_PlanP, ctypes.c_uint64, ctypes.POINTER(_i64)]),
     "wpm_plan_kernel_basis_stats": (ctypes.c_int, [_PlanP, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "wpm_plan_set_devices": (ctypes.c_int, [_PlanP, _i32p, _i32]),
+    "wpm_plan_create_orbits_multi": (ctypes.c_int, [_i32, _i32, _i64, _i32p, _i32, ctypes.POINTER(_PlanP)]),
+    "wpm_plan_device_stats": (ctypes.c_int, [_PlanP, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64)]),
+    "wpm_plan_set_split": (ctypes.c_int, [_PlanP, _i32]),
+    "wpm_plan_set_progress": (ctypes.c_int, [_PlanP, ctypes.c_void_p, ctypes.c_void_p]),
+    "wpm_plan_split": (ctypes.c_int, [_PlanP, _i32, _i64, ctypes.POINTER(_i64)]),
+    "wpm_plan_frontier": (ctypes.c_int, [_PlanP, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(_i64),
+                                         ctypes.POINTER(_i32)]),
+    "wpm_plan_load_frontier": (ctypes.c_int, [_PlanP, ctypes.c_void_p, _i64]),
+    "wpm_claim_counter_create": (ctypes.c_int, [_i32, ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p]),
+    "wpm_claim_counter_open": (ctypes.c_int, [_i32, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "wpm_claim_counter_reset": (ctypes.c_int, [_i32, ctypes.c_void_p]),
+    "wpm_claim_counter_close": (ctypes.c_int, [_i32, ctypes.c_void_p, _i32]),
+    "wpm_plan_run_claim": (ctypes.c_int, [_PlanP, ctypes.c_void_p, ctypes.POINTER(_i64)]),
     "wpm_plan_run_kernel_basis_prefix": (ctypes.c_int, [_PlanP, _i32, _i32, _i32p, ctypes.c_uint64,
                                                         ctypes.POINTER(_i64)]),
     "wpm_plan_space_blocks": (_i32, [_PlanP, _i32, _i32p, _i32]),
@@ -269,6 +291,29 @@ def canonical_sort_device(device: int, bits32_ptr: int, map_ptr: int, count: int
     return int(d.value)
 
 
+def claim_counter_create(device: int = 0):
+    """(device pointer, 64-byte CUDA IPC handle) of a new shared claim counter."""
+    p = ctypes.c_void_p()
+    h = (ctypes.c_uint8 * 64)()
+    _check(_lib.wpm_claim_counter_create(device, ctypes.byref(p), h))
+    return p.value, bytes(h)
+
+
+def claim_counter_open(device: int, handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    h = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    _check(_lib.wpm_claim_counter_open(device, h, ctypes.byref(p)))
+    return p.value
+
+
+def claim_counter_reset(device: int, ptr: int) -> None:
+    _check(_lib.wpm_claim_counter_reset(device, ptr))
+
+
+def claim_counter_close(device: int, ptr: int, opened: bool) -> None:
+    _check(_lib.wpm_claim_counter_close(device, ptr, 1 if opened else 0))
+
+
 def cyclic_facet_bound(n: int) -> int:
     """affine_property.hpp:35-45."""
     return int(_lib.wpm_cyclic_facet_bound(n))
@@ -338,10 +383,57 @@ class Plan:
         self.num_maps = int(_lib.wpm_plan_num_maps(self._h))
 
     @classmethod
-    def orbits(cls, n: int, p: int = 4, facet_cap: int = WPM_CAP_UBT, device: int = 0) -> "Plan":
+    def orbits(cls, n: int, p: int = 4, facet_cap: int = WPM_CAP_UBT, device: int = 0,
+               devices: Optional[Sequence[int]] = None) -> "Plan":
+        """devices: one job over several GPUs (wpm_plan_create_orbits_multi)."""
         h = _PlanP()
-        _check(_lib.wpm_plan_create_orbits(n, p, facet_cap, device, ctypes.byref(h)))
+        if devices and len(devices) > 1:
+            arr, ap = _i32a(list(devices))
+            _check(_lib.wpm_plan_create_orbits_multi(n, p, facet_cap, ap, len(devices), ctypes.byref(h)))
+        else:
+            _check(_lib.wpm_plan_create_orbits(n, p, facet_cap, device, ctypes.byref(h)))
         return cls(h.value, n, n + p)
+
+    def set_devices(self, devices: Sequence[int]) -> None:
+        arr, ap = _i32a(list(devices) or [0])
+        _check(_lib.wpm_plan_set_devices(self._h, ap, len(devices)))
+
+    def set_split(self, depth: int) -> None:
+        """Split the tree below the root at this branch depth before the search (0 = off)."""
+        _check(_lib.wpm_plan_set_split(self._h, depth))
+
+    def set_progress(self, fn) -> None:
+        """fn(done, total) while runs are in flight (SearchJob::progress); None = off."""
+        self._progress = _PROGRESS(lambda d, t, u: fn(int(d), int(t))) if fn else None
+        _check(_lib.wpm_plan_set_progress(self._h, ctypes.cast(self._progress, ctypes.c_void_p) if fn else None,
+                                          None))
+
+    def device_stats(self):
+        """[(kernel-3 ms, nodes)] per device of the last multi-GPU run."""
+        ms = (ctypes.c_double * 64)()
+        nd = (_i64 * 64)()
+        k = int(_lib.wpm_plan_device_stats(self._h, 64, ms, nd))
+        return [(ms[i], int(nd[i])) for i in range(max(k, 0))]
+
+    # -- the cross-process protocol (one process per GPU, see dist.py)
+    def split(self, depth: int = 3, target: int = 0) -> int:
+        c = _i64()
+        _check(_lib.wpm_plan_split(self._h, depth, target, ctypes.byref(c)))
+        return int(c.value)
+
+    def frontier(self):
+        """(device pointer, records, uint32 words per record) of the last split."""
+        p, c, w = ctypes.c_void_p(), _i64(), _i32()
+        _check(_lib.wpm_plan_frontier(self._h, ctypes.byref(p), ctypes.byref(c), ctypes.byref(w)))
+        return p.value or 0, int(c.value), int(w.value)
+
+    def load_frontier(self, ptr: int, count: int) -> None:
+        _check(_lib.wpm_plan_load_frontier(self._h, ptr or None, count))
+
+    def run_claim(self, counter: int) -> int:
+        tot = _i64()
+        _check(_lib.wpm_plan_run_claim(self._h, counter, ctypes.byref(tot)))
+        return int(tot.value)
 
     @classmethod
     def charmaps(cls, n: int, m: int, cols: Sequence[Sequence[int]], facet_cap: int = WPM_CAP_UBT,
@@ -691,9 +783,12 @@ def canonical_form(m: int, n: int, facets: Sequence[int], device: int = 0) -> Li
 class SearchJob:
     """search.hpp:46-55.  ``basis`` is not needed by the ridge-driven search;
     pins are given directly as facet indices (apply_link_constraints
-    semantics, kernel_basis.hpp:248-321).  ``threads`` and ``candidate_cap``
-    are accepted for API compatibility; the device search has no combination
-    space to cap."""
+    semantics, kernel_basis.hpp:248-321).  ``facets`` may be in any order (the
+    reference's incidence_matrix indexes by hash); results come back in
+    canonical order.  ``progress(done, total)`` is SearchJob::progress;
+    ``devices`` (several GPUs for one job) replaces ``threads``;
+    ``candidate_cap`` is accepted for API compatibility (the device search
+    has no combination space to cap)."""
 
     m: int
     n: int
@@ -704,6 +799,8 @@ class SearchJob:
     threads: int = 1
     candidate_cap: int = 1 << 48
     device: int = 0
+    progress: Optional[object] = None
+    devices: Optional[List[int]] = None
 
 
 def _facet_cap(job: SearchJob) -> int:
@@ -729,14 +826,17 @@ def bits_to_facets(bits_row: np.ndarray, universe: Sequence[int]) -> List[int]:
 
 
 def enumerate_wpm_bits(job: SearchJob) -> Result:
-    """enumerate_wpm returning the canonical bitsets (no PureComplex build)."""
+    """enumerate_wpm returning the canonical bitsets over the universe in
+    ascending (canonical) order (no PureComplex build)."""
     facets = list(job.facets)
     if not facets:
         raise PurityError("incidence of an empty facet set")
-    order = sorted(range(len(facets)), key=lambda i: facets[i])
-    if order != list(range(len(facets))):
-        raise ValueError("SearchJob.facets must be in canonical (ascending) order")
-    with Plan.universes(job.m, job.n, [facets], _facet_cap(job), job.required, job.forbidden, job.device) as p:
+    dev0 = job.devices[0] if job.devices else job.device
+    with Plan.universes(job.m, job.n, [facets], _facet_cap(job), job.required, job.forbidden, dev0) as p:
+        if job.progress is not None:
+            p.set_progress(job.progress)
+        if job.devices and len(job.devices) > 1:
+            p.set_devices(job.devices)
         p.run()
         return p.fetch()
 
@@ -745,7 +845,8 @@ def enumerate_wpm(job: SearchJob) -> List[List[int]]:
     """search.hpp:141-258: every nonempty WPM inside job.facets satisfying the
     properties, canonical order; each as its ascending facet-mask list."""
     res = enumerate_wpm_bits(job)
-    return [bits_to_facets(row, job.facets) for row in res.map_bits(0)]
+    uni = sorted(job.facets)
+    return [bits_to_facets(row, uni) for row in res.map_bits(0)]
 
 
 def matroid_universe(d: DualCharMatrix) -> List[int]:

@@ -14,6 +14,7 @@
 #include <mutex>
 #include <unordered_map>
 #include <chrono>
+#include <functional>
 #include <cstdlib>
 #include <climits>
 #include <cstdio>
@@ -21,6 +22,7 @@
 #include <numeric>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/wpm_b200.h"
@@ -33,6 +35,14 @@ using namespace wpm;
 namespace {
 
 thread_local std::string g_err;
+
+// WPM_TRACE=1: report a pending (non-sticky) CUDA error at a checkpoint
+void trace_pending(const char* where) {
+    static const bool on = std::getenv("WPM_TRACE") != nullptr;
+    if (!on) return;
+    const cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) std::fprintf(stderr, "[wpm] pending CUDA error at %s: %s\n", where, cudaGetErrorString(e));
+}
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -81,6 +91,14 @@ struct DevBuf {
         }
         n = c;
         return 0;
+    }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;  // owning: a copy would free twice
+    DevBuf& operator=(const DevBuf&) = delete;
+    void swap(DevBuf& o) {
+        std::swap(p, o.p);
+        std::swap(n, o.n);
+        std::swap(s, o.s);
     }
     ~DevBuf() {
         if (p) cudaFreeAsync(p, s);
@@ -216,6 +234,30 @@ struct wpm_plan {
     long long leaves = 0, checked = 0;
     double ms_prep = 0, ms_basis = 0;
     bool spaces_ok = false;
+    // frontier (split below the root) and shared-frontier claims
+    DevBuf<uint32_t> d_front;
+    DevBuf<unsigned long long> d_front_ctl, d_acc;
+    unsigned long long front_cap = 0;
+    long long frontier = 0;       // records of the last split
+    int split_depth = 0;          // > 0: split at this branch depth, then search the frontier
+    long long claim_count = 0;
+    unsigned long long* claim_ctr = nullptr;
+    // progress callback (search.hpp:54): root tasks finished / root tasks
+    void (*progress_fn)(int64_t, int64_t, void*) = nullptr;
+    void* progress_user = nullptr;
+    unsigned long long* progress_host = nullptr;  // host-mapped
+    unsigned long long* progress_dev = nullptr;
+    DevBuf<unsigned int> d_root_pend;
+    // multi-GPU: plans of the same maps on the other devices of the job
+    std::vector<wpm_plan*> peers;
+    std::vector<double> dev_ms;   // per device: kernel-3 ms of the last run
+    std::vector<long long> dev_nodes;
+    void* claim_raw = nullptr;  // the shared claim counter of a multi-GPU job (the leader's)
+    std::function<int(int, wpm_plan_t**)> recreate;  // the same plan on another device
+    DevBuf<uint32_t> d_front2, d_gather;
+    bool split_kept = false;  // wpm_plan_split ran: the claim run appends to its rows
+    int ntasks = 0, frame_cap = 64;
+    bool full_depth = false;
 };
 
 // ------------------------------------------------------------------ host
@@ -442,6 +484,11 @@ static int plan_init(wpm_plan* P, int device) {
     if (device < 0 || device >= count || device >= 64) return fail(WPM_EINVAL, "device ordinal out of range");
     P->device = device;
     CU(cudaSetDevice(device));
+    // a non-sticky error left by an earlier call must not fail this plan's
+    // first launch check (a sticky fault still fails every call)
+    const cudaError_t stale = cudaGetLastError();
+    if (stale != cudaSuccess && std::getenv("WPM_TRACE"))
+        std::fprintf(stderr, "[wpm] cleared a stale CUDA error: %s\n", cudaGetErrorString(stale));
     DevCtx& dc = g_dev[device];
     {
         std::lock_guard<std::mutex> lk(g_dev_mu);
@@ -586,6 +633,12 @@ static int create_from_cols(int32_t n, int32_t m, int32_t K, const uint32_t* col
     rc = plan_build_tables(P, foff);
     tr.mark("kernel 2 + sync");
     if (rc) { delete P; return rc; }
+    {
+        std::vector<uint32_t> c(cols, cols + (size_t)K * m);
+        P->recreate = [n, m, K, c, facet_cap](int dev, wpm_plan_t** o) {
+            return create_from_cols(n, m, K, c.data(), facet_cap, dev, o);
+        };
+    }
     *out = P;
     return WPM_OK;
 }
@@ -611,6 +664,14 @@ extern "C" int wpm_plan_create_orbits(int32_t n, int32_t p, int64_t facet_cap, i
     return create_from_cols(n, m, K, cols.data(), facet_cap, device, out);
 }
 
+// Explicit universes (SearchJob.facets), in ANY order: incidence_matrix
+// indexes ridges by hash (incidence.hpp:34-55) and enumerate_wpm rebuilds and
+// sorts its output (search.hpp:247-257), so the reference accepts an
+// unsorted universe.  Here each universe is sorted into the canonical order
+// (the plan's facet j = the j-th smallest mask; results and wpm_plan_universe
+// use that order) and required / forbidden indices (into the caller's order)
+// are remapped.  Duplicate facets are rejected like PureComplex::validate
+// (complex.hpp:50-51).
 extern "C" int wpm_plan_create_universes(int32_t m, int32_t n, int32_t K, const int32_t* counts,
                                          const uint64_t* facets, int64_t facet_cap, const int32_t* required,
                                          int32_t num_required, const int32_t* forbidden, int32_t num_forbidden,
@@ -619,22 +680,30 @@ extern "C" int wpm_plan_create_universes(int32_t m, int32_t n, int32_t K, const 
     if (n < 1 || m < n || m > WPM_MAX_M) return fail(WPM_EINVAL, "unsupported (m, n): need 1 <= n <= m <= 16");
     if (K < 1) return fail(WPM_EINVAL, "no universes");
     if ((num_required || num_forbidden) && K != 1) return fail(WPM_EINVAL, "pins need a single universe");
-    // validate: pure, labels in 1..m, strictly ascending (PureComplex::validate, complex.hpp:37-55)
+    // validate: pure, labels in 1..m (PureComplex::validate, complex.hpp:37-55); sort
     std::vector<uint32_t> h;
     std::vector<uint32_t> foff(K);
+    std::vector<int32_t> rank_of;  // caller index -> canonical index (universe 0, for the pins)
     size_t off = 0;
     const uint64_t full = ((1ull << m) - 1ull) << 1;
     for (int i = 0; i < K; ++i) {
         foff[i] = (uint32_t)off;
         if (counts[i] <= 0) return fail(WPM_EINVAL, "incidence of an empty facet set");
+        std::vector<std::pair<uint64_t, int32_t>> u((size_t)counts[i]);
         for (int j = 0; j < counts[i]; ++j) {
             const uint64_t f = facets[off + j];
             if (f & ~full) return fail(WPM_EINVAL, "facet uses a label outside 1..m");
             if (__builtin_popcountll(f) != n) return fail(WPM_EINVAL, "facet size differs from n (purity)");
-            if (j > 0 && !(facets[off + j - 1] < f))
-                return fail(WPM_EINVAL, "universe not in canonical (strictly ascending) order");
-            h.push_back((uint32_t)f);
+            u[(size_t)j] = {f, j};
         }
+        std::sort(u.begin(), u.end());
+        for (int j = 1; j < counts[i]; ++j)
+            if (u[(size_t)j].first == u[(size_t)j - 1].first) return fail(WPM_EINVAL, "duplicate facet in the universe");
+        if (i == 0) {
+            rank_of.assign((size_t)counts[0], 0);
+            for (int j = 0; j < counts[0]; ++j) rank_of[(size_t)u[(size_t)j].second] = j;
+        }
+        for (const auto& x : u) h.push_back((uint32_t)x.first);
         off += counts[i];
     }
     auto* P = new wpm_plan();
@@ -657,16 +726,25 @@ extern "C" int wpm_plan_create_universes(int32_t m, int32_t n, int32_t K, const 
         P->pin_in.assign(P->mw, 0);
         P->pin_out.assign(P->mw, 0);
         for (int i = 0; i < num_required; ++i) {
-            const int f = required[i];
-            if (f < 0 || f >= M) { delete P; return fail(WPM_EINVAL, "required facet index out of range"); }
+            if (required[i] < 0 || required[i] >= M) { delete P; return fail(WPM_EINVAL, "required facet index out of range"); }
+            const int f = rank_of[(size_t)required[i]];
             P->pin_in[f >> 5] |= 1u << (f & 31);
         }
         for (int i = 0; i < num_forbidden; ++i) {
-            const int f = forbidden[i];
-            if (f < 0 || f >= M) { delete P; return fail(WPM_EINVAL, "forbidden facet index out of range"); }
+            if (forbidden[i] < 0 || forbidden[i] >= M) { delete P; return fail(WPM_EINVAL, "forbidden facet index out of range"); }
+            const int f = rank_of[(size_t)forbidden[i]];
             P->pin_out[f >> 5] |= 1u << (f & 31);
         }
         P->has_pins = true;
+    }
+    {
+        std::vector<int32_t> c(counts, counts + K);
+        std::vector<uint64_t> fa(facets, facets + off);
+        std::vector<int32_t> rq(required, required + num_required), fb(forbidden, forbidden + num_forbidden);
+        P->recreate = [m, n, K, c, fa, facet_cap, rq, fb](int dev, wpm_plan_t** o) {
+            return wpm_plan_create_universes(m, n, K, c.data(), fa.data(), facet_cap, rq.data(), (int32_t)rq.size(),
+                                             fb.data(), (int32_t)fb.size(), dev, o);
+        };
     }
     *out = P;
     return WPM_OK;
@@ -715,54 +793,170 @@ extern "C" int32_t wpm_plan_incidence(wpm_plan_t* P, int32_t map, uint64_t* ridg
 
 static int plan_sort(wpm_plan* P);
 
-static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
-    Trace tr;
-    const int K = P->num_maps;
-    // root tasks: (f, map) f-major so the largest subtrees start first;
-    // pinned universes get one ENTRY task
-    std::vector<int32_t> tm, tf, tk;
+// ---- one kernel-3 launch on the plan's stream: seed (root tasks or task
+// records), optional frontier output (split mode) or shared-frontier claims
+struct K3Launch {
+    const int32_t* d_tm = nullptr;  // root tasks (map, f, kind), ntasks of them
+    const int32_t* d_tf = nullptr;
+    const int32_t* d_tk = nullptr;
+    int ntasks = 0;
+    const uint32_t* d_recs = nullptr;  // or task records (a frontier)
+    long long nrecs = 0;
+    int cutoff = 0;                    // split mode: frames at depth >= cutoff go to d_front_out
+    uint32_t* d_front_out = nullptr;
+    unsigned long long front_cap = 0;
+    const uint32_t* claim_recs = nullptr;  // claim mode
+    long long claim_count = 0;
+    unsigned long long* claim_ctr = nullptr;
+    bool full_depth = false;
+    bool progress = false;             // root-task progress accounting (the main phase)
+};
+
+static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
+    const long long nseed = L.d_recs ? L.nrecs : L.ntasks;
+    const long long nroots = L.claim_recs ? L.claim_count : nseed;
+    int qcap = 1 << 16;
+    while (qcap < 2 * nseed) qcap <<= 1;
+    if (qcap > P->qcap) {
+        P->qcap = qcap;
+        if (P->d_qrec.ensure((size_t)qcap * P->recw) || P->d_qready.ensure(qcap))
+            return fail(WPM_EINTERNAL, "device allocation failed (queue)");
+    }
+    const bool prog = L.progress && P->progress_fn;
+    if (prog && P->d_root_pend.ensure((size_t)std::max<long long>(nroots, 1)))
+        return fail(WPM_EINTERNAL, "device allocation failed (progress)");
+    unsigned long long ctl[3] = {(unsigned long long)nseed << 32, 0, (unsigned long long)nseed};
+    CU(cudaMemcpyAsync(P->d_qctl.p, ctl, sizeof(ctl), cudaMemcpyHostToDevice, P->stream));  // [3], [4] add up
+    CU(cudaMemsetAsync(P->d_qready.p, 0, (size_t)P->qcap * 8, P->stream));
+    P->h2d += (long long)sizeof(ctl);
+    SearchParams sp{};
+    sp.num_maps = P->num_maps;
+    sp.max_M = P->maxM;
+    sp.max_N = P->maxN;
+    sp.max_n = P->n;
+    sp.max_depth = L.full_depth ? P->maxDepth : frame_cap;
+    sp.maps = P->d_maps.p;
+    sp.fr = P->d_fr.p;
+    sp.rp = P->d_rp.p;
+    sp.npar = P->d_npar.p;
+    sp.qrec = P->d_qrec.p;
+    sp.qready = P->d_qready.p;
+    sp.qctl = P->d_qctl.p;
+    sp.qcap = P->qcap;
+    sp.recw = P->recw;
+    sp.mw = P->mw;
+    sp.out_keys = P->d_out_keys.p;
+    sp.out_ctl = P->d_out_ctl.p;
+    sp.per_map = P->d_per_map.p;
+    sp.out_cap = P->out_cap;
+    sp.rw = P->rw;
+    sp.node_budget = P->node_budget;
+    sp.cutoff = L.cutoff;
+    sp.front_out = L.d_front_out;
+    sp.front_ctl = P->d_front_ctl.p;
+    sp.front_cap = L.front_cap;
+    sp.claim_recs = L.claim_recs;
+    sp.claim_count = L.claim_count;
+    sp.claim_ctr = L.claim_ctr;
+    if (prog) {
+        sp.root_pend = P->d_root_pend.p;
+        sp.roots_done = P->d_acc.p;
+        sp.progress_host = P->progress_dev;
+        CU(cudaMemsetAsync(P->d_acc.p, 0, 8, P->stream));
+        *(volatile unsigned long long*)P->progress_host = 0;
+        if (L.claim_recs && launch_fill_u32(sp.root_pend, 1u, nroots, P->stream))
+            return fail(WPM_EINTERNAL, "progress init failed");
+    }
+    if (L.d_recs) {
+        if (launch_seed_records(sp, L.d_recs, L.nrecs, P->stream)) return fail(WPM_EINTERNAL, "seed launch failed");
+    } else if (launch_seed_tasks(sp, L.ntasks, L.d_tm, L.d_tf, L.d_tk, P->has_pins ? P->d_pin_in.p : nullptr,
+                                 P->has_pins ? P->d_pin_out.p : nullptr, P->stream)) {
+        return fail(WPM_EINTERNAL, "seed launch failed");
+    }
+    const int est_warps = P->num_sms * 16;
+    sp.hungry = std::max(64, est_warps / 2);
+    sp.backoff_min = 32;
+    sp.backoff_max = 8192;
+    if (const char* e = std::getenv("WPM_BACKOFF_MIN")) sp.backoff_min = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("WPM_HUNGRY")) sp.hungry = std::atoi(e);
+    if (const char* e = std::getenv("WPM_BACKOFF_MAX")) sp.backoff_max = std::max(32, std::atoi(e));
+    // donation checks: every 16 nodes for small tables (cheap task
+    // loads; n <= 6 ramps/tails faster), 32 otherwise (n = 11 loads cost
+    // O(N) per donated task) -- measured sweep in DESIGN.md
+    sp.check_every = P->maxN <= 256 ? 16 : 32;
+    if (const char* e = std::getenv("WPM_CHECK_EVERY")) sp.check_every = std::max(1, std::atoi(e));
+    sp.donate_max = 1;
+    if (const char* e = std::getenv("WPM_DONATE_MAX")) sp.donate_max = std::max(1, std::atoi(e));
+    // claims: keep about a quarter of the warps' worth of tasks pending;
+    // donation spreads each claimed record over the GPU
+    sp.claim_low = std::max(8, est_warps / 8);
+    if (const char* e = std::getenv("WPM_CLAIM_LOW")) sp.claim_low = std::max(1, std::atoi(e));
+    if ((nseed > 0 || L.claim_recs) && !launch_k3_search(sp, P->num_sms, P->stream, &P->warps))
+        return fail(WPM_EINTERNAL, std::string("kernel 3 launch: ") + cudaGetErrorString(cudaGetLastError()));
+    return WPM_OK;
+}
+
+// the root tasks of the plan (map, minimum facet f) in queue order, or one
+// ENTRY task for a pinned universe; a static shard keeps every count-th
+static void root_tasks(const wpm_plan* P, int shard_index, int shard_count, std::vector<int32_t>* tm,
+                       std::vector<int32_t>* tf, std::vector<int32_t>* tk) {
+    tm->clear();
+    tf->clear();
+    tk->clear();
     if (P->has_pins) {
-        tm.push_back(0);
-        tf.push_back(0);
-        tk.push_back(3);
+        tm->push_back(0);
+        tf->push_back(0);
+        tk->push_back(3);
     } else {
         // map-major: at any moment the warps of an SM share few maps, so the
         // per-map tables stay L1 resident; donations balance the load
-        for (int i = 0; i < K; ++i)
+        for (int i = 0; i < P->num_maps; ++i)
             for (int f = 0; f < P->M[i]; ++f)
                 if (P->n + 1 <= P->cap[i]) {
-                    tm.push_back(i);
-                    tf.push_back(f);
-                    tk.push_back(0);
+                    tm->push_back(i);
+                    tf->push_back(f);
+                    tk->push_back(0);
                 }
     }
     if (shard_count > 1) {
         size_t k = 0;
-        for (size_t t = 0; t < tm.size(); ++t)
+        for (size_t t = 0; t < tm->size(); ++t)
             if ((int)(t % shard_count) == shard_index) {
-                tm[k] = tm[t];
-                tf[k] = tf[t];
-                tk[k] = tk[t];
+                (*tm)[k] = (*tm)[t];
+                (*tf)[k] = (*tf)[t];
+                (*tk)[k] = (*tk)[t];
                 ++k;
             }
-        tm.resize(k);
-        tf.resize(k);
-        tk.resize(k);
+        tm->resize(k);
+        tf->resize(k);
+        tk->resize(k);
     }
+}
+
+// ---- phases of one search (composable: single GPU, split + search, claims)
+
+// allocations, root tasks on the device, output sizing
+static int search_prepare(wpm_plan* P, int shard_index, int shard_count) {
+    const int K = P->num_maps;
+    std::vector<int32_t> tm, tf, tk;
+    root_tasks(P, shard_index, shard_count, &tm, &tf, &tk);
     const int ntasks = (int)tm.size();
-    int qcap = 1 << 16;
-    while (qcap < 2 * ntasks) qcap <<= 1;
-    P->qcap = qcap;
-    if (P->d_qrec.ensure((size_t)qcap * P->recw) || P->d_qready.ensure(qcap) || P->d_qctl.ensure(8) ||
-        P->d_task_map.ensure(ntasks + 1) || P->d_task_f.ensure(ntasks + 1) || P->d_task_kind.ensure(ntasks + 1) ||
-        P->d_out_ctl.ensure(4) || P->d_per_map.ensure(K))
+    P->ntasks = ntasks;
+    if (P->d_qctl.ensure(8) || P->d_acc.ensure(4) || P->d_task_map.ensure(ntasks + 1) ||
+        P->d_task_f.ensure(ntasks + 1) || P->d_task_kind.ensure(ntasks + 1) || P->d_out_ctl.ensure(4) ||
+        P->d_per_map.ensure(K) || P->d_front_ctl.ensure(2))
         return fail(WPM_EINTERNAL, "device allocation failed (queue)");
-    tr.mark("  run: tasks + queue alloc");
     if (P->has_pins) {
         if (P->d_pin_in.ensure(P->mw) || P->d_pin_out.ensure(P->mw))
             return fail(WPM_EINTERNAL, "device allocation failed (pins)");
         CU(cudaMemcpyAsync(P->d_pin_in.p, P->pin_in.data(), P->mw * 4, cudaMemcpyHostToDevice, P->stream));
         CU(cudaMemcpyAsync(P->d_pin_out.p, P->pin_out.data(), P->mw * 4, cudaMemcpyHostToDevice, P->stream));
+    }
+    if (ntasks) {
+        CU(cudaMemcpyAsync(P->d_task_map.p, tm.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
+        CU(cudaMemcpyAsync(P->d_task_f.p, tf.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
+        CU(cudaMemcpyAsync(P->d_task_kind.p, tk.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
+        P->h2d += 12LL * ntasks;
     }
     if (P->out_cap == 0) {
         // first run: 2^21 rows covers every Picard-4 n (the most WPMs of any
@@ -775,101 +969,162 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
         P->out_cap = std::min<unsigned long long>(std::max<unsigned long long>(fr / 16 / row, 1ull << 16), 1ull << 21);
         if (const char* e = std::getenv("WPM_OUT_CAP")) P->out_cap = std::max(1ull, std::strtoull(e, nullptr, 10));
     }
-    CU(cudaEventRecord(P->ev[4], P->stream));
+    if (P->front_cap == 0) P->front_cap = 1ull << 16;
     // frame stack sized for the branch depths the search reaches in practice
     // (<= 37 measured up to n = 11); a run that outgrows it is redone with
     // the worst-case layout (fewer warps per SM)
-    int frame_cap = 64;
-    if (const char* e = std::getenv("WPM_FRAME_CAP")) frame_cap = std::max(1, std::atoi(e));
-    bool full_depth = P->maxDepth <= frame_cap;
-    for (int attempt = 0; attempt < 3; ++attempt) {
-        if (P->d_out_keys.ensure(P->out_cap * P->rw)) return fail(WPM_EINTERNAL, "device allocation failed (output)");
-        if (ntasks) {
-            CU(cudaMemcpyAsync(P->d_task_map.p, tm.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
-            CU(cudaMemcpyAsync(P->d_task_f.p, tf.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
-            CU(cudaMemcpyAsync(P->d_task_kind.p, tk.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
-            P->h2d += 12LL * ntasks;
+    P->frame_cap = 64;
+    if (const char* e = std::getenv("WPM_FRAME_CAP")) P->frame_cap = std::max(1, std::atoi(e));
+    if (!P->full_depth) P->full_depth = P->maxDepth <= P->frame_cap;
+    return WPM_OK;
+}
+
+// start of an attempt: empty outputs and counters, start event
+static int search_reset(wpm_plan* P) {
+    if (P->d_out_keys.ensure(P->out_cap * P->rw)) return fail(WPM_EINTERNAL, "device allocation failed (output)");
+    CU(cudaMemsetAsync(P->d_out_ctl.p, 0, 32, P->stream));
+    CU(cudaMemsetAsync(P->d_acc.p, 0, 32, P->stream));
+    CU(cudaMemsetAsync(P->d_qctl.p, 0, 64, P->stream));
+    CU(cudaEventRecord(P->ev[0], P->stream));
+    P->frontier = 0;
+    return WPM_OK;
+}
+
+// phase A: a split launch from the root tasks; frames at split_depth become
+// frontier records (everything above them is searched here).  Synchronous:
+// returns the record count in P->frontier (> front_cap: overflowed)
+static int search_split(wpm_plan* P, int split_depth) {
+    if (P->d_front.ensure(P->front_cap * P->recw)) return fail(WPM_EINTERNAL, "allocation failed (frontier)");
+    CU(cudaMemsetAsync(P->d_front_ctl.p, 0, 16, P->stream));
+    K3Launch a;
+    a.d_tm = P->d_task_map.p;
+    a.d_tf = P->d_task_f.p;
+    a.d_tk = P->d_task_kind.p;
+    a.ntasks = P->ntasks;
+    a.cutoff = split_depth;
+    a.d_front_out = P->d_front.p;
+    a.front_cap = P->front_cap;
+    a.full_depth = P->full_depth;
+    int rc = k3_launch(P, a, P->frame_cap);
+    if (rc) return rc;
+    unsigned long long fc = 0;
+    CU(cudaMemcpyAsync(&fc, P->d_front_ctl.p, 8, cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaStreamSynchronize(P->stream));
+    P->d2h += 8;
+    P->frontier = (long long)fc;
+    return WPM_OK;
+}
+
+// phase B, asynchronous: the root tasks, the frontier records, or (claim)
+// the shared frontier
+enum MainSrc { SRC_ROOTS, SRC_FRONTIER, SRC_CLAIM };
+static int search_main(wpm_plan* P, MainSrc src) {
+    K3Launch b;
+    b.full_depth = P->full_depth;
+    b.progress = true;
+    if (src == SRC_CLAIM) {
+        b.claim_recs = P->d_front.p;
+        b.claim_count = P->claim_count;
+        b.claim_ctr = P->claim_ctr;
+    } else if (src == SRC_FRONTIER) {
+        b.d_recs = P->d_front.p;
+        b.nrecs = P->frontier;
+    } else {
+        b.d_tm = P->d_task_map.p;
+        b.d_tf = P->d_task_f.p;
+        b.d_tk = P->d_task_kind.p;
+        b.ntasks = P->ntasks;
+    }
+    const int rc = k3_launch(P, b, P->frame_cap);
+    if (rc) return rc;
+    CU(cudaEventRecord(P->ev[1], P->stream));
+    return WPM_OK;
+}
+
+// end of an attempt: wait (calling the progress callback meanwhile), read
+// counts.  *again = 1: rerun the attempt (frame stack / output / frontier
+// outgrew its buffer; the buffers are resized)
+static int search_finish(wpm_plan* P, long long progress_total, int* again) {
+    *again = 0;
+    unsigned long long octl[4], qc[8];
+    CU(cudaMemcpyAsync(octl, P->d_out_ctl.p, 32, cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaMemcpyAsync(qc, P->d_qctl.p, 64, cudaMemcpyDeviceToHost, P->stream));
+    if (P->progress_fn) {
+        // the reference's progress(done, total) (search.hpp:54, :244): root
+        // tasks finished, published by the kernel to host-mapped memory
+        unsigned long long seen = 0;
+        while (cudaEventQuery(P->ev[1]) == cudaErrorNotReady) {
+            const unsigned long long v = *(volatile unsigned long long*)P->progress_host;
+            if (v > seen && (long long)v < progress_total) {
+                seen = v;
+                P->progress_fn((int64_t)v, (int64_t)progress_total, P->progress_user);
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(200));
         }
-        unsigned long long ctl[8] = {(unsigned long long)ntasks << 32, 0, (unsigned long long)ntasks, 0, 0, 0, 0, 0};
-        CU(cudaMemcpyAsync(P->d_qctl.p, ctl, sizeof(ctl), cudaMemcpyHostToDevice, P->stream));
-        CU(cudaMemsetAsync(P->d_qready.p, 0, (size_t)qcap * 8, P->stream));
-        CU(cudaMemsetAsync(P->d_out_ctl.p, 0, 32, P->stream));
-        SearchParams sp{};
-        sp.num_maps = K;
-        sp.max_M = P->maxM;
-        sp.max_N = P->maxN;
-        sp.max_n = P->n;
-        sp.max_depth = full_depth ? P->maxDepth : frame_cap;
-        sp.maps = P->d_maps.p;
-        sp.fr = P->d_fr.p;
-        sp.rp = P->d_rp.p;
-        sp.npar = P->d_npar.p;
-        sp.qrec = P->d_qrec.p;
-        sp.qready = P->d_qready.p;
-        sp.qctl = P->d_qctl.p;
-        sp.qcap = qcap;
-        sp.recw = P->recw;
-        sp.mw = P->mw;
-        sp.out_keys = P->d_out_keys.p;
-        sp.out_ctl = P->d_out_ctl.p;
-        sp.per_map = P->d_per_map.p;
-        sp.out_cap = P->out_cap;
-        sp.rw = P->rw;
-        sp.node_budget = P->node_budget;
-        if (launch_seed_tasks(sp, ntasks, P->d_task_map.p, P->d_task_f.p, P->d_task_kind.p,
-                              P->has_pins ? P->d_pin_in.p : nullptr, P->has_pins ? P->d_pin_out.p : nullptr,
-                              P->stream))
-            return fail(WPM_EINTERNAL, "seed launch failed");
-        const int est_warps = P->num_sms * 16;
-        sp.hungry = std::max(64, est_warps / 2);
-        sp.backoff_min = 32;
-        sp.backoff_max = 8192;
-        if (const char* e = std::getenv("WPM_BACKOFF_MIN")) sp.backoff_min = std::max(1, std::atoi(e));
-        if (const char* e = std::getenv("WPM_HUNGRY")) sp.hungry = std::atoi(e);
-        if (const char* e = std::getenv("WPM_BACKOFF_MAX")) sp.backoff_max = std::max(32, std::atoi(e));
-        // donation checks: every 16 nodes for small tables (cheap task
-        // loads; n <= 6 ramps/tails faster), 32 otherwise (n = 11 loads cost
-        // O(N) per donated task) -- measured sweep in DESIGN.md
-        sp.check_every = P->maxN <= 256 ? 16 : 32;
-        if (const char* e = std::getenv("WPM_CHECK_EVERY")) sp.check_every = std::max(1, std::atoi(e));
-        sp.donate_max = 1;
-        if (const char* e = std::getenv("WPM_DONATE_MAX")) sp.donate_max = std::max(1, std::atoi(e));
-        tr.mark("  run: output alloc, H2D, seed");
-        CU(cudaEventRecord(P->ev[0], P->stream));
-        if (ntasks > 0 && !launch_k3_search(sp, P->num_sms, P->stream, &P->warps))
-            return fail(WPM_EINTERNAL, std::string("kernel 3 launch: ") + cudaGetErrorString(cudaGetLastError()));
-        CU(cudaEventRecord(P->ev[1], P->stream));
-        unsigned long long octl[4], qc[8];
-        CU(cudaMemcpyAsync(octl, P->d_out_ctl.p, 32, cudaMemcpyDeviceToHost, P->stream));
-        CU(cudaMemcpyAsync(qc, P->d_qctl.p, sizeof(qc), cudaMemcpyDeviceToHost, P->stream));
-        tr.mark("  run: k3 launch");
-        CU(cudaStreamSynchronize(P->stream));
-        tr.mark("  run: k3 sync");
-        P->h2d += (long long)sizeof(ctl);
-        P->d2h += 32 + (long long)sizeof(qc);
-        P->total = (long long)octl[0];
-        P->tasks = (long long)qc[3];
-        P->nodes = (long long)qc[4];
-        if (std::getenv("WPM_PROFILE") && (qc[5] | qc[6] | qc[7])) {
-            const double all = (double)(qc[5] + qc[6] + qc[7]);
-            std::fprintf(stderr, "[wpm] warp clocks: busy %.1f%%  waiting %.1f%%  final wait %.1f%%  (tasks %llu)\n",
-                         100.0 * qc[5] / all, 100.0 * qc[6] / all, 100.0 * qc[7] / all, qc[3]);
-        }
-        P->truncated = octl[3] != 0;
-        if (octl[2]) {  // frame stack overflowed: redo with the full-depth layout
-            full_depth = true;
-            ++P->reruns;
-            continue;
-        }
-        if (P->truncated) {  // a budgeted stress run: keep what fits, no rerun
-            P->total = std::min<long long>(P->total, (long long)P->out_cap);
-            break;
-        }
-        if (octl[0] <= P->out_cap) break;
+    }
+    CU(cudaStreamSynchronize(P->stream));
+    if (P->progress_fn) P->progress_fn((int64_t)progress_total, (int64_t)progress_total, P->progress_user);
+    P->d2h += 96;
+    P->total = (long long)octl[0];
+    P->tasks = (long long)qc[3];  // kernel-3 launches of one attempt add up in qctl[3] / [4]
+    P->nodes = (long long)qc[4];
+    if (std::getenv("WPM_PROFILE") && (qc[5] | qc[6] | qc[7])) {
+        const double all = (double)(qc[5] + qc[6] + qc[7]);
+        std::fprintf(stderr, "[wpm] warp clocks: busy %.1f%%  waiting %.1f%%  final wait %.1f%%  (tasks %llu)\n",
+                     100.0 * qc[5] / all, 100.0 * qc[6] / all, 100.0 * qc[7] / all, qc[3]);
+    }
+    P->truncated = octl[3] != 0;
+    if (octl[2]) {  // frame stack overflowed: redo with the full-depth layout
+        P->full_depth = true;
+        ++P->reruns;
+        *again = 1;
+        return WPM_OK;
+    }
+    if (P->truncated) {  // a budgeted stress run: keep what fits, no rerun
+        P->total = std::min<long long>(P->total, (long long)P->out_cap);
+        return WPM_OK;
+    }
+    if (octl[0] > P->out_cap) {
         ++P->reruns;
         P->out_cap = octl[0] + octl[0] / 8 + 1024;  // exact count known now: rerun once
+        *again = 1;
     }
-    return plan_sort(P);
+    return WPM_OK;
+}
+
+// single GPU: [split, then the frontier] or the root tasks
+static int plan_search_phases(wpm_plan* P, int shard_index, int shard_count) {
+    Trace tr;
+    int rc = search_prepare(P, shard_index, shard_count);
+    if (rc) return rc;
+    tr.mark("  run: tasks + queue alloc");
+    CU(cudaEventRecord(P->ev[4], P->stream));
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        if ((rc = search_reset(P))) return rc;
+        long long roots = P->ntasks;
+        if (P->split_depth > 0) {
+            if ((rc = search_split(P, P->split_depth))) return rc;
+            if ((unsigned long long)P->frontier > P->front_cap) {  // rerun with the exact size
+                P->front_cap = (unsigned long long)P->frontier + (unsigned long long)P->frontier / 4 + 1024;
+                ++P->reruns;
+                continue;
+            }
+            roots = P->frontier;
+            tr.mark("  run: split");
+        }
+        if ((rc = search_main(P, P->split_depth > 0 ? SRC_FRONTIER : SRC_ROOTS))) return rc;
+        tr.mark("  run: k3 launch");
+        int again = 0;
+        if ((rc = search_finish(P, roots, &again))) return rc;
+        tr.mark("  run: k3 sync");
+        if (!again) break;
+    }
+    return WPM_OK;
+}
+
+static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
+    const int rc = plan_search_phases(P, shard_index, shard_count);
+    return rc ? rc : plan_sort(P);
 }
 
 // canonical sort of the key rows in d_out_keys (P->total of them), per-map
@@ -914,6 +1169,8 @@ static int plan_sort(wpm_plan* P) {
     return WPM_OK;
 }
 
+static int plan_run_multi(wpm_plan* P);
+
 extern "C" int wpm_plan_run(wpm_plan_t* P, int32_t shard_index, int32_t shard_count, int64_t* total_out) {
     if (!P) return fail(WPM_EINVAL, "null plan");
     if (shard_count < 1) shard_count = 1;
@@ -922,10 +1179,369 @@ extern "C" int wpm_plan_run(wpm_plan_t* P, int32_t shard_index, int32_t shard_co
     g_alloc_stream = P->stream;
     P->ran = false;
     P->line7 = P->line13 = P->line15 = -1;
-    const int rc = plan_search(P, shard_index, shard_count);
+    const int rc = P->peers.empty() ? plan_search(P, shard_index, shard_count) : plan_run_multi(P);
     if (rc) return rc;
     P->ran = true;
     if (total_out) *total_out = P->total;
+    return WPM_OK;
+}
+
+// ------------------------------------------------------------------ multi-GPU
+
+namespace {
+
+// split rounds on the plan: from the root tasks at `depth`, then (while the
+// frontier is smaller than `target`) from the frontier two levels deeper.
+// Rows and nodes of everything above the final frontier stay in the plan.
+int split_rounds(wpm_plan* P, int depth, long long target) {
+    if (P->d_front2.ensure(1)) return fail(WPM_EINTERNAL, "allocation failed (frontier)");
+    int rc = search_split(P, depth);
+    if (rc) return rc;
+    for (int round = 1; round < 8; ++round) {
+        if ((unsigned long long)P->frontier > P->front_cap) return WPM_OK;  // caller reruns with room
+        if (P->frontier >= target || P->frontier == 0) return WPM_OK;
+        depth += 2;
+        if (P->d_front2.ensure(P->front_cap * P->recw)) return fail(WPM_EINTERNAL, "allocation failed (frontier)");
+        P->d_front.swap(P->d_front2);  // the current frontier seeds the next round
+        CU(cudaMemsetAsync(P->d_front_ctl.p, 0, 16, P->stream));
+        K3Launch a;
+        a.d_recs = P->d_front2.p;
+        a.nrecs = P->frontier;
+        a.cutoff = depth;
+        a.d_front_out = P->d_front.p;
+        a.front_cap = P->front_cap;
+        a.full_depth = P->full_depth;
+        if ((rc = k3_launch(P, a, P->frame_cap))) return rc;
+        unsigned long long fc = 0;
+        CU(cudaMemcpyAsync(&fc, P->d_front_ctl.p, 8, cudaMemcpyDeviceToHost, P->stream));
+        CU(cudaStreamSynchronize(P->stream));
+        P->d2h += 8;
+        P->frontier = (long long)fc;
+    }
+    return WPM_OK;
+}
+
+int enable_peer(int dev, int leader) {
+    if (dev == leader) return WPM_OK;
+    int ok = 0;
+    CU(cudaDeviceCanAccessPeer(&ok, dev, leader));
+    if (!ok) return fail(WPM_EINTERNAL, "no peer access between the job's GPUs (the shared claim counter needs P2P)");
+    CU(cudaSetDevice(dev));
+    const cudaError_t e = cudaDeviceEnablePeerAccess(leader, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return fail(WPM_EINTERNAL, "cudaDeviceEnablePeerAccess failed");
+    cudaGetLastError();
+    return WPM_OK;
+}
+
+// frontier target: enough records that dynamic claims balance the GPUs (a
+// few hundred per GPU); the split depth grows two levels per round until then
+long long frontier_target(int ndev) { return std::max<long long>(1024, 512LL * ndev); }
+
+}  // namespace
+
+// One job over the leader plan and its peers (one plan per device, same
+// maps): the leader splits the tree below the root (split_rounds), copies the
+// frontier to every device, and every device's kernel 3 pulls frontier
+// records through ONE claim counter in the leader's HBM (system-scope atomics
+// over NVLink) into its own work queue, sharing them further by donation.
+// No device waits for another; the rows are gathered into the leader with
+// peer copies and sorted there once.  Host: one thread per device.
+static int plan_run_multi(wpm_plan* P) {
+    Trace tr;
+    auto peek = [&](const char* where) {
+        const cudaError_t e = cudaPeekAtLastError();
+        if (e != cudaSuccess && tr.on) std::fprintf(stderr, "[wpm] pending CUDA error after %s: %s\n", where, cudaGetErrorString(e));
+    };
+    const int W = 1 + (int)P->peers.size();
+    std::vector<wpm_plan*> all{P};
+    for (auto* q : P->peers) all.push_back(q);
+    int rc = search_prepare(P, 0, 1);
+    if (rc) return rc;
+    CU(cudaEventRecord(P->ev[4], P->stream));
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        CU(cudaSetDevice(P->device));
+        g_alloc_stream = P->stream;
+        if ((rc = search_reset(P))) return rc;
+        if ((rc = split_rounds(P, P->split_depth > 0 ? P->split_depth : 3, frontier_target(W)))) return rc;
+        if ((unsigned long long)P->frontier > P->front_cap) {
+            P->front_cap = (unsigned long long)P->frontier + (unsigned long long)P->frontier / 4 + 1024;
+            ++P->reruns;
+            continue;
+        }
+        tr.mark("  multi: split");
+        peek("split");
+        const long long F = P->frontier;
+        if (!P->claim_raw) {  // plain cudaMalloc: peers reach it through P2P (pool memory would need pool access)
+            CU(cudaMalloc(&P->claim_raw, 64));
+        }
+        CU(cudaMemsetAsync(P->claim_raw, 0, 64, P->stream));
+        P->claim_count = F;
+        P->claim_ctr = static_cast<unsigned long long*>(P->claim_raw);
+        for (auto* q : P->peers) {
+            CU(cudaSetDevice(q->device));
+            g_alloc_stream = q->stream;
+            if ((rc = search_prepare(q, 0, 1)) || (rc = search_reset(q))) return rc;
+            if (q->d_front.ensure((size_t)std::max<long long>(F, 1) * q->recw))
+                return fail(WPM_EINTERNAL, "allocation failed (peer frontier)");
+            CU(cudaStreamSynchronize(q->stream));
+            if (F) CU(cudaMemcpyPeerAsync(q->d_front.p, q->device, P->d_front.p, P->device, (size_t)F * P->recw * 4, P->stream));
+            q->claim_count = F;
+            q->claim_ctr = P->claim_ctr;
+        }
+        CU(cudaSetDevice(P->device));
+        CU(cudaStreamSynchronize(P->stream));
+        tr.mark("  multi: frontier to peers");
+        peek("frontier copies");
+        // every device claims from the shared frontier
+        std::vector<int> rcs(W, 0), again(W, 0);
+        std::vector<std::thread> th;
+        for (int d = 1; d < W; ++d)
+            th.emplace_back([&, d]() {
+                wpm_plan* q = all[d];
+                if (cudaSetDevice(q->device) != cudaSuccess) {
+                    rcs[d] = fail(WPM_EINTERNAL, "cudaSetDevice failed");
+                    return;
+                }
+                g_alloc_stream = q->stream;
+                rcs[d] = search_main(q, SRC_CLAIM);
+                if (!rcs[d]) rcs[d] = search_finish(q, F, &again[d]);
+            });
+        rcs[0] = search_main(P, SRC_CLAIM);
+        if (!rcs[0]) rcs[0] = search_finish(P, F, &again[0]);
+        for (auto& t : th) t.join();
+        CU(cudaSetDevice(P->device));
+        g_alloc_stream = P->stream;
+        for (int d = 0; d < W; ++d)
+            if (rcs[d]) return rcs[d];
+        tr.mark("  multi: claim phase");
+        peek("claim phase");
+        bool redo = false;
+        for (int d = 0; d < W; ++d) redo |= again[d] != 0;
+        if (redo) {
+            for (int d = 1; d < W; ++d) all[d]->full_depth |= all[0]->full_depth;
+            continue;
+        }
+        break;
+    }
+    // gather every device's key rows into the leader, then one canonical sort
+    long long total = 0, nodes = 0, tasks = 0;
+    P->dev_ms.assign(W, 0.0);
+    P->dev_nodes.assign(W, 0);
+    for (int d = 0; d < W; ++d) {
+        total += all[d]->total;
+        nodes += all[d]->nodes;
+        tasks += all[d]->tasks;
+        float ms = 0;
+        CU(cudaSetDevice(all[d]->device));
+        CU(cudaEventElapsedTime(&ms, all[d]->ev[0], all[d]->ev[1]));
+        P->dev_ms[d] = ms;
+        P->dev_nodes[d] = all[d]->nodes;
+    }
+    CU(cudaSetDevice(P->device));
+    if (P->d_gather.ensure((size_t)std::max<long long>(total, 1) * P->rw))
+        return fail(WPM_EINTERNAL, "device allocation failed (gather)");
+    long long at = 0;
+    for (int d = 0; d < W; ++d) {
+        const size_t bytes = (size_t)all[d]->total * P->rw * 4;
+        if (bytes)
+            CU(cudaMemcpyPeerAsync(P->d_gather.p + (size_t)at * P->rw, P->device, all[d]->d_out_keys.p, all[d]->device,
+                                   bytes, P->stream));
+        at += all[d]->total;
+        if (d) P->d2h += 0;  // peer copies stay on NVLink
+    }
+    P->d_out_keys.swap(P->d_gather);
+    P->total = total;
+    P->nodes = nodes;
+    P->tasks = tasks;
+    tr.mark("  multi: gather");
+    peek("gather");
+    const int src = plan_sort(P);
+    peek("sort");
+    return src;
+}
+
+// a plan spanning devices[0..ndev): devices[0] must be the plan's device; the
+// other devices get plans of the same maps (peers); wpm_plan_run then runs
+// the job on all of them (plan_run_multi) and leaves the canonical result on
+// the leader.  ndev <= 1 detaches the peers.
+extern "C" int wpm_plan_set_devices(wpm_plan_t* P, const int32_t* devices, int32_t ndev) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    for (auto* q : P->peers) wpm_plan_destroy(q);
+    P->peers.clear();
+    if (ndev <= 1) return WPM_OK;
+    if (devices[0] != P->device) return fail(WPM_EINVAL, "devices[0] must be the plan's device");
+    if (!P->recreate) return fail(WPM_EINVAL, "this plan cannot be replicated");
+    for (int i = 1; i < ndev; ++i) {
+        int rc = enable_peer(devices[i], P->device);
+        if (rc) return rc;
+        wpm_plan_t* q = nullptr;
+        rc = P->recreate(devices[i], &q);
+        if (rc) return rc;
+        q->split_depth = P->split_depth;
+        P->peers.push_back(q);
+    }
+    CU(cudaSetDevice(P->device));
+    g_alloc_stream = P->stream;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_create_orbits_multi(int32_t n, int32_t p, int64_t facet_cap, const int32_t* devices,
+                                            int32_t ndev, wpm_plan_t** out) {
+    *out = nullptr;
+    if (ndev < 1 || !devices) return fail(WPM_EINVAL, "no devices");
+    int rc = wpm_plan_create_orbits(n, p, facet_cap, devices[0], out);
+    if (rc) return rc;
+    rc = wpm_plan_set_devices(*out, devices, ndev);
+    if (rc) {
+        wpm_plan_destroy(*out);
+        *out = nullptr;
+    }
+    return rc;
+}
+
+extern "C" int wpm_plan_device_stats(const wpm_plan_t* P, int32_t cap, double* ms_out, int64_t* nodes_out) {
+    if (!P) return -fail(WPM_EINVAL, "null plan");
+    const int W = (int)P->dev_ms.size();
+    for (int d = 0; d < W && d < cap; ++d) {
+        if (ms_out) ms_out[d] = P->dev_ms[d];
+        if (nodes_out) nodes_out[d] = P->dev_nodes[d];
+    }
+    return W;
+}
+
+// split below the root: depth of the first split (0 = off for single-GPU
+// runs; multi-GPU runs always split, from depth 3 by default)
+extern "C" int wpm_plan_set_split(wpm_plan_t* P, int32_t depth) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (depth < 0 || depth > 255) return fail(WPM_EINVAL, "split depth out of range");
+    P->split_depth = depth;
+    for (auto* q : P->peers) q->split_depth = depth;
+    return WPM_OK;
+}
+
+// ---- the same protocol across processes (one per GPU, torch.distributed):
+// rank 0 splits and broadcasts the frontier; a claim counter in rank 0's HBM
+// is shared through a CUDA IPC handle; every rank runs the claim phase.
+
+extern "C" int wpm_plan_split(wpm_plan_t* P, int32_t depth, int64_t target, int64_t* count) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    CU(cudaSetDevice(P->device));
+    g_alloc_stream = P->stream;
+    P->ran = false;
+    int rc = search_prepare(P, 0, 1);
+    if (rc) return rc;
+    CU(cudaEventRecord(P->ev[4], P->stream));
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        if ((rc = search_reset(P))) return rc;
+        if ((rc = split_rounds(P, depth > 0 ? depth : 3, target > 0 ? target : frontier_target(1)))) return rc;
+        if ((unsigned long long)P->frontier <= P->front_cap) break;
+        P->front_cap = (unsigned long long)P->frontier + (unsigned long long)P->frontier / 4 + 1024;
+    }
+    P->split_kept = true;  // the split's rows / nodes belong to this plan's claim run
+    if (count) *count = P->frontier;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_frontier(const wpm_plan_t* P, const uint32_t** recs, int64_t* count, int32_t* recw) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    if (recs) *recs = P->d_front.p;
+    if (count) *count = P->frontier;
+    if (recw) *recw = P->recw;
+    return WPM_OK;
+}
+
+extern "C" int wpm_plan_load_frontier(wpm_plan_t* P, const uint32_t* recs, int64_t count) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    CU(cudaSetDevice(P->device));
+    g_alloc_stream = P->stream;
+    if (P->d_front.ensure((size_t)std::max<int64_t>(count, 1) * P->recw))
+        return fail(WPM_EINTERNAL, "allocation failed (frontier)");
+    if (count) CU(cudaMemcpyAsync(P->d_front.p, recs, (size_t)count * P->recw * 4, cudaMemcpyDefault, P->stream));
+    CU(cudaStreamSynchronize(P->stream));
+    P->frontier = count;
+    P->split_kept = false;
+    return WPM_OK;
+}
+
+extern "C" int wpm_claim_counter_create(int32_t device, void** counter, uint8_t* ipc_handle) {
+    CU(cudaSetDevice(device));
+    void* p = nullptr;
+    CU(cudaMalloc(&p, 64));
+    CU(cudaMemset(p, 0, 64));
+    if (ipc_handle) {
+        cudaIpcMemHandle_t h;
+        CU(cudaIpcGetMemHandle(&h, p));
+        std::memcpy(ipc_handle, &h, sizeof(h));
+    }
+    *counter = p;
+    return WPM_OK;
+}
+
+extern "C" int wpm_claim_counter_open(int32_t device, const uint8_t* ipc_handle, void** counter) {
+    CU(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handle, sizeof(h));
+    CU(cudaIpcOpenMemHandle(counter, h, cudaIpcMemLazyEnablePeerAccess));
+    return WPM_OK;
+}
+
+extern "C" int wpm_claim_counter_reset(int32_t device, void* counter) {
+    CU(cudaSetDevice(device));
+    CU(cudaMemset(counter, 0, 64));
+    return WPM_OK;
+}
+
+extern "C" int wpm_claim_counter_close(int32_t device, void* counter, int32_t opened) {
+    CU(cudaSetDevice(device));
+    if (opened) CU(cudaIpcCloseMemHandle(counter));
+    else CU(cudaFree(counter));
+    return WPM_OK;
+}
+
+// the claim phase on this plan: pull records of the loaded (or own) frontier
+// through the shared counter; the rank that split keeps the split's rows and
+// nodes.  Sorts this plan's rows canonically (the input of the gather).
+extern "C" int wpm_plan_run_claim(wpm_plan_t* P, void* counter, int64_t* total_out) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    CU(cudaSetDevice(P->device));
+    g_alloc_stream = P->stream;
+    P->ran = false;
+    int rc;
+    if (!P->split_kept) {
+        if ((rc = search_prepare(P, 0, 1))) return rc;
+        CU(cudaEventRecord(P->ev[4], P->stream));
+        if ((rc = search_reset(P))) return rc;
+    }
+    P->claim_count = P->frontier;
+    P->claim_ctr = static_cast<unsigned long long*>(counter);
+    if ((rc = search_main(P, SRC_CLAIM))) return rc;
+    int again = 0;
+    if ((rc = search_finish(P, P->frontier, &again))) return rc;
+    P->split_kept = false;
+    if (again) return fail(WPM_EINTERNAL, "claim phase outgrew its buffers; rerun the job (sizes were raised)");
+    if ((rc = plan_sort(P))) return rc;
+    P->ran = true;
+    if (total_out) *total_out = P->total;
+    return WPM_OK;
+}
+
+// progress (SearchJob::progress, search.hpp:54): fn(done, total, user) from
+// the calling thread while a run is in flight -- root tasks finished of the
+// run's root tasks (or frontier records), monotone, the last call done == total
+extern "C" int wpm_plan_set_progress(wpm_plan_t* P, void (*fn)(int64_t, int64_t, void*), void* user) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    CU(cudaSetDevice(P->device));
+    if (fn && !P->progress_host) {
+        void* h = nullptr;
+        CU(cudaHostAlloc(&h, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+        std::memset(h, 0, 64);
+        void* d = nullptr;
+        CU(cudaHostGetDevicePointer(&d, h, 0));
+        P->progress_host = static_cast<unsigned long long*>(h);
+        P->progress_dev = static_cast<unsigned long long*>(d);
+    }
+    P->progress_fn = fn;
+    P->progress_user = user;
     return WPM_OK;
 }
 
@@ -1052,17 +1668,26 @@ extern "C" int wpm_plan_fetch(wpm_plan_t* P, wpm_result_t** out) {
     R->ms_sort = P->ms_sort;
     R->tasks = P->tasks;
     *out = R;
+    trace_pending("fetch");
     return WPM_OK;
 }
 
 extern "C" void wpm_plan_destroy(wpm_plan_t* P) {
     if (!P) return;
+    trace_pending("destroy (entry)");
+    for (auto* q : P->peers) wpm_plan_destroy(q);
+    P->peers.clear();
     cudaSetDevice(P->device);
+    trace_pending("destroy (peers gone)");
+    if (P->progress_host) cudaFreeHost(P->progress_host);
+    if (P->claim_raw) cudaFree(P->claim_raw);
+    trace_pending("destroy (host / claim memory)");
     DevCtx::Bundle b;
     b.s = P->stream;
     for (int i = 0; i < 5; ++i) b.ev[i] = P->ev[i];
     const int dev = P->device;
     delete P;  // buffers go back to the pool, ordered on the stream
+    trace_pending("destroy (buffers)");
     if (b.s) {
         std::lock_guard<std::mutex> lk(g_dev[dev].mu);
         g_dev[dev].free_bundles.push_back(b);
@@ -1093,10 +1718,13 @@ extern "C" int wpm_enumerate(const wpm_job_t* job, wpm_result_t** out) {
     if (!job) return fail(WPM_EINVAL, "null job");
     const int32_t M = job->num_facets;
     wpm_plan_t* P = nullptr;
+    const int dev0 = job->num_devices > 1 && job->devices ? job->devices[0] : job->device;
     int rc = wpm_plan_create_universes(job->m, job->n, 1, &M, job->facets, job->facet_cap, job->required,
-                                       job->num_required, job->forbidden, job->num_forbidden, job->device, &P);
+                                       job->num_required, job->forbidden, job->num_forbidden, dev0, &P);
     if (rc) return rc;
-    rc = wpm_plan_run(P, job->shard_count > 1 ? job->shard_index : 0, std::max(1, job->shard_count), nullptr);
+    if (job->progress) rc = wpm_plan_set_progress(P, job->progress, job->progress_user);
+    if (!rc && job->num_devices > 1 && job->devices) rc = wpm_plan_set_devices(P, job->devices, job->num_devices);
+    if (!rc) rc = wpm_plan_run(P, job->shard_count > 1 ? job->shard_index : 0, std::max(1, job->shard_count), nullptr);
     if (!rc) rc = wpm_plan_fetch(P, out);
     wpm_plan_destroy(P);
     return rc;

@@ -88,7 +88,8 @@ struct LC {
     static constexpr int FRAMES = TRAIL + a16(2 * MP);     // uint2 per branch frame
     static constexpr int NOPEN = FRAMES + a16(8 * (DMAX + 2));    // uint16 per frame: open ridges at its mark
     static constexpr int SCRATCH = NOPEN + a16(2 * (DMAX + 2));   // closing-ridge list
-    static constexpr int BYTES = SCRATCH + 64;
+    static constexpr int META = SCRATCH + 64;                      // task scalars kept out of registers
+    static constexpr int BYTES = META + 16;
     // CTAs per SM the register budget is cut for: 10 (48 registers, no
     // spills) up to the n = 8 shapes -- measured +1.5 / +5 / +6 % nodes/s
     // at n = 5 / 6 / 8 over 8 CTAs (64 registers) -- and 8 for the larger
@@ -139,6 +140,10 @@ struct WS {
     __device__ __forceinline__ uint2* frames() const { return reinterpret_cast<uint2*>(base + C::FRAMES); }
     __device__ __forceinline__ uint16_t* nopen_at() const { return reinterpret_cast<uint16_t*>(base + C::NOPEN); }
     __device__ __forceinline__ uint16_t* scratch() const { return reinterpret_cast<uint16_t*>(base + C::SCRATCH); }
+    // [0] absolute branch depth of frames[0] (the root's closed frame is
+    // depth 0), [1] root task id of the current task (progress accounting)
+    __device__ __forceinline__ int dbase() const { return reinterpret_cast<const int*>(base + C::META)[0]; }
+    __device__ __forceinline__ uint32_t root() const { return reinterpret_cast<const uint32_t*>(base + C::META)[1]; }
     // shared-window addresses for the PTX helpers
     __device__ __forceinline__ uint32_t a_rs_word(int r) const { return sb + C::RS + (r & ~3); }
     __device__ __forceinline__ uint32_t a_rs(int r) const { return sb + C::RS + r; }
@@ -475,6 +480,34 @@ __device__ __forceinline__ void emit(const WS<C>& w, const MapView& mp, const Se
     }
 }
 
+// the current state as a task record "resume branch frame `ridge` from its
+// first child" (frontier expansion: the frame at the cutoff depth)
+template <class C>
+__device__ __forceinline__ void write_frontier(const WS<C>& w, const MapView& mp, const SearchParams& p, uint32_t ridge,
+                                               int lane) {
+    unsigned long long slot = 0;
+    if (lane == 0) slot = atomicAdd(&p.front_ctl[0], 1ull);
+    slot = __shfl_sync(FULL, slot, 0);
+    if (slot >= p.front_cap) return;  // counted: the host reruns with room
+    uint32_t* rec = p.front_out + slot * (unsigned long long)p.recw;
+    if (lane == 0) {
+        rec[0] = (uint32_t)mp.map | ((ridge == CLOSED_FRAME ? (uint32_t)T_CLOSED : (uint32_t)T_OPEN) << 24);
+        rec[1] = ridge;
+        rec[2] = (uint32_t)(w.dbase() + w.depth) << 16;
+        rec[3] = w.root();
+    }
+    const int mw = (mp.M + 31) >> 5;
+    for (int f0 = 0; f0 < mw * 32; f0 += 32) {
+        const int f = f0 + lane;
+        const uint8_t st = f < mp.M ? w.fst()[f] : (uint8_t)FU;
+        const unsigned bi = __ballot_sync(FULL, st == FIN), bo = __ballot_sync(FULL, st == FOUT);
+        if (lane == 0) {
+            rec[4 + (f0 >> 5)] = bi;
+            rec[4 + p.mw + (f0 >> 5)] = bo;
+        }
+    }
+}
+
 // The descent below a node just entered (after an include, or at a task
 // entry): emit / prune, follow forced moves as a chain of includes, stop at
 // the next real branch point by pushing its frame.  Returns true if a frame
@@ -504,6 +537,10 @@ __device__ __forceinline__ bool descend(WS<C>& w, const MapView& mp, const Searc
                 DEBUG_CHECK(w, mp, lane, 1);
                 continue;
             }
+        }
+        if (p.cutoff && w.dbase() + w.depth >= p.cutoff) {  // split mode: hand the frame on
+            write_frontier(w, mp, p, ridge, lane);
+            return false;
         }
         if (w.depth >= C::kDepth) {
             // frame stack full (the fast layouts hold FRAME_CAP frames): flag the
@@ -642,6 +679,7 @@ __device__ __forceinline__ bool try_donate(WS<C>& w, const MapView& mp, const Se
         unsigned long long t = 0;
         if (lane == 0) {
             atomicAdd(&p.qctl[2], 1ull);  // pending, before publishing
+            if (p.root_pend) atomicAdd(&p.root_pend[w.root()], 1u);
             t = atomicAdd(&p.qctl[0], 1ull << 32) >> 32;
         }
         t = __shfl_sync(FULL, t, 0);
@@ -649,8 +687,8 @@ __device__ __forceinline__ bool try_donate(WS<C>& w, const MapView& mp, const Se
         if (lane == 0) {
             rec[0] = (uint32_t)mp.map | ((ridge == CLOSED_FRAME ? (uint32_t)T_CLOSED : (uint32_t)T_OPEN) << 24);
             rec[1] = ridge;
-            rec[2] = pos;
-            rec[3] = 0;
+            rec[2] = pos | ((uint32_t)(w.dbase() + d) << 16);
+            rec[3] = w.root();
         }
         for (int f0 = 0; f0 < mw * 32; f0 += 32) {
             const int f = f0 + lane;
@@ -698,24 +736,61 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
         // pusher holding push-ticket t publishes it (FIFO hand-off, no CAS
         // retries, no shared spin address).  pending == 0 means no task
         // exists anywhere and no warp can push again: every waiter leaves.
+        // In claim mode a waiter also pulls shared frontier records into the
+        // queue while this GPU runs low (pending < claim_low), and leaves only
+        // once the shared frontier is exhausted too.
+        unsigned long long tk = 0;
+        if (lane == 0) tk = atomicAdd(&p.qctl[0], 1ull) & 0xFFFFFFFFull;
         long long t = -1;
-        if (lane == 0) {
-            const unsigned long long tk = atomicAdd(&p.qctl[0], 1ull) & 0xFFFFFFFFull;
-            volatile unsigned long long* rdy = p.qready + (tk % (unsigned long long)p.qcap);
-            volatile unsigned long long* pend = p.qctl + 2;
-            unsigned backoff = (unsigned)p.backoff_min;
-            for (;;) {
-                if (*rdy == tk + 1ull) {
-                    t = (long long)tk;
-                    break;
+        bool exhausted = p.claim_recs == nullptr;
+        for (;;) {
+            long long claim = -1;
+            if (lane == 0) {
+                volatile unsigned long long* rdy = p.qready + (tk % (unsigned long long)p.qcap);
+                volatile unsigned long long* pend = p.qctl + 2;
+                unsigned backoff = (unsigned)p.backoff_min;
+                for (;;) {
+                    if (*rdy == tk + 1ull) {
+                        t = (long long)tk;
+                        break;
+                    }
+                    if (!exhausted) {
+                        if (atomicAdd(&p.qctl[2], 1ull) < (unsigned long long)p.claim_low) {
+                            const unsigned long long i = atomicAdd_system(p.claim_ctr, 1ull);
+                            if (i < (unsigned long long)p.claim_count) {
+                                claim = (long long)i;  // pending already counts it
+                                break;
+                            }
+                            exhausted = true;
+                        }
+                        atomicAdd(&p.qctl[2], (unsigned long long)-1ll);
+                        if (!exhausted) {
+                            unsigned long long c;
+                            asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(c) : "l"(p.claim_ctr));
+                            exhausted = c >= (unsigned long long)p.claim_count;
+                        }
+                        __threadfence();  // the shared counter before the pending count
+                    }
+                    if (exhausted && (*pend == 0ull || (p.node_budget && ld_relaxed_u64(&p.out_ctl[3])))) {
+                        t = -2;  // no task left anywhere, or the node budget is spent
+                        break;
+                    }
+                    __nanosleep(backoff);
+                    backoff = min(backoff * 2u, (unsigned)p.backoff_max);
                 }
-                if (*pend == 0ull || (p.node_budget && ld_relaxed_u64(&p.out_ctl[3]))) {
-                    t = -2;  // no task left anywhere, or the node budget is spent
-                    break;
-                }
-                __nanosleep(backoff);
-                backoff = min(backoff * 2u, (unsigned)p.backoff_max);
             }
+            claim = __shfl_sync(FULL, claim, 0);
+            if (claim < 0) break;
+            // push the claimed frontier record (root id = its frontier index)
+            unsigned long long pt = 0;
+            if (lane == 0) pt = atomicAdd(&p.qctl[0], 1ull << 32) >> 32;
+            pt = __shfl_sync(FULL, pt, 0);
+            const uint32_t* src = p.claim_recs + (unsigned long long)claim * p.recw;
+            uint32_t* dst = p.qrec + (pt % (unsigned long long)p.qcap) * (unsigned long long)p.recw;
+            for (int i = lane; i < p.recw; i += 32) dst[i] = i == 3 ? (uint32_t)claim : __ldcg(src + i);
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicExch(&p.qready[pt % (unsigned long long)p.qcap], pt + 1ull);
         }
         t = __shfl_sync(FULL, t, 0);
 #ifdef WPM_PROFILE
@@ -739,7 +814,12 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
             if (__shfl_sync(FULL, spent, 0)) break;
         }
         const uint32_t* rec = p.qrec + slot * (unsigned long long)p.recw;
-        const uint32_t h0 = __ldcg(rec), h1 = __ldcg(rec + 1), h2 = __ldcg(rec + 2);
+        const uint32_t h0 = __ldcg(rec), h1 = __ldcg(rec + 1), h2 = __ldcg(rec + 2), h3 = __ldcg(rec + 3);
+        if (lane == 0) {
+            reinterpret_cast<int*>(w.base + C::META)[0] = (int)(h2 >> 16);
+            reinterpret_cast<uint32_t*>(w.base + C::META)[1] = h3;
+        }
+        __syncwarp();
         const int map = (int)(h0 & 0xFFFFu);
         const uint32_t kind = h0 >> 24;
         const MapDesc md = p.maps[map];
@@ -853,7 +933,14 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
             }
         }
         // task finished
-        if (lane == 0) atomicAdd(&p.qctl[2], (unsigned long long)-1ll);
+        if (lane == 0) {
+            if (p.root_pend && atomicSub(&p.root_pend[w.root()], 1u) == 1u) {
+                const unsigned long long d = atomicAdd(p.roots_done, 1ull) + 1ull;
+                if (p.progress_host)  // host takes the max of what it sees
+                    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p.progress_host), "l"(d) : "memory");
+            }
+            atomicAdd(&p.qctl[2], (unsigned long long)-1ll);
+        }
 #ifdef WPM_PROFILE
         {
             const unsigned long long now = clock64();
@@ -884,8 +971,9 @@ __global__ void seed_tasks(SearchParams p, int ntasks, const int32_t* __restrict
     if (lane == 0) {
         rec[0] = (uint32_t)map | ((uint32_t)kind << 24);
         rec[1] = (uint32_t)f;
-        rec[2] = 0;
-        rec[3] = 0;
+        rec[2] = (kind == T_SINGLE ? 1u : 0u) << 16;  // a root task includes a child of the depth-0 frame
+        rec[3] = (uint32_t)t;
+        if (p.root_pend) p.root_pend[t] = 1u;
     }
     for (int i = lane; i < p.mw; i += 32) {
         uint32_t in = 0, out = 0;
@@ -900,6 +988,20 @@ __global__ void seed_tasks(SearchParams p, int ntasks, const int32_t* __restrict
         rec[4 + p.mw + i] = out;
     }
     if (lane == 0) p.qready[t] = (unsigned long long)t + 1ull;
+}
+
+// seed the queue with task records (a frontier): record i -> ticket i, root id i
+__global__ void seed_records(SearchParams p, const uint32_t* __restrict__ recs, long long count) {
+    const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= count) return;
+    const uint32_t* src = recs + (size_t)i * p.recw;
+    uint32_t* dst = p.qrec + (size_t)i * p.recw;
+    for (int k = lane; k < p.recw; k += 32) dst[k] = k == 3 ? (uint32_t)i : src[k];
+    if (lane == 0) {
+        if (p.root_pend) p.root_pend[i] = 1u;
+        p.qready[i] = (unsigned long long)i + 1ull;
+    }
 }
 
 template <class C>
@@ -931,6 +1033,24 @@ int launch_seed_tasks(const SearchParams& p, int ntasks, const int32_t* d_task_m
     if (ntasks <= 0) return 0;
     const int threads = 128, blocks = (ntasks * 32 + threads - 1) / threads;
     seed_tasks<<<blocks, threads, 0, st>>>(p, ntasks, d_task_map, d_task_f, d_task_kind, d_pin_in, d_pin_out);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+__global__ void fill_u32(unsigned int* d, unsigned int v, long long count) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) d[i] = v;
+}
+
+int launch_fill_u32(unsigned int* d, unsigned int v, long long count, cudaStream_t st) {
+    if (count <= 0) return 0;
+    fill_u32<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(d, v, count);
+    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int launch_seed_records(const SearchParams& p, const uint32_t* d_recs, long long count, cudaStream_t st) {
+    if (count <= 0) return 0;
+    const long long threads = count * 32;
+    seed_records<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(p, d_recs, count);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

@@ -45,7 +45,34 @@ struct SearchParams {
     // at every queue check and stop once the total reaches it (out_ctl[3]
     // = 1: the run is truncated -- a throughput stress, not an enumeration)
     unsigned long long node_budget;
+    // frontier expansion (cutoff > 0): a branch frame at absolute depth >=
+    // cutoff is not explored; its state is appended to front_out (a task
+    // record) instead -- the split of the search tree below the root
+    int cutoff;
+    uint32_t* front_out;
+    unsigned long long* front_ctl;   // [0] records written (may exceed front_cap: rerun)
+    unsigned long long front_cap;
+    // claim mode: idle warps pull frontier records claim_recs[i] (a local
+    // copy) by i = atomicAdd on *claim_ctr -- one counter shared by every GPU
+    // of the job (peer or IPC memory, system-scope atomics) -- while fewer
+    // than claim_low tasks are pending on this GPU
+    const uint32_t* claim_recs;
+    long long claim_count;
+    unsigned long long* claim_ctr;
+    int claim_low;
+    // progress (search.hpp:54, :244): root_pend[root] = unfinished tasks of
+    // each root task (header word 3); a finished root bumps roots_done and
+    // publishes it to host-mapped memory (optional)
+    unsigned int* root_pend;
+    unsigned long long* roots_done;
+    unsigned long long* progress_host;
 };
+
+// task record header (queue, frontier): [0] map | kind << 24, [1] facet or
+// ridge, [2] resume position | absolute branch depth << 16, [3] root task id;
+// then the IN and OUT facet bitsets (mw words each)
+int launch_seed_records(const SearchParams& p, const uint32_t* d_recs, long long count, cudaStream_t st);
+int launch_fill_u32(unsigned int* d, unsigned int v, long long count, cudaStream_t st);
 
 // seeds root tasks (map, f) in queue order; required/forbidden lists for ENTRY tasks
 int launch_seed_tasks(const SearchParams& p, int ntasks, const int32_t* d_task_map,

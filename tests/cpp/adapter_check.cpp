@@ -6,8 +6,11 @@
 // on the same reference SearchJob and compares the outputs complex by
 // complex: every orbit map for n = 2..5 (UBT cap), full-subset universes, the
 // test_search.cpp:178-220 link-pinned octahedron basis, random pinned bases
-// from apply_link_constraints, and the candidate_cap error.  Built by
+// from apply_link_constraints, universes in shuffled order, hand-made bases
+// (a block whose WPMs need three generators, the raw kernel basis, a block
+// list with a gap), SearchJob::progress, and the candidate_cap error.  Built by
 // oracle/Makefile (target `ref`) into oracle/_ref/; run by tests/test_gpu_parity.py.
+#include <algorithm>
 #include <cstdio>
 #include <random>
 #include <set>
@@ -86,6 +89,62 @@ int main() {
         if (!pinned) continue;
         job.basis = *pinned;
         check(job, "random pin");
+        ++jobs;
+    }
+    {  // a universe in any order (incidence_matrix indexes by hash, incidence.hpp:34-55)
+        std::mt19937 sh(11);
+        for (int n = 3; n <= 5; ++n) {
+            auto u = matroid_universe(idcm_orbits(n, 4)[1]);
+            std::shuffle(u.begin(), u.end(), sh);
+            auto job = make_job(u, n + 4, n);
+            job.properties = {ubt_property(n, static_cast<int>(u.size()))};
+            check(job, "unsorted universe");
+            ++jobs;
+        }
+    }
+    {  // hand-made bases: the adapter must return exactly what the reference reaches
+        auto u = matroid_universe(idcm_orbits(5, 4)[2]);
+        auto job = make_job(u, 9, 5);
+        job.properties = {ubt_property(5, static_cast<int>(u.size()))};
+        int b3 = -1;
+        for (std::size_t b = 0; b < job.basis.blocks.size() && b3 < 0; ++b)
+            if (job.basis.blocks[b].width >= 3) b3 = static_cast<int>(b);
+        if (b3 >= 0) {  // g2 += g0 + g1 inside one block: a WPM g2 now needs 3 block generators
+            const int off = job.basis.blocks[static_cast<std::size_t>(b3)].offset;
+            job.basis.gens[static_cast<std::size_t>(off + 2)] ^= job.basis.gens[static_cast<std::size_t>(off)];
+            job.basis.gens[static_cast<std::size_t>(off + 2)] ^= job.basis.gens[static_cast<std::size_t>(off + 1)];
+            check(job, "block-mixed basis");
+            ++jobs;
+        } else {
+            std::printf("MISMATCH no block of width >= 3 for the mixed-basis case\n");
+            ++failures;
+        }
+        auto raw = job;  // the raw kernel basis: every generator a free singleton, the full span
+        raw.basis = KernelBasis{};
+        raw.basis.M = static_cast<int>(u.size());
+        raw.basis.gens = kernel_basis(incidence_matrix(u));
+        check(raw, "raw kernel basis");
+        ++jobs;
+        auto sub = job;  // a truncated block list: the skipped generators are never used
+        if (sub.basis.blocks.size() > 1) {
+            sub.basis.blocks.erase(sub.basis.blocks.begin());
+            check(sub, "block list without its first block");
+            ++jobs;
+        }
+    }
+    {  // SearchJob::progress (search.hpp:54): called, monotone, ends at done == total
+        auto u = matroid_universe(idcm_orbits(6, 4)[0]);
+        auto job = make_job(u, 10, 6);
+        job.properties = {ubt_property(6, static_cast<int>(u.size()))};
+        std::vector<std::pair<long long, long long>> calls;
+        job.progress = [&](long long d, long long t) { calls.emplace_back(d, t); };
+        const auto got = b200::enumerate_wpm(job);
+        bool ok = !calls.empty() && calls.back().first == calls.back().second && !got.empty();
+        for (std::size_t i = 1; i < calls.size(); ++i) ok &= calls[i - 1].first <= calls[i].first;
+        if (!ok) {
+            std::printf("MISMATCH progress: %zu calls\n", calls.size());
+            ++failures;
+        }
         ++jobs;
     }
     {  // candidate_cap: same exception type

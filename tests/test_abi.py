@@ -133,8 +133,8 @@ def test_job_validation_errors(wpm):
     incidence.hpp:35) is checked on the host before any device work."""
     with pytest.raises(wpm.PurityError):
         wpm.enumerate_wpm(wpm.SearchJob(4, 2, []))
-    with pytest.raises(ValueError):
-        wpm.enumerate_wpm(wpm.SearchJob(4, 2, [0b1100, 0b0110]))  # not canonical order
+    with pytest.raises(ValueError, match="duplicate"):
+        wpm.enumerate_wpm(wpm.SearchJob(4, 2, [0b1100, 0b0110, 0b1100]))  # PureComplex::validate, complex.hpp:50-51
     with pytest.raises(ValueError):
         wpm.enumerate_wpm(wpm.SearchJob(4, 2, [0b0110], properties=[wpm.AffineProperty([2], 3)]))
 
