@@ -21,9 +21,14 @@ the driver's ratio is the wall-time ratio.  The reference's own search size
   cpu_baseline : the reference compiled from its own headers (oracle/_ref),
           nproc threads, the same workload
 
-Multi-GPU (torchrun): root tasks are sharded t % world == rank (weak split of
-one fixed workload = strong scaling); NCCL only for the final counts and the
-result gather to rank 0.
+Multi-GPU (torchrun, one process per GPU): the library's shared-frontier
+protocol (paper_2301_00806_b200/dist.py): rank 0 splits the search tree below
+the root, the frontier records go to every rank (NCCL broadcast), every GPU's
+kernel 3 claims records through one counter in rank 0's HBM (CUDA IPC, peer
+atomics) -- one fixed workload split dynamically = strong scaling -- and the
+rows are gathered to rank 0 (send/recv) and sorted there once.  On one GPU the
+line carries a scaling PROJECTION from measured per-record node counts
+(`scaling_projection`).
 """
 from __future__ import annotations
 
@@ -88,9 +93,30 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def workload_config(n, maps):
+    """The `config` of both arms (identical dicts: the driver compares them)."""
+    return {"workload": f"Picard 4, n={n} (m={n + 4}): all {maps} characteristic maps, UBT cap "
+                        "(BASELINE configs[1])" if n == 5 else f"Picard 4, n={n} (m={n + 4}): all {maps} "
+                        "characteristic maps, UBT cap",
+            "n": n, "m": n + 4, "maps": maps, "facet_cap": "ubt (cyclic_facet_bound)",
+            "output": "every WPM of every map, canonical order (search.hpp:247-257)"}
+
+
+def _ref_run(ref, n, threads, maps=None, timeout=900):
+    cmd = [ref, "enumerate", str(n), "--threads", str(threads)]
+    if maps:
+        cmd += ["--maps", maps]
+    t0 = time.perf_counter()
+    out = subprocess.run(cmd, check=True, capture_output=True, text=True, timeout=timeout).stdout
+    wall = time.perf_counter() - t0
+    tot = [ln for ln in out.splitlines() if ln.startswith("total")][0].split()
+    return {"wall_s": wall, "wpms": int(tot[2]), "leaves": int(tot[4]), "prep_s": float(tot[6]),
+            "enum_s": float(tot[8])}
+
+
 def reference_arm(args):
     """`--impl reference`: the reference's own CPU path (oracle/_ref, built
-    from the unmodified headers), nproc threads, same workload and unit."""
+    from the unmodified headers), all host threads, same workload and unit."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -102,45 +128,32 @@ def reference_arm(args):
     if not os.path.exists(ref):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/plseeds_ref not built"}))
         return 0
-
-    def one():
-        t0 = time.perf_counter()
-        out = subprocess.run([ref, "enumerate", str(n), "--threads", str(threads)], check=True,
-                             capture_output=True, text=True).stdout
-        wall = time.perf_counter() - t0
-        tot = [ln for ln in out.splitlines() if ln.startswith("total")][0].split()
-        return wall, int(tot[2]), int(tot[4]), float(tot[6]), float(tot[8])
-
     for _ in range(args.warmup):
-        one()
-    walls, leaves = [], 0
-    wpms = 0
-    for _ in range(args.steps):
-        wall, wpms, leaves, prep, enum = one()
-        walls.append(wall)
-    t = sum(walls) / len(walls)
+        _ref_run(ref, n, threads)
+    runs = [_ref_run(ref, n, threads) for _ in range(args.steps)]
+    t = sum(r["wall_s"] for r in runs) / len(runs)
     value = nodes / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64 (GF(2) bitsets)", "data": "synthetic (IDCM orbit maps, deterministic)",
-        "config": {"workload": f"Picard 4, n={n} (m={n + 4}): all {len(g['orbits'][str(n)])} characteristic maps, "
-                               "UBT cap", "n": n, "maps": len(g["orbits"][str(n)]), "wpms": wpms,
-                   "reference_leaves": leaves, "threads": threads},
+        "config": workload_config(n, len(g["orbits"][str(n)])),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"full n={n} enumeration (all maps), {args.steps} steps"},
+                         "sample": f"full n={n} enumeration (all maps, reference enumerate_wpm, {threads} threads), "
+                                   f"{args.steps} steps"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "reference_leaves_per_s": leaves / t, "wall_s": t,
+        "reference": {"wpms": runs[-1]["wpms"], "leaves": runs[-1]["leaves"], "threads": threads,
+                      "leaves_per_s": runs[-1]["leaves"] / t, "wall_s": t},
     }
     print(json.dumps(line))
     return 0
 
 
 METRIC = "search nodes/sec and wall time to enumerate all WPMs per Picard-4 dim n"
-# per step at n = 5, from the ncu launch list of this command
-# (profiles/r01_bench_n5_launches.txt): seed_tasks + k3_search + CUB merge sort
-# of the key rows (1 block sort + 9 partition/merge pairs) + split_rows
-LAUNCHES_PER_STEP = 22
+# per step at n = 5 (1 GPU), from the ncu launch list of this command
+# (profiles/r02_bench_n5_launches.txt): seed_tasks + k3_search + k4_sort (one
+# cooperative launch: tile sort, merge passes, split)
+LAUNCHES_PER_STEP = 3
 
 
 def _profile_summary(n):
@@ -170,18 +183,41 @@ UNIT = "search nodes/s (DFS facet-inclusion steps of the workload / wall s)"
 
 
 def cpu_baseline(n, nodes):
+    """The reference on this host, same run: nproc threads and 1 thread on the
+    full n workload, plus the reference's leaves/s at n = 6 (all maps) and
+    n = 7 (map 0) for the labelled n = 8..11 projections."""
+    import psutil
+
     ref = os.path.join(ROOT, "oracle", "_ref", "plseeds_ref")
     threads = os.cpu_count() or 1
     if not os.path.exists(ref):
         return None
-    t0 = time.perf_counter()
-    out = subprocess.run([ref, "enumerate", str(n), "--threads", str(threads)], check=True, capture_output=True,
-                         text=True, timeout=600).stdout
-    wall = time.perf_counter() - t0
-    tot = [ln for ln in out.splitlines() if ln.startswith("total")][0].split()
-    return {"value": nodes / wall, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"one full n={n} enumeration, all maps (reference enumerate_wpm, {threads} threads)",
-            "wall_s": wall, "reference_leaves": int(tot[4]), "wpms": int(tot[2])}
+    full = _ref_run(ref, n, threads, timeout=600)
+    one = _ref_run(ref, n, 1, timeout=600)
+    g = _golden()
+    rate = {}
+    for nn, maps in ((6, None), (7, "0:1")):
+        r = _ref_run(ref, nn, threads, maps, timeout=600)
+        rate[nn] = {"leaves": r["leaves"], "enum_s": r["enum_s"], "leaves_per_s": r["leaves"] / r["enum_s"],
+                    "maps": maps or "all"}
+    lps = rate[7]["leaves_per_s"]
+    proj = {}
+    for nn in range(8, 12):
+        leaves = g.get("leaves", {}).get(str(nn))
+        if leaves:
+            proj[str(nn)] = {"leaves": leaves, "projected_s": leaves / lps,
+                             "projected_days": leaves / lps / 86400.0}
+    return {"value": nodes / full["wall_s"], "unit": UNIT, "cores": threads, "kind": "reference",
+            "physical_cores": psutil.cpu_count(logical=False),
+            "sample": f"one full n={n} enumeration, all maps (reference enumerate_wpm, {threads} threads); "
+                      f"also 1 thread, n=6 all maps and n=7 map 0 for the projections",
+            "wall_s": full["wall_s"], "reference_leaves": full["leaves"], "wpms": full["wpms"],
+            "one_thread": {"wall_s": one["wall_s"], "value": nodes / one["wall_s"], "cores": 1},
+            "leaves_per_s_by_n": rate,
+            "projection": {"note": f"PROJECTION, not a run: combination-space leaves (search.hpp:62-104) / the "
+                                   f"reference's measured leaves/s at n=7 on {threads} threads ({lps:.3g}/s); the "
+                                   "per-leaf cost grows with the word count, so these are lower bounds",
+                           "by_n": proj}}
 
 
 def main():
@@ -193,13 +229,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-n", dest="per_n", action="store_false",
-                    help="skip the n = 2..11 sweep (1 GPU only)")
+                    help="skip the n = 2..11 sweep, the synthetic band and the scaling projection (1 GPU only)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
     args.warmup = max(args.warmup, 3)
 
-    import numpy as np
     import torch
 
     import paper_2301_00806_b200 as wpm
@@ -222,8 +257,23 @@ def main():
 
     plan = wpm.Plan.orbits(n, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")  # > 126 MB L2
+    counter = None
+    if world > 1:
+        from paper_2301_00806_b200 import dist as wdist
+
+        counter = wdist.share_claim_counter(dist, rank, dev)
+
+    def step():
+        """one full enumeration of the workload: 1 GPU = kernel 3 + the sort;
+        N GPUs = split, frontier broadcast, shared claims, gather + sort on rank 0"""
+        if world == 1:
+            plan.run()
+            return
+        wdist.run_job(dist, plan, rank, world, dev, counter)
+        wdist.gather_to_rank0_device(dist, plan, rank, dev)
+
     for _ in range(args.warmup):
-        plan.run(rank, world)
+        step()
 
     def barrier():
         if dist:
@@ -235,13 +285,23 @@ def main():
     sampler.start()
     ms_total = ms_search = ms_sort = 0.0
     nodes = 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_host = time.perf_counter()
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between timed iterations (outside the device-timed window)
         torch.cuda.synchronize(dev)
-        plan.run(rank, world)
+        if world == 1:
+            step()
+            ms_total += plan.timing()["ms_total"]  # plan-stream CUDA events: first to last op of the run
+        else:
+            # every library call blocks on its own stream, so the events on
+            # torch's stream bracket the whole step (NCCL included)
+            ev0.record()
+            step()
+            ev1.record()
+            torch.cuda.synchronize(dev)
+            ms_total += ev0.elapsed_time(ev1)
         st = plan.stats()
-        ms_total += plan.timing()["ms_total"]
         ms_search += st["ms_search"]
         ms_sort += st["ms_sort"]
         nodes = st["nodes"]
@@ -253,24 +313,24 @@ def main():
     tot_nodes = nodes
     ms_step = ms_total / args.steps
     if dist:
-        t = torch.tensor([float(nodes), ms_step, float(res.total)], dtype=torch.float64, device=f"cuda:{dev}")
-        mx = t.clone()
+        t = torch.tensor([float(nodes), float(res.total)], dtype=torch.float64, device=f"cuda:{dev}")
+        mx = torch.tensor([ms_step], dtype=torch.float64, device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         tot_nodes = int(t[0].item())
-        ms_step = mx[1].item()
-        tot_wpms = int(t[2].item())
+        ms_step = mx[0].item()
+        tot_wpms = int(t[1].item())
     else:
         tot_wpms = res.total
     value = tot_nodes / (ms_step * 1e-3)
 
-    # e2e: the reference-facing one-shot C-ABI call, host buffers, all copies inside
+    # e2e: the reference-facing call, host buffers, all copies inside
     e2e_times = []
     h2d = d2h = 0
     for i in range(max(2, min(args.steps, 10)) + 1):
         barrier()
         t0 = time.perf_counter()
-        r = wpm_orbits_oneshot(wpm, n, dev, rank, world)
+        r = wpm_orbits_oneshot(wpm, n, dev, rank, world, counter)
         dt = time.perf_counter() - t0
         if i > 0:  # first call pays context/module load
             e2e_times.append(dt)
@@ -281,12 +341,12 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = t.item()
     e2e_value = tot_nodes / e2e_s
+    dropin = e2e_dropin(n, dev) if world == 1 else None
 
     # roofline of kernel 3 vs measured INT32 issue peak
     peak = wpm.int_peak(dev)
-    ops = tot_nodes / max(world, 1) * 5 * n if world > 1 else nodes * 5 * n
     ms_k3 = ms_search / args.steps
-    achieved = ops / (ms_k3 * 1e-3)
+    achieved = nodes * 5 * n / (ms_k3 * 1e-3)
     prof = _profile_summary(n)
     roofline = {"bound": "int-issue", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
                 "frac": achieved / peak, "traffic": prof.get("traffic"),
@@ -297,15 +357,16 @@ def main():
                           "issue_active_pct": prof.get("issue_pct"),
                           "warp_inst_peak_per_s": 4 * 148 * 1.965e9,
                           "note": "the kernel is issue-bound: one DFS per warp has O(n) lanes of work per node; "
-                                  "see profiles/r01_k3_n5_ncu.txt"}}
+                                  "see profiles/ (k3 ncu summaries)"}}
 
     num_maps = plan.num_maps
-    per_n = None
+    per_n = synthetic = scaling = None
     if world == 1 and args.per_n:
         plan.close()
+        plan = None
         per_n = sweep_per_n(wpm, dev, flush, g)
         synthetic = sweep_synthetic(wpm, dev, flush, g)
-        plan = None
+        scaling = scaling_projection(wpm, dev, flush)
 
     if rank == 0:
         cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(n, expect_nodes)
@@ -314,18 +375,21 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64 (GF(2) bitsets)",
             "data": "synthetic (IDCM orbit maps, deterministic; no dataset)",
-            "config": {"workload": f"Picard 4, n={n} (m={n + 4}): all {num_maps} characteristic maps, UBT cap "
-                                   "(BASELINE configs[1])", "n": n, "maps": num_maps, "wpms": tot_wpms,
-                       "dfs_nodes": tot_nodes, "l2": "flushed (256 MB write) between timed steps",
-                       "parallelism": f"root-task shards x{world}"},
+            "config": workload_config(n, num_maps),
+            "run": {"wpms": tot_wpms, "dfs_nodes": tot_nodes, "l2": "flushed (256 MB write) between timed steps",
+                    "parallelism": "1 GPU: persistent kernel 3, in-GPU work queue" if world == 1 else
+                    f"{world} GPUs: split below the root + shared-frontier claims (dist.run_job)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                    "wall_ms": e2e_s * 1e3, "min_ms": min(e2e_times) * 1e3, "samples_ms": [round(t * 1e3, 3) for t in e2e_times],
-                    "call": "wpm_enumerate_orbits (one-shot C-ABI)"},
+                    "wall_ms": e2e_s * 1e3, "min_ms": min(e2e_times) * 1e3,
+                    "samples_ms": [round(t * 1e3, 3) for t in e2e_times],
+                    "call": "wpm_enumerate_orbits (one-shot C-ABI)" if world == 1 else
+                            "Plan.orbits + dist.run_job + gather to rank 0 + D2H"},
+            "e2e_dropin": dropin,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clocks,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
-            "gpu_launches_per_step": {"seed_tasks": 1, "k3_search": 1, "cub_merge_sort": 19, "split_rows": 1},
+            "gpu_launches_per_step": {"seed_tasks": 1, "k3_search": 1, "k4_sort": 1},
             "breakdown_ms": {"search": ms_k3, "sort": ms_sort / args.steps, "step": ms_step},
             "parity": {"wpms_expected": expect_wpms, "nodes_expected": expect_nodes,
                        "ok": tot_wpms == expect_wpms and tot_nodes == expect_nodes},
@@ -334,6 +398,7 @@ def main():
         if per_n is not None:
             line["per_n"] = per_n
             line["synthetic"] = synthetic
+            line["scaling_projection"] = scaling
             row = next((r for r in per_n if r["n"] == n), None)
             if row and row.get("alg1"):
                 # the same algorithm on both sides: the reference's leaves per
@@ -350,6 +415,9 @@ def main():
     if plan is not None:
         plan.close()
     if dist:
+        if counter is not None:
+            dist.barrier()
+            wpm.claim_counter_close(dev, counter[0], counter[1])
         dist.destroy_process_group()
     return 0
 
@@ -484,11 +552,11 @@ class _E2E:
         self.h2d_bytes, self.d2h_bytes, self.total = h2d, d2h, total
 
 
-def wpm_orbits_oneshot(wpm, n, dev, rank, world):
+def wpm_orbits_oneshot(wpm, n, dev, rank, world, counter=None):
     """wpm_enumerate_orbits for world == 1.  For world > 1: every rank builds
-    its plan from the host maps, searches its root-task shard, NCCL gathers
-    the canonical rows into rank 0's HBM, rank 0 sorts them canonically and
-    copies the full list to the host."""
+    its plan from the host maps, the ranks run the shared-frontier job
+    (dist.run_job), the canonical rows go to rank 0 (send/recv), rank 0 sorts
+    them and copies the full list to the host."""
     if world == 1:
         return wpm.enumerate_orbits(n, device=dev)
     import torch
@@ -497,7 +565,7 @@ def wpm_orbits_oneshot(wpm, n, dev, rank, world):
     from paper_2301_00806_b200 import dist as wdist
 
     with wpm.Plan.orbits(n, device=dev) as p:
-        p.run(rank, world)
+        wdist.run_job(dist, p, rank, world, dev, counter)
         total, dups, rows, maps = wdist.gather_to_rank0_device(dist, p, rank, dev, return_rows=True)
         d2h = 0
         if rank == 0:
@@ -506,6 +574,90 @@ def wpm_orbits_oneshot(wpm, n, dev, rank, world):
             host.copy_(rows)
             d2h = host.numel() * host.element_size()
     return _E2E(0, d2h, total)
+
+
+def e2e_dropin(n, dev):
+    """The drop-in's own return type, timed: tools/dropin_e2e (C++,
+    include/plseeds_b200.hpp) runs the Algorithm-2 per-orbit loop
+    (pipeline.hpp:58-72) through plseeds_b200::enumerate_orbits and builds
+    every std::vector<PureComplex> -- the reference arm's output objects."""
+    exe = os.path.join(ROOT, "build", "dropin_e2e")
+    if not os.path.exists(exe):
+        return None
+    out = subprocess.run([exe, str(n), str(dev), "7"], capture_output=True, text=True, timeout=300)
+    if out.returncode != 0:
+        return {"error": out.stderr[-300:]}
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)), max_w=8):
+    """1-GPU PROJECTION of the multi-GPU job (labelled as such; the driver's
+    SCALE run measures the real thing).  The job as max_w GPUs would run it:
+    split below the root until >= 2048 records per GPU, then the claim phase
+    over the frontier with per-record node accounting.  From the measured
+    per-record nodes, for W = 1, 2, 4, 8: the static strided split's max/mean
+    and a list schedule of the records in claim order over W GPUs (the
+    shared counter hands each record to the first free GPU) at the measured
+    single-GPU rate; projected T_W = t_split + makespan_W / rate."""
+    import heapq
+    import sys as _sys
+
+    import numpy as np
+    import torch
+
+    _sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import catalog as C
+
+    out = []
+    for n, d in cases:
+        if d is None:
+            mk = lambda: wpm.Plan.orbits(n, device=dev)  # noqa: E731
+            name = f"n={n}, all maps"
+        else:
+            u = C.synthetic_universe(1, d)
+            mk = lambda: wpm.Plan.universes(15, 11, [u], facet_cap=252, device=dev)  # noqa: E731
+            name = f"synthetic (15, 11) d={d} seed 1"
+        with mk() as p:
+            p.run()
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            p.run()
+            t_one = p.timing()["ms_total"]
+            p.set_root_stats(True)
+            ctr, _ = wpm.claim_counter_create(dev)
+            try:
+                t0 = time.perf_counter()
+                F = p.split(3, 2048 * max_w)
+                t_split = (time.perf_counter() - t0) * 1e3
+                p.run_claim(ctr)
+            finally:
+                wpm.claim_counter_close(dev, ctr, False)
+            st = p.stats()
+            per, split_nodes = p.root_nodes()
+        per = per.astype(np.float64)
+        tot = per.sum()
+        t_main = max(st["ms_search"] - t_split, 1e-3)
+        rate = tot / t_main  # nodes per ms, claim phase
+        rows = []
+        for W in (1, 2, 4, 8):
+            loads = np.zeros(W)
+            for i, x in enumerate(per):
+                loads[i % W] += x
+            h = [(0.0, i) for i in range(W)]
+            for x in per:
+                t, i = heapq.heappop(h)
+                heapq.heappush(h, (t + x, i))
+            mk_nodes = max(t for t, _ in h)
+            t_w = t_split + mk_nodes / rate
+            rows.append({"W": W, "static_max_over_mean": float(loads.max() / loads.mean()),
+                         "dynamic_makespan_over_mean": float(mk_nodes / (tot / W)),
+                         "projected_ms": round(t_w, 3), "projected_speedup": round((t_split + t_main) / t_w, 3)})
+        out.append({"case": name, "frontier_records": int(F), "split_ms_host": round(t_split, 3),
+                    "claim_ms": round(t_main, 3), "one_gpu_run_ms": round(t_one, 3),
+                    "split_nodes": int(split_nodes), "claim_nodes": int(tot),
+                    "largest_record_frac": float(per.max() / tot) if tot else None, "by_W": rows})
+    return {"note": "PROJECTION from measured per-frontier-record node counts on 1 B200 (not a multi-GPU run); "
+                    "excludes the NCCL frontier broadcast and the rank-0 gather", "cases": out}
 
 
 if __name__ == "__main__":

@@ -39,6 +39,7 @@
 #include <ostream>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "wpm_b200.h"
@@ -184,19 +185,24 @@ inline std::vector<VertexSet> universe_of(wpm_plan_t* p, int map) {
     return out;
 }
 
+// rows of map `map` -> PureComplex (search.hpp:247-253): facets in
+// ascending order, each vector sized once
 inline std::vector<PureComplex> complexes_of(const wpm_result_t* r, int map, int m, int n,
                                              const std::vector<VertexSet>& u) {
-    std::vector<PureComplex> out;
-    out.reserve(static_cast<std::size_t>(r->counts[map]));
-    for (std::int64_t i = r->offsets[map]; i < r->offsets[map + 1]; ++i) {
-        PureComplex K;
+    std::vector<PureComplex> out(static_cast<std::size_t>(r->counts[map]));
+    const int W = r->words;
+    const std::uint64_t* row = r->bits + static_cast<std::size_t>(r->offsets[map]) * W;
+    for (auto& K : out) {
         K.m = m;
         K.n = n;
         K.embedded = true;
-        const std::uint64_t* row = r->bits + static_cast<std::size_t>(i) * r->words;
-        for (int w = 0; w < r->words; ++w)
-            for (std::uint64_t x = row[w]; x; x &= x - 1) K.facets.push_back(u[static_cast<std::size_t>(w * 64 + __builtin_ctzll(x))]);
-        out.push_back(std::move(K));
+        int k = 0;
+        for (int w = 0; w < W; ++w) k += __builtin_popcountll(row[w]);
+        K.facets.resize(static_cast<std::size_t>(k));
+        VertexSet* f = K.facets.data();
+        for (int w = 0; w < W; ++w)
+            for (std::uint64_t x = row[w]; x; x &= x - 1) *f++ = u[static_cast<std::size_t>(w * 64 + __builtin_ctzll(x))];
+        row += W;
     }
     return out;
 }
@@ -274,9 +280,19 @@ inline std::vector<std::vector<PureComplex>> enumerate_orbits(int n, int p = 4, 
     check(wpm_plan_run(P.p, 0, 1, &total));
     detail::Result R;
     check(wpm_plan_fetch(P.p, &R.r));
-    std::vector<std::vector<PureComplex>> out;
-    for (int i = 0; i < R.r->num_maps; ++i)
-        out.push_back(detail::complexes_of(R.r, i, n + p, n, detail::universe_of(P.p, i)));
+    const int K = R.r->num_maps;
+    std::vector<std::vector<VertexSet>> uni(static_cast<std::size_t>(K));
+    for (int i = 0; i < K; ++i) uni[static_cast<std::size_t>(i)] = detail::universe_of(P.p, i);
+    // the reference's return objects, built in parallel over the maps
+    std::vector<std::vector<PureComplex>> out(static_cast<std::size_t>(K));
+    const int T = std::max(1, std::min<int>(K, static_cast<int>(std::thread::hardware_concurrency())));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t)
+        pool.emplace_back([&, t]() {
+            for (int i = t; i < K; i += T)
+                out[static_cast<std::size_t>(i)] = detail::complexes_of(R.r, i, n + p, n, uni[static_cast<std::size_t>(i)]);
+        });
+    for (auto& th : pool) th.join();
     return out;
 }
 

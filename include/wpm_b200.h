@@ -195,7 +195,7 @@ int wpm_plan_device_result(const wpm_plan_t *plan, const uint32_t **bits32, cons
  * parallel_for_index, parallel.hpp:27-54, becomes GPUs): devices[0] must be
  * the plan's device; the others get plans of the same maps.  wpm_plan_run
  * then splits the search tree below the root on devices[0] (split rounds
- * until the frontier has >= 512 records per GPU), copies the frontier to
+ * until the frontier has >= 2048 records per GPU), copies the frontier to
  * every GPU, and each GPU's kernel 3 pulls records through one claim counter
  * in devices[0]'s HBM (peer atomics over NVLink) and shares them further by
  * donation; the rows are gathered into devices[0] (peer copies) and sorted
@@ -208,6 +208,12 @@ int wpm_plan_device_stats(const wpm_plan_t *plan, int32_t cap, double *ms_out, i
 /* split below the root before the search: first split depth (branch frames;
  * 0 = off for single-GPU runs, multi-GPU runs default to 3) */
 int wpm_plan_set_split(wpm_plan_t *plan, int32_t depth);
+/* per-root search nodes of the following runs (root tasks, or frontier
+ * records after a split): wpm_plan_root_nodes returns the root count, writes
+ * at most cap counts and the split phase's own nodes (*split_nodes) -- the
+ * measured input of the multi-GPU scaling projection */
+int wpm_plan_set_root_stats(wpm_plan_t *plan, int32_t on);
+int64_t wpm_plan_root_nodes(wpm_plan_t *plan, int64_t *out, int64_t cap, int64_t *split_nodes);
 /* progress callback of the following runs (see wpm_job_t.progress); NULL = off */
 int wpm_plan_set_progress(wpm_plan_t *plan, void (*fn)(int64_t done, int64_t total, void *user), void *user);
 /* The same protocol across processes (one per GPU): rank 0 calls

@@ -217,6 +217,8 @@ _SIGS = {
     "wpm_claim_counter_reset": (ctypes.c_int, [_i32, ctypes.c_void_p]),
     "wpm_claim_counter_close": (ctypes.c_int, [_i32, ctypes.c_void_p, _i32]),
     "wpm_plan_run_claim": (ctypes.c_int, [_PlanP, ctypes.c_void_p, ctypes.POINTER(_i64)]),
+    "wpm_plan_set_root_stats": (ctypes.c_int, [_PlanP, _i32]),
+    "wpm_plan_root_nodes": (_i64, [_PlanP, ctypes.POINTER(_i64), _i64, ctypes.POINTER(_i64)]),
     "wpm_plan_run_kernel_basis_prefix": (ctypes.c_int, [_PlanP, _i32, _i32, _i32p, ctypes.c_uint64,
                                                         ctypes.POINTER(_i64)]),
     "wpm_plan_space_blocks": (_i32, [_PlanP, _i32, _i32p, _i32]),
@@ -414,6 +416,19 @@ class Plan:
         nd = (_i64 * 64)()
         k = int(_lib.wpm_plan_device_stats(self._h, 64, ms, nd))
         return [(ms[i], int(nd[i])) for i in range(max(k, 0))]
+
+    def set_root_stats(self, on: bool = True) -> None:
+        _check(_lib.wpm_plan_set_root_stats(self._h, 1 if on else 0))
+
+    def root_nodes(self):
+        """(per-root node counts of the last run's main phase, split-phase nodes)."""
+        sp = _i64()
+        k = int(_lib.wpm_plan_root_nodes(self._h, None, 0, ctypes.byref(sp)))
+        if k < 0:
+            _check(-k)
+        out = np.zeros(max(k, 1), dtype=np.int64)
+        _lib.wpm_plan_root_nodes(self._h, out.ctypes.data_as(ctypes.POINTER(_i64)), k, ctypes.byref(sp))
+        return out[:k], int(sp.value)
 
     # -- the cross-process protocol (one process per GPU, see dist.py)
     def split(self, depth: int = 3, target: int = 0) -> int:

@@ -256,6 +256,10 @@ struct wpm_plan {
     std::function<int(int, wpm_plan_t**)> recreate;  // the same plan on another device
     DevBuf<uint32_t> d_front2, d_gather;
     bool split_kept = false;  // wpm_plan_split ran: the claim run appends to its rows
+    bool root_stats = false;  // count search nodes per root task / frontier record
+    std::vector<uint32_t> h_facets;  // host copy of every universe (wpm_plan_universe)
+    DevBuf<unsigned long long> d_root_nodes;
+    long long root_count = 0;
     int ntasks = 0, frame_cap = 64;
     bool full_depth = false;
 };
@@ -579,7 +583,7 @@ static int plan_build_tables(wpm_plan* P, const std::vector<uint32_t>& foff) {
     CU(cudaMemcpyAsync(P->d_maps.p, P->desc.data(), K * sizeof(MapDesc), cudaMemcpyHostToDevice, P->stream));
     P->mw = (P->maxM + 31) / 32;
     P->w32 = 2 * ((P->maxM + 63) / 64);
-    P->rw = key_words_for(P->w32) + 1;
+    P->rw = rec_words(P->w32);
     P->recw = 4 + 2 * P->mw;
     CU(cudaStreamSynchronize(P->stream));
     return WPM_OK;
@@ -754,12 +758,18 @@ extern "C" int wpm_plan_num_maps(const wpm_plan_t* P) { return P ? P->num_maps :
 
 extern "C" int32_t wpm_plan_universe(wpm_plan_t* P, int32_t map, uint64_t* out, int32_t cap) {
     if (!P || map < 0 || map >= P->num_maps) return -fail(WPM_EINVAL, "bad map index");
-    cudaSetDevice(P->device);
+    if (P->h_facets.empty()) {  // every map's universe in one copy, kept on the host
+        cudaSetDevice(P->device);
+        const MapDesc& last = P->desc[P->num_maps - 1];
+        P->h_facets.resize((size_t)last.facet_off + (size_t)last.M);
+        if (cudaMemcpy(P->h_facets.data(), P->d_facets.p, P->h_facets.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            P->h_facets.clear();
+            return -fail(WPM_EINTERNAL, "copy failed");
+        }
+        P->d2h += (long long)P->h_facets.size() * 4;
+    }
     const int M = P->M[map];
-    std::vector<uint32_t> h(M);
-    if (cudaMemcpy(h.data(), P->d_facets.p + P->desc[map].facet_off, M * sizeof(uint32_t), cudaMemcpyDeviceToHost) !=
-        cudaSuccess)
-        return -fail(WPM_EINTERNAL, "copy failed");
+    const uint32_t* h = P->h_facets.data() + P->desc[map].facet_off;
     for (int j = 0; j < M && j < cap; ++j) out[j] = h[j];
     return M;
 }
@@ -887,10 +897,18 @@ static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
     if (const char* e = std::getenv("WPM_CHECK_EVERY")) sp.check_every = std::max(1, std::atoi(e));
     sp.donate_max = 1;
     if (const char* e = std::getenv("WPM_DONATE_MAX")) sp.donate_max = std::max(1, std::atoi(e));
-    // claims: keep about a quarter of the warps' worth of tasks pending;
-    // donation spreads each claimed record over the GPU
-    sp.claim_low = std::max(8, est_warps / 8);
+    // claims: while fewer tasks than warps are pending on this GPU, waiting
+    // warps pull records (measured at 1 GPU: a quarter of the warps starved
+    // the claim phase 2-5x; >= the warp count matches the seeded run)
+    sp.claim_low = P->num_sms * 40;
     if (const char* e = std::getenv("WPM_CLAIM_LOW")) sp.claim_low = std::max(1, std::atoi(e));
+    if (L.progress && P->root_stats) {  // nodes per root task / frontier record (the scaling projection)
+        if (P->d_root_nodes.ensure((size_t)std::max<long long>(nroots, 1)))
+            return fail(WPM_EINTERNAL, "device allocation failed (root stats)");
+        CU(cudaMemsetAsync(P->d_root_nodes.p, 0, (size_t)std::max<long long>(nroots, 1) * 8, P->stream));
+        sp.root_nodes = P->d_root_nodes.p;
+        P->root_count = nroots;
+    }
     if ((nseed > 0 || L.claim_recs) && !launch_k3_search(sp, P->num_sms, P->stream, &P->warps))
         return fail(WPM_EINTERNAL, std::string("kernel 3 launch: ") + cudaGetErrorString(cudaGetLastError()));
     return WPM_OK;
@@ -1233,9 +1251,10 @@ int enable_peer(int dev, int leader) {
     return WPM_OK;
 }
 
-// frontier target: enough records that dynamic claims balance the GPUs (a
-// few hundred per GPU); the split depth grows two levels per round until then
-long long frontier_target(int ndev) { return std::max<long long>(1024, 512LL * ndev); }
+// frontier target: enough records that dynamic claims balance the GPUs
+// (2048 per GPU; the largest record is then ~0.2-0.3 % of the work at n = 8
+// and 11); the split depth grows two levels per round until then
+long long frontier_target(int ndev) { return std::max<long long>(2048, 2048LL * ndev); }
 
 }  // namespace
 
@@ -1545,6 +1564,31 @@ extern "C" int wpm_plan_set_progress(wpm_plan_t* P, void (*fn)(int64_t, int64_t,
     return WPM_OK;
 }
 
+// per-root search nodes of the following runs' main phase (root tasks, or
+// frontier records after a split): the input of the multi-GPU scaling
+// projection (a list schedule of the records over W GPUs)
+extern "C" int wpm_plan_set_root_stats(wpm_plan_t* P, int32_t on) {
+    if (!P) return fail(WPM_EINVAL, "null plan");
+    P->root_stats = on != 0;
+    return WPM_OK;
+}
+
+// nodes of each root task / frontier record of the last run (at most cap);
+// returns the root count, and the split phase's own nodes in *split_nodes
+extern "C" int64_t wpm_plan_root_nodes(wpm_plan_t* P, int64_t* out, int64_t cap, int64_t* split_nodes) {
+    if (!P) return -fail(WPM_EINVAL, "null plan");
+    if (!P->root_stats || P->root_count <= 0) return 0;
+    CU(cudaSetDevice(P->device));
+    const long long k = std::min<long long>(cap, P->root_count);
+    std::vector<unsigned long long> h((size_t)P->root_count);
+    CU(cudaMemcpy(h.data(), P->d_root_nodes.p, (size_t)P->root_count * 8, cudaMemcpyDeviceToHost));
+    long long sum = 0;
+    for (long long i = 0; i < P->root_count; ++i) sum += (long long)h[(size_t)i];
+    for (long long i = 0; i < k; ++i) out[i] = (int64_t)h[(size_t)i];
+    if (split_nodes) *split_nodes = P->nodes - sum;
+    return P->root_count;
+}
+
 // search-node budget of the following runs (0 = none): a run that reaches it
 // stops early and reports truncated = 1 -- a throughput / divergence stress
 // on universes whose full enumeration is out of reach, not an enumeration
@@ -1601,7 +1645,7 @@ extern "C" int wpm_canonical_sort_device(int32_t device, const uint32_t* bits32,
     DevBuf<uint32_t> keys;
     DevBuf<unsigned long long> d;
     const size_t tb = canon_sort_temp_bytes(count, words32);
-    if (temp.ensure(tb) || keys.ensure((size_t)count * (kw + 1)) || d.ensure(1))
+    if (temp.ensure(tb) || keys.ensure((size_t)count * rec_words(words32)) || d.ensure(1))
         return fail(WPM_EINTERNAL, "allocation failed (sort)");
     CU(cudaMemsetAsync(d.p, 0, 8, st));
     if (canon_pack(bits32, map_ids, count, words32, keys.p, st) ||
@@ -1819,7 +1863,7 @@ extern "C" int wpm_plan_line13(wpm_plan_t* P, int64_t* line7_out, int64_t* line1
     const size_t tsel = l13_select_temp_bytes(std::max<long long>(cnt, 1));
     size_t total_facets = 0;
     for (const MapDesc& d : P->desc) total_facets = std::max<size_t>(total_facets, d.facet_off + d.M);
-    if (P->d_gidx.ensure(total_facets) || P->d_l13_keys.ensure((size_t)cnt * (kw + 1)) ||
+    if (P->d_gidx.ensure(total_facets) || P->d_l13_keys.ensure((size_t)cnt * rec_words(gw)) ||
         P->d_l13_rows.ensure((size_t)cnt * gw) || P->d_l13_map.ensure(cnt) || P->d_l13_iota.ensure(cnt) ||
         P->d_l13_uidx.ensure(cnt) || P->d_l13_sidx.ensure(cnt) || P->d_l13_flags.ensure(cnt) ||
         P->d_l13_temp.ensure(std::max(tsort, tsel)) || P->d_l13_num.ensure(2) || P->d_l13_dups.ensure(1))
@@ -1827,7 +1871,7 @@ extern "C" int wpm_plan_line13(wpm_plan_t* P, int64_t* line7_out, int64_t* line1
     CU(cudaEventRecord(P->ev[0], P->stream));
     CU(cudaMemsetAsync(P->d_l13_dups.p, 0, 8, P->stream));
     if (l13_global_rank(P->num_maps, P->d_maps.p, P->d_facets.p, P->d_gidx.p, P->stream) ||
-        l13_remap(P->d_sorted_bits.p, P->d_sorted_map.p, cnt, P->w32, P->d_maps.p, P->d_gidx.p, kw,
+        l13_remap(P->d_sorted_bits.p, P->d_sorted_map.p, cnt, P->w32, P->d_maps.p, P->d_gidx.p, kw, rec_words(gw),
                   P->d_l13_keys.p, P->num_sms, P->stream) ||
         canon_sort_keys(P->d_l13_keys.p, cnt, gw, P->d_l13_rows.p, P->d_l13_map.p, P->d_l13_temp.p,
                         P->d_l13_temp.n, nullptr, P->d_l13_dups.p, P->stream) ||

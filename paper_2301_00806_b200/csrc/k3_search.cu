@@ -818,6 +818,7 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
         if (lane == 0) {
             reinterpret_cast<int*>(w.base + C::META)[0] = (int)(h2 >> 16);
             reinterpret_cast<uint32_t*>(w.base + C::META)[1] = h3;
+            reinterpret_cast<unsigned long long*>(w.base + C::META)[1] = nodes;  // per-root node accounting
         }
         __syncwarp();
         const int map = (int)(h0 & 0xFFFFu);
@@ -934,6 +935,8 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
         }
         // task finished
         if (lane == 0) {
+            if (p.root_nodes)
+                atomicAdd(&p.root_nodes[w.root()], nodes - reinterpret_cast<unsigned long long*>(w.base + C::META)[1]);
             if (p.root_pend && atomicSub(&p.root_pend[w.root()], 1u) == 1u) {
                 const unsigned long long d = atomicAdd(p.roots_done, 1ull) + 1ull;
                 if (p.progress_host)  // host takes the max of what it sees

@@ -1,4 +1,5 @@
-// k4_canon.cu -- canonical order of the emitted WPMs.
+// k4_canon.cu -- canonical order of the emitted WPMs: one persistent
+// merge-sort kernel (cooperative launch, grid-wide barriers between passes).
 //
 // Replaces the merge + sort + unique of enumerate_wpm (search.hpp:247-257):
 // complexes are ordered by their facet lists (std::vector<VertexSet>
@@ -7,251 +8,314 @@
 // that is decided at d = the lowest facet in exactly one of A, B: the list
 // holding d is smaller unless the other list ends before d.
 //
-// Kernel 3 emits each WPM as a fixed-width key row -- W uint32 words of the
-// characteristic bitset (zero padded, W a bucket >= the plan's width)
-// followed by the map id.  Narrow rows (W <= 4, M <= 128, i.e. n <= 5) are
-// merge-sorted (CUB) as keys themselves: no indirection, comparisons in
-// registers.  W is the exact word count there (n = 5 has M <= 88: 16-byte
-// keys instead of 20).  Wider rows merge-sort row indices instead, the comparator
-// reading the rows from L2 (moving 36-132 B keys through every merge pass
-// measured 2-4x slower).  A split/gather pass then writes the canonical rows
-// (the C-ABI width) and map ids, records per-map group boundaries and counts
-// adjacent duplicates (the DFS partitions the space, so the count is 0 -- a
-// checked invariant, not a dedupe).
-#include <cub/device/device_merge_sort.cuh>
+// Records are what kernel 3 emits: w32 bitset words, zero padding, the map
+// id in the last word -- rw = rec_words(w32), a multiple of 4 (16-byte
+// vectors move them) -- ordered by (map, canonical order).
+// A prefix of the facet list does not bound the work (rows of one map share
+// long prefixes: 8-facet prefixes still tie up to 1,260 rows at n = 11), so
+// the sort compares whole records:
+//   phase 1  every CTA sorts tiles of T records in shared memory (bitonic
+//            network over record indices; the records stay put);
+//   phase 2  merge passes, runs of T, 2T, 4T, ...: each CTA owns chunks of C
+//            output records, finds its input ranges by merge-path binary
+//            searches on the L2-resident records, stages them in shared
+//            memory and merges (every thread a merge-path diagonal);
+//   phase 3  the C-ABI split: rows (w32 words) + map ids, the first row of
+//            each map, adjacent duplicates counted (the DFS partitions the
+//            space, so 0 -- a checked invariant, not a dedupe).
+// One launch per sort; passes are separated by grid.sync().
+#include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "wpm_internal.h"
 
+namespace cg = cooperative_groups;
+
 namespace wpm {
 
-template <int W>
-struct RowKey {
-    uint32_t w[W];
-    uint32_t map;
+namespace {
+
+constexpr int SORT_THREADS = 512;
+
+struct SortParams {
+    const uint32_t* in;    // count * rw records (kernel-3 output)
+    uint32_t* buf0;        // ping-pong record buffers (buf0 may alias nothing)
+    uint32_t* buf1;
+    long long count;
+    int w32, rw;
+    int tile;              // records per phase-1 tile (power of two)
+    int chunk;             // output records per merge chunk (<= tile)
+    uint32_t* out_bits;    // count * w32
+    uint16_t* out_map;
+    long long* first_row;  // per map (may be null)
+    unsigned long long* dups;
 };
 
-template <int W>
-struct RowLess {
-    __device__ __forceinline__ bool operator()(const RowKey<W>& A, const RowKey<W>& B) const {
-        if (A.map != B.map) return A.map < B.map;
-#pragma unroll
-        for (int i = 0; i < W; ++i) {
-            const uint32_t x = A.w[i] ^ B.w[i];
-            if (!x) continue;
-            const uint32_t low = x & (0u - x);
-            const bool a_has = (A.w[i] & low) != 0u;
-            const RowKey<W>& O = a_has ? B : A;
-            bool more = (O.w[i] & ~((low << 1) - 1u)) != 0u;
-#pragma unroll
-            for (int v = i + 1; v < W; ++v) more |= O.w[v] != 0u;
-            return a_has ? more : !more;
+// canonical record order: map, then the facet-list order on the bitsets
+__device__ __forceinline__ bool rec_less(const uint32_t* A, const uint32_t* B, int w32) {
+    const int mp = rec_words(w32) - 1;  // the map id
+    const uint32_t ma = A[mp], mb = B[mp];
+    if (ma != mb) return ma < mb;
+    for (int w = 0; w < w32; ++w) {
+        const uint32_t a = A[w], b = B[w];
+        const uint32_t x = a ^ b;
+        if (!x) continue;
+        const uint32_t low = x & (0u - x);
+        const bool a_has = (a & low) != 0u;
+        const uint32_t* O = a_has ? B : A;
+        bool more = (O[w] & ~((low << 1) - 1u)) != 0u;
+        for (int v = w + 1; v < w32 && !more; ++v) more = O[v] != 0u;
+        return a_has ? more : !more;
+    }
+    return false;
+}
+
+// copy nw words (a multiple of 4; 16-byte aligned) global -> shared in
+// 16-byte vectors, four loads in flight per thread
+__device__ __forceinline__ void stage16(uint32_t* dst, const uint32_t* src, long long nw) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    const long long nv = nw >> 2;
+    const int bd = blockDim.x;
+    long long i = threadIdx.x;
+    for (; i + 3 * bd < nv; i += 4 * bd) {
+        const uint4 a = __ldcg(s + i), b = __ldcg(s + i + bd), c = __ldcg(s + i + 2 * bd), e = __ldcg(s + i + 3 * bd);
+        d[i] = a;
+        d[i + bd] = b;
+        d[i + 2 * bd] = c;
+        d[i + 3 * bd] = e;
+    }
+    for (; i < nv; i += bd) d[i] = __ldcg(s + i);
+}
+
+// merge-path split of diagonal d between sorted A[0..na) and B[0..nb):
+// the number of A elements among the first d outputs (A wins ties)
+__device__ __forceinline__ long long merge_split(const uint32_t* A, long long na, const uint32_t* B, long long nb,
+                                                 long long d, int w32, int rw) {
+    long long lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+    while (lo < hi) {
+        const long long a = (lo + hi) >> 1;  // take a from A, d - a from B
+        // A[a] vs B[d - a - 1]: if B[d-a-1] < A[a] then fewer A needed
+        if (rec_less(B + (size_t)(d - a - 1) * rw, A + (size_t)a * rw, w32)) hi = a;
+        else lo = a + 1;
+    }
+    return lo;
+}
+
+// the same split searched by a whole warp: 32 probes per round (a 33-ary
+// search), so a merge-path search over L2-resident runs costs log33 rounds
+// of dependent loads instead of log2
+__device__ __forceinline__ long long merge_split_warp(const uint32_t* A, long long na, const uint32_t* B, long long nb,
+                                                      long long d, int w32, int rw, int lane) {
+    long long lo = d > nb ? d - nb : 0, hi = d < na ? d : na;  // answer in [lo, hi]
+    while (hi - lo > 0) {
+        const long long span = hi - lo;
+        // probe a_i = lo + (i + 1) * span / 33 for lanes i < 32 (distinct once span >= 33)
+        const long long a = lo + ((long long)(lane + 1) * span) / 33;
+        bool pred = true;  // pred(a): B[d-a-1] < A[a]  (monotone in a)
+        if (a < hi) pred = rec_less(B + (size_t)(d - a - 1) * rw, A + (size_t)a * rw, w32);
+        const unsigned t = __ballot_sync(0xFFFFFFFFu, pred);
+        const int f = t ? __ffs(t) - 1 : 32;
+        // the answer lies in (a_{f-1}, a_f]: a_{-1} = lo - 1, a_32 = hi
+        const long long nlo = f == 0 ? lo : lo + ((long long)f * span) / 33 + 1;
+        const long long nhi = f == 32 ? hi : lo + ((long long)(f + 1) * span) / 33;
+        lo = nlo;
+        hi = nhi;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(SORT_THREADS, 2) k4_sort(const __grid_constant__ SortParams p) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    cg::grid_group grid = cg::this_grid();
+    const int T = p.tile, rw = p.rw, w32 = p.w32;
+    const long long N = p.count;
+    uint32_t* recs = sm;                                       // T records
+    uint16_t* idx = reinterpret_cast<uint16_t*>(sm + (size_t)T * rw);  // T indices (bitonic)
+    const long long ntiles = (N + T - 1) / T;
+    // ---- phase 1: sort tiles of T records (in -> buf0)
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long base = tile * T;
+        const int cnt = (int)min((long long)T, N - base);
+        stage16(recs, p.in + (size_t)base * rw, (long long)cnt * rw);
+        for (int i = threadIdx.x; i < T; i += blockDim.x) idx[i] = (uint16_t)i;
+        __syncthreads();
+        for (int k = 2; k <= T; k <<= 1)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < T; i += blockDim.x) {
+                    const int l = i ^ j;
+                    if (l > i) {
+                        const int a = idx[i], b = idx[l];
+                        // indices >= cnt are +inf padding
+                        const bool b_lt_a = a >= cnt ? b < cnt || b < a
+                                                     : (b < cnt && rec_less(recs + (size_t)b * rw, recs + (size_t)a * rw, w32));
+                        const bool up = (i & k) == 0;
+                        if (up == b_lt_a) {
+                            idx[i] = (uint16_t)b;
+                            idx[l] = (uint16_t)a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        uint4* dst = reinterpret_cast<uint4*>(p.buf0 + (size_t)base * rw);
+        const int rv = rw >> 2;
+        for (int i = threadIdx.x; i < cnt * rv; i += blockDim.x) {
+            const int r = i / rv, c = i - r * rv;
+            dst[i] = reinterpret_cast<const uint4*>(recs + (size_t)idx[r] * rw)[c];
         }
-        return false;
+        __syncthreads();
     }
-};
-
-// split the sorted key rows into the C-ABI layout: rows of w32 words + map ids;
-// group boundaries (first row per map) and adjacent-duplicate count
-template <int W>
-__global__ void split_rows(const RowKey<W>* __restrict__ keys, long long n, int w32, uint32_t* __restrict__ out,
-                           uint16_t* __restrict__ out_map, unsigned long long* dups, long long* __restrict__ first_row) {
-    const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (row >= n) return;
-    const RowKey<W>& k = keys[row];
-    for (int i = 0; i < w32; ++i) out[(size_t)row * w32 + i] = k.w[i];
-    out_map[row] = (uint16_t)k.map;
-    if (row == 0 || keys[row - 1].map != k.map) {
-        if (first_row) first_row[k.map] = row;
-    } else {
-        bool same = true;
-        const RowKey<W>& p = keys[row - 1];
-#pragma unroll
-        for (int i = 0; i < W; ++i) same &= p.w[i] == k.w[i];
-        if (same) atomicAdd(dups, 1ull);
-    }
-}
-
-// pack externally supplied rows (w32 words + uint16 map ids) into key rows
-template <int W>
-__global__ void pack_rows(const uint32_t* __restrict__ bits, const uint16_t* __restrict__ map, long long n, int w32,
-                          RowKey<W>* __restrict__ keys) {
-    const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (row >= n) return;
-    RowKey<W> k;
-#pragma unroll
-    for (int i = 0; i < W; ++i) k.w[i] = i < w32 ? bits[(size_t)row * w32 + i] : 0u;
-    k.map = map[row];
-    keys[row] = k;
-}
-
-// ---- wide rows: merge-sort row indices instead (moving > 20-byte keys costs
-// more than the comparator's L2 reads); the comparator reads the key rows
-struct IdxLess {
-    const uint32_t* keys;
-    int rw, w32;
-    __device__ __forceinline__ bool operator()(const uint32_t& a, const uint32_t& b) const {
-        const uint32_t* A = keys + (size_t)a * rw;
-        const uint32_t* B = keys + (size_t)b * rw;
-        const uint32_t ma = A[rw - 1], mb = B[rw - 1];
-        if (ma != mb) return ma < mb;
-        for (int w = 0; w < w32; ++w) {
-            const uint32_t x = A[w] ^ B[w];
-            if (!x) continue;
-            const uint32_t low = x & (0u - x);
-            const bool a_has = (A[w] & low) != 0u;
-            const uint32_t* O = a_has ? B : A;
-            bool more = (O[w] & ~((low << 1) - 1u)) != 0u;
-            for (int v = w + 1; v < w32 && !more; ++v) more = O[v] != 0u;
-            return a_has ? more : !more;
+    grid.sync();
+    // ---- phase 2: merge passes (runs of L -> 2L), C = T output records per chunk
+    const uint32_t* src = p.buf0;
+    uint32_t* dst = p.buf1;
+    __shared__ long long s_rng[4];
+    const int C = p.chunk;
+    for (long long L = T; L < N; L <<= 1) {
+        const long long nchunks = (N + C - 1) / C;
+        for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
+            const long long o0 = c * C, o1 = min(N, o0 + C);
+            const long long run = o0 / (2 * L), rbase = run * 2 * L;
+            const long long na = min(L, N - rbase), nb = max(0ll, min(L, N - rbase - L));
+            const uint32_t* A = src + (size_t)rbase * rw;
+            const uint32_t* B = A + (size_t)na * rw;
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            if (warp < 2) {
+                const long long r = merge_split_warp(A, na, B, nb, (warp ? o1 : o0) - rbase, w32, rw, lane);
+                if (lane == 0) s_rng[warp] = r;
+            }
+            __syncthreads();
+            const long long a0 = s_rng[0], a1 = s_rng[1];
+            const long long b0 = (o0 - rbase) - a0, b1 = (o1 - rbase) - a1;
+            const int ca = (int)(a1 - a0), cb = (int)(b1 - b0);
+            // stage A[a0..a1) then B[b0..b1) in shared memory
+            stage16(recs, A + (size_t)a0 * rw, (long long)ca * rw);
+            stage16(recs + (size_t)ca * rw, B + (size_t)b0 * rw, (long long)cb * rw);
+            __syncthreads();
+            const uint32_t* SA = recs;
+            const uint32_t* SB = recs + (size_t)ca * rw;
+            const int total = ca + cb;
+            const int per = (total + blockDim.x - 1) / blockDim.x;
+            const int d0 = min(total, (int)threadIdx.x * per), d1 = min(total, d0 + per);
+            if (d0 < d1) {  // each thread: its merge-path diagonal, then `per` sources
+                int ia = (int)merge_split(SA, ca, SB, cb, d0, w32, rw);
+                int ib = d0 - ia;
+                for (int d = d0; d < d1; ++d) {
+                    const bool take_a = ib >= cb || (ia < ca && !rec_less(SB + (size_t)ib * rw, SA + (size_t)ia * rw, w32));
+                    idx[d] = (uint16_t)(take_a ? ia++ : ca + ib++);
+                }
+            }
+            __syncthreads();
+            // coalesced write of the merged chunk
+            uint4* out = reinterpret_cast<uint4*>(dst + (size_t)o0 * rw);
+            const int rv = rw >> 2;
+            for (int i = threadIdx.x; i < total * rv; i += blockDim.x) {
+                const int r = i / rv, c = i - r * rv;
+                out[i] = reinterpret_cast<const uint4*>(recs + (size_t)idx[r] * rw)[c];
+            }
+            __syncthreads();
         }
-        return false;
+        grid.sync();
+        const uint32_t* t = src;
+        src = dst;
+        dst = const_cast<uint32_t*>(t);
     }
-};
-
-__global__ void iota_u32(uint32_t* idx, long long n) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) idx[i] = (uint32_t)i;
-}
-
-__global__ void gather_rows(const uint32_t* __restrict__ keys, int rw, const uint32_t* __restrict__ idx, long long n,
-                            int w32, uint32_t* __restrict__ out, uint16_t* __restrict__ out_map,
-                            unsigned long long* dups, long long* __restrict__ first_row) {
-    // one warp per row
-    const long long row = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (row >= n) return;
-    const uint32_t* S = keys + (size_t)idx[row] * rw;
-    const uint32_t* P = row > 0 ? keys + (size_t)idx[row - 1] * rw : S;
-    const bool new_group = row == 0 || P[rw - 1] != S[rw - 1];
-    if (lane == 0 && new_group && first_row) first_row[S[rw - 1]] = row;
-    bool same = !new_group;
-    for (int w = lane; w < w32; w += 32) {
-        const uint32_t v = S[w];
-        out[(size_t)row * w32 + w] = v;
-        if (P[w] != v) same = false;
+    // ---- phase 3: the C-ABI layout, group boundaries, duplicates
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N * w32; i += stride) {
+        const long long r = i / w32, c = i - r * w32;
+        p.out_bits[i] = src[(size_t)r * rw + c];
     }
-    same = __all_sync(0xFFFFFFFFu, same);
-    if (lane == 0) {
-        out_map[row] = (uint16_t)S[rw - 1];
-        if (same) atomicAdd(dups, 1ull);
+    unsigned long long nd = 0;
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += stride) {
+        const uint32_t* R = src + (size_t)r * rw;
+        const uint32_t* Q = R - rw;  // the previous record (r > 0)
+        p.out_map[r] = (uint16_t)R[rw - 1];
+        if (r == 0 || Q[rw - 1] != R[rw - 1]) {
+            if (p.first_row) p.first_row[R[rw - 1]] = r;
+        } else {
+            bool same = true;
+            for (int i = 0; i < w32; ++i) same &= R[i] == Q[i];
+            nd += same;
+        }
     }
+    if (nd) atomicAdd(p.dups, nd);
 }
 
+int g_sort_sms[64] = {0};
 
-int key_words_for(int w32) {
-#ifdef WPM_KEY_FINE
-    static const int buckets[] = {1, 2, 3, 4, 5, 6, 8, 16, 24, 32, 48, 64};
-#else
-    static const int buckets[] = {1, 2, 3, 4, 8, 16, 24, 32, 48, 64};
-#endif
-    for (int b : buckets)
-        if (w32 <= b) return b;
-    return -1;
-}
+}  // namespace
 
-template <int W>
-static size_t temp_bytes_w(long long count) {
-    size_t bytes = 0;
-    cub::DeviceMergeSort::SortKeys(nullptr, bytes, (RowKey<W>*)nullptr, (int)count, RowLess<W>());
-    return bytes;
-}
+int key_words_for(int w32) { return w32 >= 1 && w32 <= 64 ? w32 : -1; }
 
-template <int W>
-static int sort_w(uint32_t* d_keys, long long count, int w32, uint32_t* d_sorted_bits, uint16_t* d_sorted_map,
-                  void* d_temp, size_t temp_bytes, long long* d_first_row, unsigned long long* d_dups,
-                  cudaStream_t st) {
-    auto* keys = reinterpret_cast<RowKey<W>*>(d_keys);
-    size_t bytes = temp_bytes;
-    if (cub::DeviceMergeSort::SortKeys(d_temp, bytes, keys, (int)count, RowLess<W>(), st) != cudaSuccess) return 1;
-    split_rows<W><<<(unsigned)((count + 255) / 256), 256, 0, st>>>(keys, count, w32, d_sorted_bits, d_sorted_map,
-                                                                    d_dups, d_first_row);
-    return cudaGetLastError() == cudaSuccess ? 0 : 1;
-}
-
-#ifdef WPM_KEY_FINE
-#define WPM_KEY_FINE_CASES(CALL) \
-    case 5: CALL(5);             \
-    case 6: CALL(6);
-#else
-#define WPM_KEY_FINE_CASES(CALL)
-#endif
-#define WPM_KEY_DISPATCH(KW, CALL) \
-    switch (KW) {                  \
-        case 1: CALL(1);           \
-        case 2: CALL(2);           \
-        case 3: CALL(3);           \
-        case 4: CALL(4);           \
-        WPM_KEY_FINE_CASES(CALL)   \
-        case 8: CALL(8);           \
-        case 16: CALL(16);         \
-        case 24: CALL(24);         \
-        case 32: CALL(32);         \
-        case 48: CALL(48);         \
-        case 64: CALL(64);         \
-        default: break;            \
-    }
-
-// temp = merge-sort scratch (+ the index array on the wide-row path)
+// temp = the two ping-pong record buffers (the input stays intact)
 size_t canon_sort_temp_bytes(long long count, int w32) {
-    const int kw = key_words_for(w32);
-    switch (kw) {
-        case 1: return temp_bytes_w<1>(count);
-        case 2: return temp_bytes_w<2>(count);
-        case 3: return temp_bytes_w<3>(count);
-        case 4: return temp_bytes_w<4>(count);
-#ifdef WPM_KEY_DIRECT6
-        case 5: return temp_bytes_w<5>(count);
-        case 6: return temp_bytes_w<6>(count);
-#endif
-        default: break;
-    }
-    size_t bytes = 0;
-    cub::DeviceMergeSort::SortKeys(nullptr, bytes, (uint32_t*)nullptr, (int)count, IdxLess{nullptr, kw + 1, w32});
-    return bytes + ((size_t)count * 4 + 256);
+    return (size_t)2 * (size_t)count * (size_t)rec_words(w32) * 4 + 256;
 }
 
 int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sorted_bits, uint16_t* d_sorted_map,
                     void* d_temp, size_t temp_bytes, long long* d_first_row, unsigned long long* d_dups,
                     cudaStream_t st) {
     if (count <= 0) return 0;
-    const int kw = key_words_for(w32);
-#define SW(W)                                                                                                  \
-    case W:                                                                                                    \
-        return sort_w<W>(d_keys, count, w32, d_sorted_bits, d_sorted_map, d_temp, temp_bytes, d_first_row, d_dups, st);
-    switch (kw) {
-        SW(1) SW(2) SW(3) SW(4)
-#ifdef WPM_KEY_DIRECT6
-        SW(5) SW(6)
-#endif
-        default: break;
-    }
-#undef SW
-    const size_t idx_bytes = (size_t)count * 4 + 256;
-    uint32_t* idx = reinterpret_cast<uint32_t*>(d_temp);
-    void* sort_temp = static_cast<uint8_t*>(d_temp) + idx_bytes;
-    size_t bytes = temp_bytes - idx_bytes;
-    iota_u32<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(idx, count);
-    const IdxLess cmp{d_keys, kw + 1, w32};
-    if (cub::DeviceMergeSort::SortKeys(sort_temp, bytes, idx, (int)count, cmp, st) != cudaSuccess) return 1;
-    const long long threads = count * 32;
-    gather_rows<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(d_keys, kw + 1, idx, count, w32, d_sorted_bits,
-                                                                     d_sorted_map, d_dups, d_first_row);
-    return cudaGetLastError() == cudaSuccess ? 0 : 1;
+    const int rw = rec_words(w32);
+    if (temp_bytes < canon_sort_temp_bytes(count, w32)) return 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 1;
+    if (!g_sort_sms[dev] && cudaDeviceGetAttribute(&g_sort_sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return 1;
+    // tile: a power of two with T records + T indices in <= 200 KB of shared
+    // memory; merge chunks of the same size
+    int T = 2048;  // tile / chunk sweep 2048-8192 x 512-2048 at n = 5 and 8: 2048 / 2048 best
+    while (T > 64 && (size_t)T * rw * 4 + (size_t)T * 2 > 200u * 1024u) T >>= 1;
+    if (const char* e = std::getenv("WPM_SORT_TILE")) T = std::max(64, std::min(T, std::atoi(e)));
+    int Cc = T;
+    if (const char* e = std::getenv("WPM_SORT_CHUNK")) Cc = std::max(32, std::min(T, std::atoi(e)));
+    const size_t smem = (size_t)T * rw * 4 + (size_t)T * 2 + 16;
+    if (cudaFuncSetAttribute(k4_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 1;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_sort, SORT_THREADS, smem) != cudaSuccess || per_sm < 1)
+        return 1;
+    const long long work = std::max((count + T - 1) / T, (count + Cc - 1) / Cc);
+    const int grid = (int)std::min<long long>(work, (long long)per_sm * g_sort_sms[dev]);
+    SortParams sp{};
+    sp.in = d_keys;
+    sp.buf0 = static_cast<uint32_t*>(d_temp);
+    sp.buf1 = sp.buf0 + (size_t)count * rw;
+    sp.count = count;
+    sp.w32 = w32;
+    sp.rw = rw;
+    sp.tile = T;
+    sp.chunk = Cc;
+    sp.out_bits = d_sorted_bits;
+    sp.out_map = d_sorted_map;
+    sp.first_row = d_first_row;
+    sp.dups = d_dups;
+    void* args[] = {&sp};
+    if (cudaLaunchCooperativeKernel((const void*)k4_sort, dim3(grid), dim3(SORT_THREADS), args, smem, st) != cudaSuccess)
+        return 1;
+    return 0;
+}
+
+__global__ void pack_records(const uint32_t* __restrict__ bits, const uint16_t* __restrict__ map, long long n, int w32,
+                             uint32_t* __restrict__ recs) {
+    const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= n) return;
+    const int rw = rec_words(w32);
+    uint32_t* r = recs + (size_t)row * rw;
+    for (int i = 0; i < rw - 1; ++i) r[i] = i < w32 ? bits[(size_t)row * w32 + i] : 0u;
+    r[rw - 1] = map[row];
 }
 
 int canon_pack(const uint32_t* d_bits, const uint16_t* d_map, long long count, int w32, uint32_t* d_keys,
                cudaStream_t st) {
     if (count <= 0) return 0;
-    const int kw = key_words_for(w32);
-#define PK(W)                                                                                                    \
-    pack_rows<W><<<(unsigned)((count + 255) / 256), 256, 0, st>>>(d_bits, d_map, count, w32,                      \
-                                                                    reinterpret_cast<RowKey<W>*>(d_keys));       \
+    pack_records<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(d_bits, d_map, count, w32, d_keys);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
-    WPM_KEY_DISPATCH(kw, PK)
-#undef PK
-    return 1;
 }
 
 }  // namespace wpm

@@ -61,9 +61,10 @@ __global__ void global_rank(const MapDesc* __restrict__ maps, const uint32_t* __
         gidx[d.facet_off + j] = (uint16_t)colex_rank(facets[d.facet_off + j] >> 1, B);
 }
 
-// one warp per WPM row: universe bits -> global key row (kw words + map 0)
+// one warp per WPM row: universe bits -> global key record (kw words, zero
+// padding, map 0 in the last of rw words)
 __global__ void remap_rows(const uint32_t* __restrict__ rows, const uint16_t* __restrict__ map_ids, long long count,
-                           int w32, const MapDesc* __restrict__ maps, const uint16_t* __restrict__ gidx, int kw,
+                           int w32, const MapDesc* __restrict__ maps, const uint16_t* __restrict__ gidx, int kw, int rw,
                            uint32_t* __restrict__ keys) {
     __shared__ uint32_t buf[L13_WARPS][64];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -80,8 +81,8 @@ __global__ void remap_rows(const uint32_t* __restrict__ rows, const uint16_t* __
                 atomicOr(&b[g >> 5], 1u << (g & 31));
             }
         __syncwarp();
-        uint32_t* dst = keys + (size_t)row * (kw + 1);
-        for (int w = lane; w <= kw; w += 32) dst[w] = w < kw ? b[w] : 0u;
+        uint32_t* dst = keys + (size_t)row * rw;
+        for (int w = lane; w < rw; w += 32) dst[w] = w < kw ? b[w] : 0u;
         __syncwarp();
     }
 }
@@ -256,10 +257,11 @@ int l13_global_rank(int num_maps, const MapDesc* d_maps, const uint32_t* d_facet
 }
 
 int l13_remap(const uint32_t* d_rows, const uint16_t* d_map, long long count, int w32, const MapDesc* d_maps,
-              const uint16_t* d_gidx, int kw, uint32_t* d_keys, int num_sms, cudaStream_t st) {
+              const uint16_t* d_gidx, int kw, int rw, uint32_t* d_keys, int num_sms, cudaStream_t st) {
     if (count <= 0) return 0;
     const long long blocks = std::min<long long>((count + L13_WARPS - 1) / L13_WARPS, (long long)num_sms * 16);
-    remap_rows<<<(unsigned)blocks, 32 * L13_WARPS, 0, st>>>(d_rows, d_map, count, w32, d_maps, d_gidx, kw, d_keys);
+    remap_rows<<<(unsigned)blocks, 32 * L13_WARPS, 0, st>>>(d_rows, d_map, count, w32, d_maps, d_gidx, kw, rw,
+                                                            d_keys);
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

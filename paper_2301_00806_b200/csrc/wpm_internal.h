@@ -66,6 +66,7 @@ struct SearchParams {
     unsigned int* root_pend;
     unsigned long long* roots_done;
     unsigned long long* progress_host;
+    unsigned long long* root_nodes;  // optional: search nodes per root task / frontier record
 };
 
 // task record header (queue, frontier): [0] map | kind << 24, [1] facet or
@@ -87,6 +88,10 @@ int launch_k3_search(const SearchParams& p, int num_sms, cudaStream_t st, int* w
 // and splits them into sorted_bits (w32 words per row) / sorted_map, with the
 // first row of each map and the adjacent-duplicate count.
 int key_words_for(int w32);
+// record layout of every sort input (kernel 3, kernel 6, the line-13 union):
+// w32 bitset words, zero padding, the map id in the last word; the record is
+// a whole number of 16-byte vectors
+__host__ __device__ inline int rec_words(int w32) { return (w32 + 1 + 3) & ~3; }
 size_t canon_sort_temp_bytes(long long count, int w32);
 int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sorted_bits, uint16_t* d_sorted_map,
                     void* d_temp, size_t temp_bytes, long long* d_first_row, unsigned long long* d_dups,
@@ -99,7 +104,7 @@ int canon_pack(const uint32_t* d_bits, const uint16_t* d_map, long long count, i
 int l13_global_rank(int num_maps, const MapDesc* d_maps, const uint32_t* d_facets, uint16_t* d_gidx,
                     cudaStream_t st);
 int l13_remap(const uint32_t* d_rows, const uint16_t* d_map, long long count, int w32, const MapDesc* d_maps,
-              const uint16_t* d_gidx, int kw, uint32_t* d_keys, int num_sms, cudaStream_t st);
+              const uint16_t* d_gidx, int kw, int rw, uint32_t* d_keys, int num_sms, cudaStream_t st);
 size_t l13_select_temp_bytes(long long count);
 int l13_unique(const uint32_t* d_sorted, long long count, int gw, uint8_t* d_flags, uint32_t* d_iota,
                uint32_t* d_uidx, int* d_num, void* d_temp, size_t temp_bytes, cudaStream_t st);

@@ -1,28 +1,35 @@
 """Multi-GPU plumbing for the enumeration (one process per GPU).
 
-The search shards with no data-path collective: rank r of W takes the root
-tasks t with t % W == r (Plan.run(r, W); the root tasks are the
-"minimum facet" branches of every map, disjoint and exhaustive).  The only
-collectives are at the end:
+The job (parallel_for_index, parallel.hpp:27-54, across GPUs):
 
-  1. all_reduce of the per-map WPM counts and the node count,
-  2. all_gather of the per-rank row counts, then of the (padded) rows,
-  3. one canonical sort on rank 0 (wpm_canonical_sort_device on the GPU;
-     merge_host for CPU/gloo runs) -- the union is disjoint, so the sort
-     finds no duplicate, which is checked.
+  1. rank 0 splits the search tree below the root (Plan.split: split-mode
+     kernel-3 launches until the frontier has >= 2048 records per GPU; the
+     rows and nodes above the frontier stay on rank 0);
+  2. the frontier records are broadcast (NCCL) and a claim counter in rank
+     0's HBM is shared through a CUDA IPC handle;
+  3. every rank runs the claim phase (Plan.run_claim): its kernel pulls
+     frontier records through the one counter (system-scope atomics over
+     NVLink) into its own work queue and shares them by donation -- no GPU
+     ever waits for another, the records go to whichever GPU is free;
+  4. the canonical rows are gathered to rank 0 only (point-to-point
+     send/recv, not an all-gather) and sorted there once
+     (wpm_canonical_sort_device); the union is disjoint, so the sort finds no
+     duplicate, which is checked.
 
-Backend-agnostic over torch.distributed: NCCL with CUDA tensors on the GPU
-box, gloo with CPU tensors in the CPU tests.
+The same host logic runs over gloo with CPU tensors in the CPU tests, with a
+torch.distributed Store counter standing in for the device counter
+(StoreCounter) and the CPU restatement standing in for the device search.
 """
 from __future__ import annotations
 
-from typing import List, Sequence, Tuple
+from typing import Callable, List, Sequence, Tuple
 
 import numpy as np
 
 
 def shard_roots(num_tasks: int, rank: int, world: int) -> List[int]:
-    """Root-task indices owned by `rank` (mirrors plan_search in api.cu)."""
+    """Static root-task shard of `rank` (wpm_plan_run(plan, rank, world);
+    the fallback without a shared counter)."""
     return [t for t in range(num_tasks) if t % world == rank]
 
 
@@ -54,33 +61,34 @@ def merge_host(parts: Sequence[Tuple[np.ndarray, np.ndarray]]) -> Tuple[np.ndarr
     return maps, rows, dups
 
 
-def gather_rows(dist, maps: np.ndarray, rows: np.ndarray, device=None):
-    """all_gather per-rank (map_ids, rows) to every rank; returns the list of
-    per-rank parts.  Rows are uint64 words shipped as int64 tensors."""
+# ---------------------------------------------------------------- collectives
+
+def gather_to_rank0(dist, rank: int, world: int, parts: Sequence, device=None) -> List[List]:
+    """Point-to-point gather of per-rank tensors to rank 0 (each rank sends
+    its tensors' lengths, then the tensors; rank 0 receives them in rank
+    order).  parts: a list of 1-D tensors of fixed dtypes; returns, on rank 0,
+    [[rank r's tensors] for r in ranks], [] elsewhere.  NCCL and gloo."""
     import torch
 
-    words = rows.shape[1]
-    world = dist.get_world_size()
-    n = torch.tensor([rows.shape[0]], dtype=torch.int64, device=device)
-    counts = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(world)]
-    dist.all_gather(counts, n)
-    counts = [int(c.item()) for c in counts]
-    cap = max(counts) if counts else 0
-    pad_rows = np.zeros((cap, words), dtype=np.uint64)
-    pad_rows[: rows.shape[0]] = rows
-    pad_maps = np.zeros(cap, dtype=np.int64)
-    pad_maps[: maps.shape[0]] = maps
-    t_rows = torch.from_numpy(pad_rows.view(np.int64).copy()).to(device)
-    t_maps = torch.from_numpy(pad_maps).to(device)
-    g_rows = [torch.zeros_like(t_rows) for _ in range(world)]
-    g_maps = [torch.zeros_like(t_maps) for _ in range(world)]
-    dist.all_gather(g_rows, t_rows)
-    dist.all_gather(g_maps, t_maps)
-    parts = []
-    for r in range(world):
-        c = counts[r]
-        parts.append((g_maps[r][:c].cpu().numpy(), g_rows[r][:c].cpu().numpy().view(np.uint64)))
-    return parts
+    lens = torch.tensor([p.numel() for p in parts], dtype=torch.int64, device=device)
+    if rank != 0:
+        dist.send(lens, 0)
+        for p in parts:
+            if p.numel():
+                dist.send(p.contiguous(), 0)
+        return []
+    out = [list(parts)]
+    for r in range(1, world):
+        ln = torch.zeros_like(lens)
+        dist.recv(ln, r)
+        got = []
+        for p, k in zip(parts, ln.tolist()):
+            buf = torch.empty(int(k), dtype=p.dtype, device=p.device)
+            if k:
+                dist.recv(buf, r)
+            got.append(buf)
+        out.append(got)
+    return out
 
 
 def reduce_counts(dist, per_map: Sequence[int], nodes: int, device=None) -> Tuple[List[int], int]:
@@ -93,39 +101,123 @@ def reduce_counts(dist, per_map: Sequence[int], nodes: int, device=None) -> Tupl
     return v[:-1], v[-1]
 
 
+# ---------------------------------------------------------------- the shared frontier
+
+class StoreCounter:
+    """A claim counter over a torch.distributed Store (atomic add): the host
+    stand-in for the device claim counter in CPU tests."""
+
+    def __init__(self, store, key: str = "wpm_claim"):
+        self.store, self.key = store, key
+
+    def claim(self) -> int:
+        return int(self.store.add(self.key, 1)) - 1
+
+
+def claim_loop(counter, count: int, work: Callable[[int], None]) -> int:
+    """Host form of a GPU's claim phase: pull item indices from the shared
+    counter until it passes `count`; returns the items this rank processed."""
+    done = 0
+    while True:
+        i = counter.claim()
+        if i >= count:
+            return done
+        work(i)
+        done += 1
+
+
+def share_frontier(dist, rank: int, recs, count: int, recw: int, device):
+    """Broadcast rank 0's frontier records (count x recw uint32 words, shipped
+    as int32) to every rank; returns (recs tensor on this rank's device, count, recw)."""
+    import torch
+
+    hdr = torch.tensor([count, recw] if rank == 0 else [0, 0], dtype=torch.int64, device=device)
+    dist.broadcast(hdr, 0)
+    count, recw = (int(x) for x in hdr.tolist())
+    if rank != 0:
+        recs = torch.empty(max(count * recw, 1), dtype=torch.int32, device=device)
+    if count:
+        dist.broadcast(recs[: count * recw], 0)
+    return recs, count, recw
+
+
+def share_claim_counter(dist, rank: int, device: int):
+    """Rank 0 creates the device claim counter and broadcasts its 64-byte CUDA
+    IPC handle; the other ranks open it.  Returns (pointer, opened)."""
+    import torch
+
+    import paper_2301_00806_b200 as wpm
+
+    dev = torch.device("cuda", device)
+    if rank == 0:
+        ptr, handle = wpm.claim_counter_create(device)
+        h = torch.tensor(list(handle), dtype=torch.uint8, device=dev)
+    else:
+        h = torch.zeros(64, dtype=torch.uint8, device=dev)
+    dist.broadcast(h, 0)
+    if rank == 0:
+        return ptr, False
+    return wpm.claim_counter_open(device, bytes(h.cpu().tolist())), True
+
+
+def run_job(dist, plan, rank: int, world: int, device: int, counter=None, target: int = 0) -> int:
+    """One multi-GPU enumeration across the ranks (the module docstring's steps
+    1-3) on the ranks' resident plans (same maps).  `counter` = (pointer,
+    opened) from share_claim_counter, reused across runs (reset by rank 0).
+    Returns this rank's row count; its canonical rows stay on its device."""
+    import torch
+
+    import paper_2301_00806_b200 as wpm
+
+    dev = torch.device("cuda", device)
+    if world == 1:
+        plan.split(3, target or 1024)
+        own = counter is None
+        ctr = wpm.claim_counter_create(device)[0] if own else counter[0]
+        if not own:
+            wpm.claim_counter_reset(device, ctr)
+        try:
+            return plan.run_claim(ctr)
+        finally:
+            if own:
+                wpm.claim_counter_close(device, ctr, False)
+    if rank == 0:
+        plan.split(3, target or 2048 * world)
+        ptr, count, recw = plan.frontier()
+        recs = _wrap_device(ptr, count * recw, torch.int32, dev)
+        wpm.claim_counter_reset(device, counter[0])
+    else:
+        recs, count, recw = None, 0, 0
+    torch.cuda.synchronize(dev)
+    recs, count, recw = share_frontier(dist, rank, recs, count, recw, dev)
+    if rank != 0:
+        plan.load_frontier(recs.data_ptr(), count)
+    dist.barrier()  # the counter is reset before any rank claims
+    total = plan.run_claim(counter[0])
+    dist.barrier()  # every claim is done before the counter is reused
+    return total
+
+
 def gather_to_rank0_device(dist, plan, rank: int, device: int, return_rows: bool = False):
-    """GPU path: NCCL all_gather of every rank's resident canonical rows into
-    rank 0's HBM, then one canonical sort there.  Returns (count, duplicates)
-    on rank 0, (local count, 0) elsewhere; with return_rows also the sorted
-    rows / map ids (rank 0) as device tensors."""
+    """Every rank's resident canonical rows go to rank 0 only (send/recv),
+    then one canonical sort there.  Returns (count, duplicates) on rank 0,
+    (local count, 0) elsewhere; with return_rows also the sorted rows / map
+    ids (rank 0) as device tensors."""
     import torch
 
     import paper_2301_00806_b200 as wpm
 
     bits_ptr, map_ptr, count, w32 = plan.device_result()
     dev = torch.device("cuda", device)
-    # wrap the resident rows (uint32 words) and map ids without a copy
     rows = _wrap_device(bits_ptr, count * w32, torch.int32, dev)
-    maps = _wrap_device(map_ptr, count, torch.int16, dev)
+    maps = _wrap_device(map_ptr, count, torch.int16, dev).view(torch.uint8)  # NCCL has no int16: bytes
     world = dist.get_world_size()
-    n = torch.tensor([count], dtype=torch.int64, device=dev)
-    counts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
-    dist.all_gather(counts, n)
-    counts = [int(c.item()) for c in counts]
-    cap = max(max(counts), 1)
-    pr = torch.zeros(cap * w32, dtype=torch.int32, device=dev)
-    pm = torch.zeros(cap, dtype=torch.int16, device=dev)
-    pr[: count * w32] = rows
-    pm[:count] = maps
-    g_rows = [torch.zeros_like(pr) for _ in range(world)]
-    g_maps = [torch.zeros(cap * 2, dtype=torch.uint8, device=dev) for _ in range(world)]
-    dist.all_gather(g_rows, pr)
-    dist.all_gather(g_maps, pm.view(torch.uint8))  # NCCL has no int16: ship the ids as bytes
+    got = gather_to_rank0(dist, rank, world, [rows, maps], dev)
     if rank != 0:
         return (count, 0, None, None) if return_rows else (count, 0)
-    all_rows = torch.cat([g_rows[r][: counts[r] * w32] for r in range(world)])
-    all_maps = torch.cat([g_maps[r].view(torch.int16)[: counts[r]] for r in range(world)])
-    total = sum(counts)
+    all_rows = torch.cat([g[0] for g in got])
+    all_maps = torch.cat([g[1] for g in got]).view(torch.int16)
+    total = all_maps.numel()
     out_rows = torch.empty_like(all_rows)
     out_maps = torch.empty_like(all_maps)
     torch.cuda.synchronize(dev)
