@@ -261,6 +261,7 @@ struct wpm_plan {
     DevBuf<unsigned long long> d_root_nodes;
     long long root_count = 0;
     int ntasks = 0, frame_cap = 64;
+    int fr_words = 0, rp_words = 0;  // uint16 entries of the fr / rp tables over every map
     bool full_depth = false;
 };
 
@@ -557,8 +558,11 @@ static int plan_build_tables(wpm_plan* P, const std::vector<uint32_t>& foff) {
         r_tot += rcap;
         P->maxM = std::max(P->maxM, M);
     }
-    if (P->d_maps.ensure(K) || P->d_ridges.ensure(r_tot) || P->d_fr.ensure(fr_tot * P->n) ||
-        P->d_rp.ensure(r_tot * WPM_MAX_PARENTS) || P->d_npar.ensure(r_tot) || P->d_tmpi.ensure(K + 1))
+    P->fr_words = (int)(fr_tot * P->n);
+    P->rp_words = (int)(r_tot * std::min(WPM_MAX_PARENTS, P->m - P->n + 1));
+    // fr / rp padded to 16-byte multiples (TS layouts copy them with 16-byte vectors)
+    if (P->d_maps.ensure(K) || P->d_ridges.ensure(r_tot) || P->d_fr.ensure(fr_tot * P->n + 8) ||
+        P->d_rp.ensure(r_tot * WPM_MAX_PARENTS + 8) || P->d_npar.ensure(r_tot) || P->d_tmpi.ensure(K + 1))
         return fail(WPM_EINTERNAL, "device allocation failed (tables)");
     CU(cudaMemcpyAsync(P->d_maps.p, P->desc.data(), K * sizeof(MapDesc), cudaMemcpyHostToDevice, P->stream));
     CU(cudaMemsetAsync(P->d_tmpi.p, 0, (K + 1) * sizeof(int32_t), P->stream));
@@ -848,6 +852,8 @@ static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
     sp.maps = P->d_maps.p;
     sp.fr = P->d_fr.p;
     sp.rp = P->d_rp.p;
+    sp.fr_words = P->fr_words;
+    sp.rp_words = P->rp_words;
     sp.npar = P->d_npar.p;
     sp.qrec = P->d_qrec.p;
     sp.qready = P->d_qready.p;

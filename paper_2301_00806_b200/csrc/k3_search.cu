@@ -73,9 +73,15 @@ constexpr int a16(int x) { return (x + 15) & ~15; }
 // compile-time constant, so each shared access is (warp base register +
 // immediate + index) -- one register for the whole state, no address
 // conversions in the PTX helpers.
-template <int NMAX, int MMAX, int DMAX>
+// TSM: the per-map tables (fr, rp of every map of the plan) are copied into
+// shared memory at kernel start and read with LDS (they are the L1-missing
+// loads of the global-table layout: 20-27 % long-scoreboard stalls); the CTA
+// then holds WPBV warps sharing one copy.  Used when every map's tables fit.
+template <int NMAX, int MMAX, int DMAX, bool TSM = false, int WPBV = 4, int MINBV = 0>
 struct LC {
     static constexpr int kN = NMAX, kM = MMAX, kDepth = DMAX;
+    static constexpr bool TS = TSM;
+    static constexpr int WPB = WPBV;
     static constexpr int NP = a16(NMAX + 32), MP = a16(MMAX + 32);
     static constexpr int NW = (NMAX + 31) / 32, MW = (MMAX + 31) / 32;
     static constexpr int RS = 0;                           // uint8 per ridge: count | undecided << 2
@@ -95,9 +101,9 @@ struct LC {
     // at n = 5 / 6 / 8 over 8 CTAs (64 registers) -- and 8 for the larger
     // shapes, whose shared state caps residency anyway (n = 11: -3 % at 10)
 #ifdef K3_MIN_BLOCKS
-    static constexpr int MIN_BLOCKS = K3_MIN_BLOCKS;
+    static constexpr int MIN_BLOCKS = TSM ? MINBV : K3_MIN_BLOCKS;
 #else
-    static constexpr int MIN_BLOCKS = NMAX <= 720 ? 10 : 8;
+    static constexpr int MIN_BLOCKS = TSM ? MINBV : (NMAX <= 720 ? 10 : 8);
 #endif
 };
 
@@ -113,6 +119,17 @@ using C9 = LC<1152, 440, FRAME_CAP>;
 using C10 = LC<1792, 616, FRAME_CAP>;
 using C11 = LC<2688, 840, FRAME_CAP>;
 using CG = LC<4096, 2048, FRAME_CAP>;     // any universe within the device limits
+// shared-memory-table variants (warps per CTA x CTAs per SM sized so the
+// tables + per-warp state fit 227 KB and the registers 64 K)
+using C5T = LC<128, 128, FRAME_CAP, true, 20, 2>;    // n <= 5: all 35 maps' tables ~70 KB per CTA
+using C6T = LC<232, 136, FRAME_CAP, true, 32, 1>;    // n = 6: ~137 KB
+using C10T = LC<1792, 616, FRAME_CAP, true, 24, 1>;  // n = 10: ~90 KB
+using C11T = LC<2688, 840, FRAME_CAP, true, 24, 1>;  // n = 11: ~48 KB
+// any (m, n) = (15, 11) universe (the synthetic band, up to all 1365 11-subsets)
+using C15 = LC<3008, 1368, FRAME_CAP>;
+using C15T = LC<3008, 1368, FRAME_CAP, true, 18, 1>;
+// (n = 9's seven maps need ~140 KB of tables: 16 warps per SM measured 34 %
+// slower than the global-table layout at 32 -- no TS variant for n = 7..9)
 using CGF = LC<4096, 2048, 2050>;         // full depth: the rerun after a frame overflow
 
 struct MapView {
@@ -120,6 +137,7 @@ struct MapView {
     int lpf_shift;  // lanes per facet in flattened passes: 1 << lpf_shift >= n
     const uint16_t* fr;
     const uint16_t* rp;
+    uint32_t frs, rps;  // the same tables in shared memory (TS layouts)
     int fs, ps;     // strides of fr (= n) and rp (<= 8, 0xFFFF padded)
 };
 
@@ -156,6 +174,29 @@ struct WS {
 };
 
 __device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) - 1u; }
+
+// per-map table reads: the k-th ridge of a facet (fr), the q-th candidate
+// facet of a ridge (rp); LDS for the shared-memory layouts, LDG otherwise
+template <class C>
+__device__ __forceinline__ int ldfr(const MapView& mp, int i) {
+    if constexpr (C::TS) {
+        unsigned short v;
+        asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(mp.frs + 2u * (unsigned)i));
+        return v;
+    } else {
+        return __ldg(mp.fr + i);
+    }
+}
+template <class C>
+__device__ __forceinline__ int ldrp(const MapView& mp, int i) {
+    if constexpr (C::TS) {
+        unsigned short v;
+        asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(mp.rps + 2u * (unsigned)i));
+        return v;
+    } else {
+        return __ldg(mp.rp + i);
+    }
+}
 
 // Predicated shared-memory updates: one instruction each, no branch, so the
 // warp never diverges around them (a C++ `if (cond) atomicXor(...)` costs a
@@ -213,7 +254,7 @@ __device__ __forceinline__ void apply_exclusions(WS<C>& w, const MapView& mp, in
         const int e = e0 + (lane >> sh_l);
         const bool act = e < hi && k < mp.n;
         const int g = act ? (w.trail()[e] & 0x7FFF) : 0;
-        const int r = act ? __ldg(mp.fr + g * mp.fs + k) : 0;
+        const int r = act ? ldfr<C>(mp, g * mp.fs + k) : 0;
         const unsigned sh = (r & 3) * 8;
         const unsigned ob = (atom_add_if(w.a_rs_word(r), 0u - (4u << sh), act) >> sh) & 0xFFu;
         // (1,1) -> (1,0): dead and leaves the forced set; (1,2) -> (1,1): enters it
@@ -228,7 +269,7 @@ __device__ __forceinline__ void exclude_one(WS<C>& w, const MapView& mp, int g, 
     st_u8_if(w.a_fst(g), FOUT, lane == 0);
     st_u16_if(w.a_trail(w.tl), (uint32_t)g, lane == 0);
     const bool act = lane < mp.n;
-    const int r = act ? __ldg(mp.fr + g * mp.fs + lane) : 0;
+    const int r = act ? ldfr<C>(mp, g * mp.fs + lane) : 0;
     const unsigned sh = (r & 3) * 8;
     const unsigned ob = (atom_add_if(w.a_rs_word(r), 0u - (4u << sh), act) >> sh) & 0xFFu;
     red_xor_if(w.a_b1(r), 1u << (r & 31), act && (ob == 5u || ob == 9u));
@@ -252,7 +293,7 @@ template <class C>
 __device__ __forceinline__ Probe probe_facet(const WS<C>& w, const MapView& mp, int f, int lane) {
     Probe pr{0, 4u, false};
     if (lane < mp.n) {
-        pr.r = __ldg(mp.fr + f * mp.fs + lane);
+        pr.r = ldfr<C>(mp, f * mp.fs + lane);
         pr.b = w.rs()[pr.r];
     }
     pr.dead = __any_sync(FULL, pr.b == (1u << 2) && lane < mp.n);
@@ -293,7 +334,7 @@ __device__ __forceinline__ void include_facet(WS<C>& w, const MapView& mp, int f
         const int j = j0 + (lane >> 3), q = lane & 7;
         const bool slot = j < ncl && q < mp.ps;
         const int rr = w.scratch()[j & 31];
-        const int g0 = slot ? (int)__ldg(mp.rp + rr * mp.ps + q) : (int)NONE16;
+        const int g0 = slot ? ldrp<C>(mp, rr * mp.ps + q) : (int)NONE16;
         const int g = g0 == NONE16 ? 0 : g0;
         const bool v = g0 != NONE16 && w.fst()[g] == FU;
         const unsigned bv = __ballot_sync(FULL, v);
@@ -339,7 +380,7 @@ __device__ __forceinline__ void undo_to(WS<C>& w, const MapView& mp, int mark, i
         const bool act = e < hi && k < mp.n;
         const unsigned t = act ? (unsigned)w.trail()[e] : 0u;
         const int g = (int)(t & 0x7FFFu);
-        const int r = act ? __ldg(mp.fr + g * mp.fs + k) : 0;
+        const int r = act ? ldfr<C>(mp, g * mp.fs + k) : 0;
         const unsigned delta = (t & TR_INC) ? 3u : 4u;  // (c-1, a+1) or (a+1)
         const unsigned sh = (r & 3) * 8;
         const unsigned ob = (atom_add_if(w.a_rs_word(r), delta << sh, act) >> sh) & 0xFFu;
@@ -365,7 +406,7 @@ __device__ void debug_check(const WS<C>& w, const MapView& mp, int lane, int whe
     for (int r = lane; r < mp.N; r += 32) {
         unsigned c = 0, a = 0;
         for (int q = 0; q < mp.ps; ++q) {
-            const int g = __ldg(mp.rp + r * mp.ps + q);
+            const int g = ldrp<C>(mp, r * mp.ps + q);
             if (g == NONE16) continue;
             c += w.fst()[g] == FIN;
             a += w.fst()[g] == FU;
@@ -433,7 +474,7 @@ template <class C>
 __device__ __forceinline__ int first_candidate(const WS<C>& w, const MapView& mp, int ridge, int pos, int* slot,
                                                int lane) {
     const bool in_range = lane >= pos && lane < mp.ps;
-    const int g0 = in_range ? (int)__ldg(mp.rp + ridge * mp.ps + lane) : (int)NONE16;
+    const int g0 = in_range ? ldrp<C>(mp, ridge * mp.ps + lane) : (int)NONE16;
     const int g = g0 == NONE16 ? 0 : g0;
     const bool ok = g0 != NONE16 && w.fst()[g] == FU;
     const unsigned b = __ballot_sync(FULL, ok);
@@ -585,7 +626,7 @@ __device__ __forceinline__ bool load_state(WS<C>& w, const MapView& mp, const ui
         for (int r = lane; r < N; r += 32) {
             unsigned c = 0;
             for (int q = 0; q < mp.ps; ++q) {
-                const int g = __ldg(mp.rp + r * mp.ps + q);
+                const int g = ldrp<C>(mp, r * mp.ps + q);
                 c += g != NONE16 && fst[g] == FIN;
             }
             bad |= c > 2u;
@@ -597,7 +638,7 @@ __device__ __forceinline__ bool load_state(WS<C>& w, const MapView& mp, const ui
         for (int f = lane; f < M; f += 32) {
             if (fst[f] != FU) continue;
             bool on_closed = false;
-            for (int k = 0; k < mp.n; ++k) on_closed |= rs[__ldg(mp.fr + f * mp.fs + k)] == 2u;
+            for (int k = 0; k < mp.n; ++k) on_closed |= rs[ldfr<C>(mp, f * mp.fs + k)] == 2u;
             if (on_closed) fst[f] = FOUT;
         }
         __syncwarp();
@@ -611,7 +652,7 @@ __device__ __forceinline__ bool load_state(WS<C>& w, const MapView& mp, const ui
         if (r < N) {
             unsigned a = 0, ci = 0;
             for (int q = 0; q < mp.ps; ++q) {
-                const int g0 = __ldg(mp.rp + r * mp.ps + q);
+                const int g0 = ldrp<C>(mp, r * mp.ps + q);
                 const unsigned s = g0 != NONE16 ? fst[g0] : (unsigned)FOUT;
                 a += s == FU;
                 ci += s == FIN;
@@ -669,7 +710,7 @@ __device__ __forceinline__ bool try_donate(WS<C>& w, const MapView& mp, const Se
         } else {
             bool ok = false;
             if (lane >= (int)pos && lane < mp.ps) {
-                const int g = __ldg(mp.rp + ridge * mp.ps + lane);
+                const int g = ldrp<C>(mp, ridge * mp.ps + lane);
                 ok = g != NONE16 && g != cur && (fst[g] == FU || ((late[g >> 5] >> (g & 31)) & 1u));
             }
             any = __any_sync(FULL, ok);
@@ -718,11 +759,25 @@ __device__ __forceinline__ bool try_donate(WS<C>& w, const MapView& mp, const Se
 }
 
 template <class C>
-__global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_constant__ SearchParams p) {
+__global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __grid_constant__ SearchParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // TS layouts: every map's fr then rp tables at the CTA's base, then the warps
+    const int tab_bytes = C::TS ? ((2 * (p.fr_words + p.rp_words) + 15) & ~15) : 0;
+    if constexpr (C::TS) {
+        const uint4* src_fr = reinterpret_cast<const uint4*>(p.fr);
+        const uint4* src_rp = reinterpret_cast<const uint4*>(p.rp);
+        uint4* dfr = reinterpret_cast<uint4*>(smem);
+        const int nfr = (p.fr_words + 7) >> 3, nrp = (p.rp_words + 7) >> 3;
+        uint4* drp = reinterpret_cast<uint4*>(smem + 16 * nfr);
+        for (int i = threadIdx.x; i < nfr; i += blockDim.x) dfr[i] = __ldg(src_fr + i);
+        for (int i = threadIdx.x; i < nrp; i += blockDim.x) drp[i] = __ldg(src_rp + i);
+        __syncthreads();
+    }
+    const uint32_t tab_s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    const uint32_t rp_s = tab_s + 16u * (uint32_t)((p.fr_words + 7) >> 3);
     WS<C> w;
-    w.base = smem + wid * C::BYTES;
+    w.base = smem + tab_bytes + wid * C::BYTES;
     w.sb = static_cast<uint32_t>(__cvta_generic_to_shared(w.base));
     unsigned long long nodes = 0, tasks = 0;
 #ifdef WPM_PROFILE
@@ -749,7 +804,21 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
                 volatile unsigned long long* rdy = p.qready + (tk % (unsigned long long)p.qcap);
                 volatile unsigned long long* pend = p.qctl + 2;
                 unsigned backoff = (unsigned)p.backoff_min;
-                for (;;) {
+                if (exhausted) {  // no shared frontier to claim from: the tight ticket wait
+                    for (;;) {
+                        if (*rdy == tk + 1ull) {
+                            t = (long long)tk;
+                            break;
+                        }
+                        if (*pend == 0ull || (p.node_budget && ld_relaxed_u64(&p.out_ctl[3]))) {
+                            t = -2;  // no task left anywhere, or the node budget is spent
+                            break;
+                        }
+                        __nanosleep(backoff);
+                        backoff = min(backoff * 2u, (unsigned)p.backoff_max);
+                    }
+                }
+                while (t == -1) {
                     if (*rdy == tk + 1ull) {
                         t = (long long)tk;
                         break;
@@ -834,6 +903,8 @@ __global__ void __launch_bounds__(128, C::MIN_BLOCKS) k3_search(const __grid_con
         mp.lpf_shift = md.n <= 4 ? 2 : (md.n <= 8 ? 3 : 4);
         mp.fr = p.fr + md.fr_off;
         mp.rp = p.rp + md.rp_off;
+        mp.frs = tab_s + 2u * md.fr_off;
+        mp.rps = rp_s + 2u * md.rp_off;
         mp.fs = md.fr_stride;
         mp.ps = md.rp_stride;
         ++tasks;
@@ -1009,8 +1080,9 @@ __global__ void seed_records(SearchParams p, const uint32_t* __restrict__ recs, 
 
 template <class C>
 int launch_class(const SearchParams& p, int num_sms, cudaStream_t st, int* warps_out) {
-    const int wpb = 4;  // warps per CTA
-    const size_t smem = (size_t)C::BYTES * wpb;
+    const int wpb = C::WPB;  // warps per CTA
+    const size_t tab = C::TS ? (size_t)((2 * (p.fr_words + p.rp_words) + 15) & ~15) : 0;
+    const size_t smem = tab + (size_t)C::BYTES * wpb;
     if (cudaFuncSetAttribute(k3_search<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return 0;
     // experiment knob: the L1 / shared split (percent of the max shared carveout)
@@ -1057,11 +1129,32 @@ int launch_seed_records(const SearchParams& p, const uint32_t* d_recs, long long
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+// a TS layout fits if its CTAs (tables + warps) fit the SM's shared memory
+template <class C>
+bool ts_fits(const SearchParams& p) {
+    const size_t tab = (size_t)((2 * (p.fr_words + p.rp_words) + 15) & ~15);
+    return (size_t)C::MIN_BLOCKS * (tab + (size_t)C::BYTES * C::WPB) <= 227u * 1024u;
+}
+
 // the smallest size class that holds the plan (max_depth > FRAME_CAP asks for
-// the full-depth layout)
+// the full-depth layout); the shared-memory-table variant when it fits
+// (WPM_TS=0 disables it)
 int launch_k3_search(const SearchParams& p, int num_sms, cudaStream_t st, int* warps_out) {
     const int N = p.max_N, M = p.max_M;
     if (p.max_depth > FRAME_CAP) return launch_class<CGF>(p, num_sms, st, warps_out);
+    const char* ts_env = std::getenv("WPM_TS");
+    const bool ts_on = !ts_env || std::atoi(ts_env) != 0;
+    if (ts_on) {
+        if (N <= C5T::kN && M <= C5T::kM && ts_fits<C5T>(p)) return launch_class<C5T>(p, num_sms, st, warps_out);
+        if (N <= C6T::kN && M <= C6T::kM && N > C5T::kN && ts_fits<C6T>(p))
+            return launch_class<C6T>(p, num_sms, st, warps_out);
+        if (N <= C10T::kN && M <= C10T::kM && N > C9::kN && ts_fits<C10T>(p))
+            return launch_class<C10T>(p, num_sms, st, warps_out);
+        if (N <= C11T::kN && M <= C11T::kM && N > C10::kN && ts_fits<C11T>(p))
+            return launch_class<C11T>(p, num_sms, st, warps_out);
+        if (N <= C15T::kN && M <= C15T::kM && (N > C11::kN || M > C11::kM) && ts_fits<C15T>(p))
+            return launch_class<C15T>(p, num_sms, st, warps_out);
+    }
     if (N <= C5::kN && M <= C5::kM) return launch_class<C5>(p, num_sms, st, warps_out);
     if (N <= C6::kN && M <= C6::kM) return launch_class<C6>(p, num_sms, st, warps_out);
     if (N <= C7::kN && M <= C7::kM) return launch_class<C7>(p, num_sms, st, warps_out);
@@ -1069,6 +1162,7 @@ int launch_k3_search(const SearchParams& p, int num_sms, cudaStream_t st, int* w
     if (N <= C9::kN && M <= C9::kM) return launch_class<C9>(p, num_sms, st, warps_out);
     if (N <= C10::kN && M <= C10::kM) return launch_class<C10>(p, num_sms, st, warps_out);
     if (N <= C11::kN && M <= C11::kM) return launch_class<C11>(p, num_sms, st, warps_out);
+    if (N <= C15::kN && M <= C15::kM) return launch_class<C15>(p, num_sms, st, warps_out);
     return launch_class<CG>(p, num_sms, st, warps_out);
 }
 

@@ -25,6 +25,7 @@ struct SearchParams {
     const uint16_t* fr;
     const uint16_t* rp;
     const uint8_t* npar;  // host-side parity hook only
+    int fr_words, rp_words;  // uint16 entries of fr / rp over every map (16-byte padded arrays)
     // work queue
     uint32_t* qrec;
     unsigned long long* qready;
