@@ -961,6 +961,7 @@ static void root_tasks(const wpm_plan* P, int shard_index, int shard_count, std:
 
 // allocations, root tasks on the device, output sizing
 static int search_prepare(wpm_plan* P, int shard_index, int shard_count) {
+    Trace tr;
     const int K = P->num_maps;
     std::vector<int32_t> tm, tf, tk;
     root_tasks(P, shard_index, shard_count, &tm, &tf, &tk);
@@ -976,6 +977,7 @@ static int search_prepare(wpm_plan* P, int shard_index, int shard_count) {
         CU(cudaMemcpyAsync(P->d_pin_in.p, P->pin_in.data(), P->mw * 4, cudaMemcpyHostToDevice, P->stream));
         CU(cudaMemcpyAsync(P->d_pin_out.p, P->pin_out.data(), P->mw * 4, cudaMemcpyHostToDevice, P->stream));
     }
+    tr.mark("    prepare: small buffers");
     if (ntasks) {
         CU(cudaMemcpyAsync(P->d_task_map.p, tm.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
         CU(cudaMemcpyAsync(P->d_task_f.p, tf.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
@@ -984,15 +986,13 @@ static int search_prepare(wpm_plan* P, int shard_index, int shard_count) {
     }
     if (P->out_cap == 0) {
         // first run: 2^21 rows covers every Picard-4 n (the most WPMs of any
-        // n is 1.72 M, n = 8); a larger result reruns once with the exact
-        // count.  (Sizing from free memory asked the pool for GBs per plan,
-        // and a pool that had to map them again cost tens of ms per call.)
-        size_t fr = 0, tot = 0;
-        cudaMemGetInfo(&fr, &tot);
-        const unsigned long long row = (unsigned long long)P->rw * 4 * 3;  // keys + sort temp + sorted rows
-        P->out_cap = std::min<unsigned long long>(std::max<unsigned long long>(fr / 16 / row, 1ull << 16), 1ull << 21);
+        // n is 1.72 M, n = 8; <= 512 MB at the widest rows); a larger result
+        // reruns once with the exact count.  (Sizing from free memory asked
+        // the pool for GBs per plan, and cudaMemGetInfo cost 0.1 ms per call.)
+        P->out_cap = 1ull << 21;
         if (const char* e = std::getenv("WPM_OUT_CAP")) P->out_cap = std::max(1ull, std::strtoull(e, nullptr, 10));
     }
+    tr.mark("    prepare: out_cap");
     if (P->front_cap == 0) P->front_cap = 1ull << 16;
     // frame stack sized for the branch depths the search reaches in practice
     // (<= 37 measured up to n = 11); a run that outgrows it is redone with
@@ -1005,7 +1005,9 @@ static int search_prepare(wpm_plan* P, int shard_index, int shard_count) {
 
 // start of an attempt: empty outputs and counters, start event
 static int search_reset(wpm_plan* P) {
+    Trace tr;
     if (P->d_out_keys.ensure(P->out_cap * P->rw)) return fail(WPM_EINTERNAL, "device allocation failed (output)");
+    tr.mark("    reset: output buffer");
     CU(cudaMemsetAsync(P->d_out_ctl.p, 0, 32, P->stream));
     CU(cudaMemsetAsync(P->d_acc.p, 0, 32, P->stream));
     CU(cudaMemsetAsync(P->d_qctl.p, 0, 64, P->stream));

@@ -181,7 +181,8 @@ template <class C>
 __device__ __forceinline__ int ldfr(const MapView& mp, int i) {
     if constexpr (C::TS) {
         unsigned short v;
-        asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(mp.frs + 2u * (unsigned)i));
+        // volatile: never speculated -- callers guard out-of-range indices
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(mp.frs + 2u * (unsigned)i));
         return v;
     } else {
         return __ldg(mp.fr + i);
@@ -191,7 +192,7 @@ template <class C>
 __device__ __forceinline__ int ldrp(const MapView& mp, int i) {
     if constexpr (C::TS) {
         unsigned short v;
-        asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(mp.rps + 2u * (unsigned)i));
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(mp.rps + 2u * (unsigned)i));
         return v;
     } else {
         return __ldg(mp.rp + i);
@@ -517,6 +518,7 @@ __device__ __forceinline__ void emit(const WS<C>& w, const MapView& mp, const Se
     if (slot < p.out_cap) {  // key row: bitset words, zero padded, then the map id
         uint32_t* o = p.out_keys + slot * (unsigned long long)p.rw;
         const int mw = (mp.M + 31) >> 5, last = p.rw - 1;
+        #pragma unroll 1
         for (int i = lane; i < p.rw; i += 32) o[i] = i < mw ? w.inb()[i] : (i == last ? (uint32_t)mp.map : 0u);
     }
 }
@@ -538,6 +540,7 @@ __device__ __forceinline__ void write_frontier(const WS<C>& w, const MapView& mp
         rec[3] = w.root();
     }
     const int mw = (mp.M + 31) >> 5;
+    #pragma unroll 1
     for (int f0 = 0; f0 < mw * 32; f0 += 32) {
         const int f = f0 + lane;
         const uint8_t st = f < mp.M ? w.fst()[f] : (uint8_t)FU;
@@ -606,11 +609,13 @@ __device__ __forceinline__ bool load_state(WS<C>& w, const MapView& mp, const ui
     uint8_t* rs = w.rs();
     uint8_t* fst = w.fst();
     int size = 0;
+    #pragma unroll 1
     for (int i = lane; i < mw; i += 32) {
         const uint32_t iv = __ldcg(rec_in + i);
         w.inb()[i] = iv;
         size += __popc(iv);
     }
+    #pragma unroll 1
     for (int f0 = 0; f0 < M; f0 += 32) {
         const int f = f0 + lane;
         const uint32_t iv = __ldcg(rec_in + (f0 >> 5)), ov = __ldcg(rec_out + (f0 >> 5));
@@ -623,8 +628,10 @@ __device__ __forceinline__ bool load_state(WS<C>& w, const MapView& mp, const ui
     if (closure) {
         // pass 1: IN counts; a count >= 3 is infeasible
         bool bad = false;
+        #pragma unroll 1
         for (int r = lane; r < N; r += 32) {
             unsigned c = 0;
+            #pragma unroll 1
             for (int q = 0; q < mp.ps; ++q) {
                 const int g = ldrp<C>(mp, r * mp.ps + q);
                 c += g != NONE16 && fst[g] == FIN;
@@ -635,9 +642,11 @@ __device__ __forceinline__ bool load_state(WS<C>& w, const MapView& mp, const ui
         if (__any_sync(FULL, bad)) return false;
         __syncwarp();
         // closure: undecided facets on a closed ridge are excluded
+        #pragma unroll 1
         for (int f = lane; f < M; f += 32) {
             if (fst[f] != FU) continue;
             bool on_closed = false;
+            #pragma unroll 1
             for (int k = 0; k < mp.n; ++k) on_closed |= rs[ldfr<C>(mp, f * mp.fs + k)] == 2u;
             if (on_closed) fst[f] = FOUT;
         }
@@ -646,11 +655,13 @@ __device__ __forceinline__ bool load_state(WS<C>& w, const MapView& mp, const ui
     // pass 2 (the only pass for states produced by the search itself, which
     // are closed already): counts, open / b1 bitsets, open / dead tallies
     int nopen = 0, ndead = 0;
+    #pragma unroll 1
     for (int r0 = 0; r0 < nw * 32; r0 += 32) {
         const int r = r0 + lane;
         bool op = false, dd = false, one = false;
         if (r < N) {
             unsigned a = 0, ci = 0;
+            #pragma unroll 1
             for (int q = 0; q < mp.ps; ++q) {
                 const int g0 = ldrp<C>(mp, r * mp.ps + q);
                 const unsigned s = g0 != NONE16 ? fst[g0] : (unsigned)FOUT;
@@ -687,6 +698,7 @@ __device__ __forceinline__ bool try_donate(WS<C>& w, const MapView& mp, const Se
     const int M = mp.M, mw = (M + 31) >> 5;
     uint32_t* late = w.late();
     const uint8_t* fst = w.fst();
+    #pragma unroll 1
     for (int d = 0; d < w.depth; ++d) {
         const uint2 fr = w.frames()[d];
         const uint32_t ridge = fr.x & 0xFFFFu, pos = fr.x >> 16;
@@ -694,8 +706,10 @@ __device__ __forceinline__ bool try_donate(WS<C>& w, const MapView& mp, const Se
         const bool busy = (fr.y & 0xFFFFu) != NO_CHILD && d + 1 < w.depth;
         const int mk = busy ? (int)(fr.y >> 16) : w.tl;  // the frame's own state
         const int cur = busy ? (int)(fr.y & 0xFFFFu) : -1;
+        #pragma unroll 1
         for (int i = lane; i < mw; i += 32) late[i] = 0u;
         __syncwarp();
+        #pragma unroll 1
         for (int e = mk + lane; e < w.tl; e += 32) {
             const int g = w.trail()[e] & 0x7FFF;
             atomicOr(&late[g >> 5], 1u << (g & 31));
@@ -703,6 +717,7 @@ __device__ __forceinline__ bool try_donate(WS<C>& w, const MapView& mp, const Se
         __syncwarp();
         bool any = false;
         if (ridge == CLOSED_FRAME) {
+            #pragma unroll 1
             for (int f0 = (int)pos; f0 < M && !any; f0 += 32) {
                 const int f = f0 + lane;
                 any = __any_sync(FULL, f < M && f != cur && (fst[f] == FU || ((late[f >> 5] >> (f & 31)) & 1u)));
@@ -731,6 +746,7 @@ __device__ __forceinline__ bool try_donate(WS<C>& w, const MapView& mp, const Se
             rec[2] = pos | ((uint32_t)(w.dbase() + d) << 16);
             rec[3] = w.root();
         }
+        #pragma unroll 1
         for (int f0 = 0; f0 < mw * 32; f0 += 32) {
             const int f = f0 + lane;
             bool in = false, out = false;
@@ -763,7 +779,7 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     // TS layouts: every map's fr then rp tables at the CTA's base, then the warps
-    const int tab_bytes = C::TS ? ((2 * (p.fr_words + p.rp_words) + 15) & ~15) : 0;
+    const int tab_bytes = C::TS ? 16 * (((p.fr_words + 7) >> 3) + ((p.rp_words + 7) >> 3)) : 0;
     if constexpr (C::TS) {
         const uint4* src_fr = reinterpret_cast<const uint4*>(p.fr);
         const uint4* src_rp = reinterpret_cast<const uint4*>(p.rp);
@@ -1081,7 +1097,8 @@ __global__ void seed_records(SearchParams p, const uint32_t* __restrict__ recs, 
 template <class C>
 int launch_class(const SearchParams& p, int num_sms, cudaStream_t st, int* warps_out) {
     const int wpb = C::WPB;  // warps per CTA
-    const size_t tab = C::TS ? (size_t)((2 * (p.fr_words + p.rp_words) + 15) & ~15) : 0;
+    // fr and rp each padded to 16 bytes (the kernel's layout)
+    const size_t tab = C::TS ? (size_t)16 * (((p.fr_words + 7) >> 3) + ((p.rp_words + 7) >> 3)) : 0;
     const size_t smem = tab + (size_t)C::BYTES * wpb;
     if (cudaFuncSetAttribute(k3_search<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return 0;
@@ -1132,7 +1149,7 @@ int launch_seed_records(const SearchParams& p, const uint32_t* d_recs, long long
 // a TS layout fits if its CTAs (tables + warps) fit the SM's shared memory
 template <class C>
 bool ts_fits(const SearchParams& p) {
-    const size_t tab = (size_t)((2 * (p.fr_words + p.rp_words) + 15) & ~15);
+    const size_t tab = (size_t)16 * (((p.fr_words + 7) >> 3) + ((p.rp_words + 7) >> 3));
     return (size_t)C::MIN_BLOCKS * (tab + (size_t)C::BYTES * C::WPB) <= 227u * 1024u;
 }
 

@@ -1,6 +1,7 @@
 """Summarise an ncu report / launch list into profiles/ (dev tool).
 
-usage: python tools/ncu_summary.py REPORT.ncu-rep NODES OUT.txt
+usage: python tools/ncu_summary.py REPORT.ncu-rep UNITS OUT.txt [UNIT_NAME]
+       (UNITS = work units in the launch, e.g. search nodes; 0 = per launch)
        python tools/ncu_summary.py --launches launches.csv STEPS OUT.txt
 """
 import collections
@@ -18,6 +19,10 @@ KEYS = [
     "l1tex__throughput.avg.pct_of_peak_sustained_active", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
     "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread", "launch__grid_size",
     "launch__block_size", "sm__maximum_warps_per_active_cycle_pct",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+    "sm__warps_active.avg.per_cycle_active", "smsp__warps_eligible.avg.per_cycle_active",
+    "launch__shared_mem_per_block_dynamic", "launch__occupancy_limit_registers",
+    "launch__occupancy_limit_shared_mem",
 ]
 
 
@@ -25,7 +30,7 @@ def ncu_csv(args):
     return subprocess.run(["ncu"] + args, capture_output=True, text=True).stdout
 
 
-def report(rep, nodes, out):
+def report(rep, nodes, out, unit="search node"):
     raw = list(csv.reader(io.StringIO(ncu_csv(["-i", rep, "--page", "raw", "--csv"]))))
     hdr, units, vals = raw[0], raw[1], raw[2]
     lines = [f"ncu --set full summary of {rep} (kernel: {vals[hdr.index('Kernel Name')]})", ""]
@@ -37,9 +42,13 @@ def report(rep, nodes, out):
     inst = float(d.get("smsp__inst_executed.sum", "0").replace(",", ""))
     dur = float(d.get("gpu__time_duration.sum", "0").replace(",", ""))
     lines.append("")
-    lines.append(f"search nodes in this launch            {nodes}")
-    lines.append(f"warp instructions per node             {inst / nodes:.1f}")
-    lines.append(f"nodes/s in this (profiled) launch      {nodes / (dur * 1e-3):.3e}  (ncu replay: not a bench number)")
+    if nodes:
+        lines.append(f"{unit}s in this launch{'':<10s} {nodes}")
+        lines.append(f"warp instructions per {unit:<14s} {inst / nodes:.1f}")
+        lines.append(f"{unit}s/s in this (profiled) launch {nodes / (dur * 1e-3):.3e}  (ncu replay: not a bench number)")
+    else:
+        nodes = 1
+        unit = "launch"
     st = [(h, v) for h, v in zip(hdr, vals) if h.startswith("smsp__pcsamp_warps_issue_stalled_") and
           not h.endswith("not_issued")]
     tot = sum(float(v or 0) for _, v in st)
@@ -60,7 +69,7 @@ def report(rep, nodes, out):
                 except ValueError:
                     pass
         lines.append("")
-        lines.append("top CUDA source lines by warp instructions executed (per node):")
+        lines.append(f"top CUDA source lines by warp instructions executed (per {unit}):")
         for c, ln, s in sorted(agg, reverse=True)[:25]:
             lines.append(f"  {c / nodes:7.1f}  L{ln:<5d} {s}")
     open(out, "w").write("\n".join(lines) + "\n")
@@ -93,4 +102,4 @@ if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         launches(sys.argv[2], int(sys.argv[3]), sys.argv[4])
     else:
-        report(sys.argv[1], int(sys.argv[2]), sys.argv[3])
+        report(sys.argv[1], int(sys.argv[2]), sys.argv[3], *(sys.argv[4:5] or ["search node"]))
