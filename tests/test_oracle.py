@@ -317,3 +317,36 @@ def test_write_complexes_format(wpm):
     """complex_io.hpp:21-39 byte format."""
     s = wpm.write_complexes(6, 2, [[0b0110, 0b1010, 0b1100], [0b0110]])
     assert s == "6 2\n1 2\n1 3\n2 3\n\n6 2\n1 2\n"
+
+
+def test_charmap_of_dcm_general_branch(wpm, oracle):
+    """charmap_of_dcm's general kernel branch (charmap.hpp:171-203), taken when
+    the last p rows are not the identity: the product's host code equals the
+    restatement on row-permuted orbit representatives and on random rank-p
+    dual matrices; rank-deficient inputs are rejected by both."""
+    import random
+
+    rng = random.Random(4)
+    checked = 0
+    for n in (2, 3, 5, 7):
+        for d in wpm.idcm_orbits(n, 4)[:6]:
+            rows = list(d.rows)
+            rng.shuffle(rows)
+            if rows[-4:] == [1, 2, 4, 8]:
+                continue
+            dd = wpm.DualCharMatrix(d.m, 4, rows)
+            assert wpm.charmap_of_dcm(dd) == oracle.charmap_of_dcm(rows), (n, rows)
+            checked += 1
+    for _ in range(200):
+        m = rng.randrange(6, 14)
+        rows = [rng.randrange(1, 16) for _ in range(m)]
+        dd = wpm.DualCharMatrix(m, 4, rows)
+        try:
+            want = oracle.charmap_of_dcm(rows)
+        except ValueError:
+            with pytest.raises(ValueError):
+                wpm.charmap_of_dcm(dd)
+            continue
+        assert wpm.charmap_of_dcm(dd) == want, rows
+        checked += 1
+    assert checked > 100
