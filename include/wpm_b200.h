@@ -195,7 +195,7 @@ int wpm_plan_device_result(const wpm_plan_t *plan, const uint32_t **bits32, cons
  * parallel_for_index, parallel.hpp:27-54, becomes GPUs): devices[0] must be
  * the plan's device; the others get plans of the same maps.  wpm_plan_run
  * then splits the search tree below the root on devices[0] (split rounds
- * until the frontier has >= 2048 records per GPU), copies the frontier to
+ * until the frontier has >= 640 records per GPU), copies the frontier to
  * every GPU, and each GPU's kernel 3 pulls records through one claim counter
  * in devices[0]'s HBM (peer atomics over NVLink) and shares them further by
  * donation; the rows are gathered into devices[0] (peer copies) and sorted

@@ -14,6 +14,7 @@
 #include <mutex>
 #include <unordered_map>
 #include <chrono>
+#include <cmath>
 #include <functional>
 #include <cstdlib>
 #include <climits>
@@ -1225,8 +1226,12 @@ int split_rounds(wpm_plan* P, int depth, long long target) {
     if (rc) return rc;
     for (int round = 1; round < 8; ++round) {
         if ((unsigned long long)P->frontier > P->front_cap) return WPM_OK;  // caller reruns with room
-        if (P->frontier >= target || P->frontier == 0) return WPM_OK;
-        depth += 2;
+        // within 2x of the target is enough (a round costs ~0.5-1.5 ms)
+        if (2 * P->frontier >= target || P->frontier == 0) return WPM_OK;
+        // deep enough in one more round: the frontier grows ~1.7x per branch
+        // level (measured 1.6-1.9x at n = 8 and 11, tools/split_sim.c)
+        int jump = (int)std::ceil(std::log((double)target / (double)P->frontier) / std::log(1.7));
+        depth += std::max(1, std::min(jump, 8));
         if (P->d_front2.ensure(P->front_cap * P->recw)) return fail(WPM_EINTERNAL, "allocation failed (frontier)");
         P->d_front.swap(P->d_front2);  // the current frontier seeds the next round
         CU(cudaMemsetAsync(P->d_front_ctl.p, 0, 16, P->stream));
@@ -1259,10 +1264,13 @@ int enable_peer(int dev, int leader) {
     return WPM_OK;
 }
 
-// frontier target: enough records that dynamic claims balance the GPUs
-// (2048 per GPU; the largest record is then ~0.2-0.3 % of the work at n = 8
-// and 11); the split depth grows two levels per round until then
-long long frontier_target(int ndev) { return std::max<long long>(2048, 2048LL * ndev); }
+// frontier target: 640 records per GPU (>= 2048).  Enough that the GPUs
+// balance (largest record <= ~0.3 % of the work at n = 8 and 11; static
+// max/mean of 5 k records over 8 GPUs 1.05-1.08), few enough that the
+// per-record cost stays invisible (1 GPU, n = 11: the claim phase over 5 k
+// records = the direct run, over 12.7 k +28 %, tools/gpu/split_probe.py).
+// The first split is at depth 5, then one jump to the target depth.
+long long frontier_target(int ndev) { return std::max<long long>(2048, 640LL * ndev); }
 
 }  // namespace
 
@@ -1289,7 +1297,7 @@ static int plan_run_multi(wpm_plan* P) {
         CU(cudaSetDevice(P->device));
         g_alloc_stream = P->stream;
         if ((rc = search_reset(P))) return rc;
-        if ((rc = split_rounds(P, P->split_depth > 0 ? P->split_depth : 3, frontier_target(W)))) return rc;
+        if ((rc = split_rounds(P, P->split_depth > 0 ? P->split_depth : 5, frontier_target(W)))) return rc;
         if ((unsigned long long)P->frontier > P->front_cap) {
             P->front_cap = (unsigned long long)P->frontier + (unsigned long long)P->frontier / 4 + 1024;
             ++P->reruns;
@@ -1460,7 +1468,7 @@ extern "C" int wpm_plan_split(wpm_plan_t* P, int32_t depth, int64_t target, int6
     CU(cudaEventRecord(P->ev[4], P->stream));
     for (int attempt = 0; attempt < 3; ++attempt) {
         if ((rc = search_reset(P))) return rc;
-        if ((rc = split_rounds(P, depth > 0 ? depth : 3, target > 0 ? target : frontier_target(1)))) return rc;
+        if ((rc = split_rounds(P, depth > 0 ? depth : 5, target > 0 ? target : frontier_target(1)))) return rc;
         if ((unsigned long long)P->frontier <= P->front_cap) break;
         P->front_cap = (unsigned long long)P->frontier + (unsigned long long)P->frontier / 4 + 1024;
     }

@@ -3,7 +3,7 @@
 The job (parallel_for_index, parallel.hpp:27-54, across GPUs):
 
   1. rank 0 splits the search tree below the root (Plan.split: split-mode
-     kernel-3 launches until the frontier has >= 2048 records per GPU; the
+     kernel-3 launches until the frontier has >= 640 records per GPU; the
      rows and nodes above the frontier stay on rank 0);
   2. the frontier records are broadcast (NCCL) and a claim counter in rank
      0's HBM is shared through a CUDA IPC handle;
@@ -171,7 +171,7 @@ def run_job(dist, plan, rank: int, world: int, device: int, counter=None, target
 
     dev = torch.device("cuda", device)
     if world == 1:
-        plan.split(3, target or 1024)
+        plan.split(5, target or 2048)
         own = counter is None
         ctr = wpm.claim_counter_create(device)[0] if own else counter[0]
         if not own:
@@ -182,7 +182,7 @@ def run_job(dist, plan, rank: int, world: int, device: int, counter=None, target
             if own:
                 wpm.claim_counter_close(device, ctr, False)
     if rank == 0:
-        plan.split(3, target or 2048 * world)
+        plan.split(5, target or 640 * world)
         ptr, count, recw = plan.frontier()
         recs = _wrap_device(ptr, count * recw, torch.int32, dev)
         wpm.claim_counter_reset(device, counter[0])
