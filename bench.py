@@ -593,8 +593,10 @@ def e2e_dropin(n, dev):
 def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)), max_w=8):
     """1-GPU PROJECTION of the multi-GPU job (labelled as such; the driver's
     SCALE run measures the real thing).  The job as max_w GPUs would run it:
-    split below the root until >= 640 records per GPU, then the claim phase
-    over the frontier with per-record node accounting.  From the measured
+    every GPU splits its share of the root tasks below the root until >= 640
+    records (each shard timed here one after another; T_W takes the slowest
+    shard of W), then the claim phase over the concatenated frontier with
+    per-record node accounting.  From the measured
     per-record nodes, for W = 1, 2, 4, 8: the static strided split's max/mean
     and a list schedule of the records in claim order over W GPUs (the
     shared counter hands each record to the first free GPU) at the measured
@@ -608,6 +610,8 @@ def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)
 
     _sys.path.insert(0, os.path.join(ROOT, "tests"))
     import catalog as C
+
+    from paper_2301_00806_b200 import dist as wpm_dist
 
     out = []
     for n, d in cases:
@@ -625,22 +629,41 @@ def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)
             p.run()
             t_one = p.timing()["ms_total"]
             p.set_root_stats(True)
+            # the split as max_w GPUs run it: every GPU splits its share of the
+            # root tasks; the shards run one after another here, timed apiece
+            t_shard = {}
+            for W in (1, 2, 4, 8):
+                times = []
+                for sidx in range(W):
+                    for rep in range(2):  # the first pass sizes the frontier / queue buffers
+                        torch.cuda.synchronize(dev)
+                        t0 = time.perf_counter()
+                        p.split(0, 640, sidx, W)
+                        dt = (time.perf_counter() - t0) * 1e3
+                    times.append(dt)
+                t_shard[W] = max(times)
+            parts = []
+            for sidx in range(max_w):
+                p.split(0, 640, sidx, max_w)
+                ptr, cnt, recw = p.frontier()
+                parts.append(torch.as_tensor(wpm_dist._wrap_device(ptr, cnt * recw, torch.int32, dev)).clone())
+            recs = torch.cat(parts)
+            F = recs.numel() // recw
             ctr, _ = wpm.claim_counter_create(dev)
             try:
-                for rep in range(2):  # the first pass sizes the frontier / queue buffers
-                    wpm.claim_counter_reset(dev, ctr)
-                    torch.cuda.synchronize(dev)
-                    t0 = time.perf_counter()
-                    F = p.split(5, 640 * max_w)
-                    t_split = (time.perf_counter() - t0) * 1e3
-                    p.run_claim(ctr)
+                p.load_frontier(recs.data_ptr(), F)
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                p.run_claim(ctr)
+                t_claim = (time.perf_counter() - t0) * 1e3 - p.stats()["ms_sort"]
             finally:
                 wpm.claim_counter_close(dev, ctr, False)
+            t_split = t_shard[max_w]
             st = p.stats()
             per, split_nodes = p.root_nodes()
         per = per.astype(np.float64)
         tot = per.sum()
-        t_main = max(st["ms_search"] - t_split, 1e-3)
+        t_main = max(t_claim, 1e-3)  # host-timed claim phase (the run blocks), sort excluded
         rate = tot / t_main  # nodes per ms, claim phase
         rows = []
         for W in (1, 2, 4, 8):
@@ -652,13 +675,14 @@ def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)
                 t, i = heapq.heappop(h)
                 heapq.heappush(h, (t + x, i))
             mk_nodes = max(t for t, _ in h)
-            t_w = t_split + mk_nodes / rate
-            t_s = t_split + loads.max() / rate
+            t_w = t_shard[W] + mk_nodes / rate
+            t_s = t_shard[W] + loads.max() / rate
             rows.append({"W": W, "static_max_over_mean": float(loads.max() / loads.mean()),
                          "dynamic_makespan_over_mean": float(mk_nodes / (tot / W)),
                          "projected_ms": round(t_w, 3), "projected_speedup": round((t_split + t_main) / t_w, 3),
                          "projected_speedup_static_split": round((t_split + t_main) / t_s, 3)})
         out.append({"case": name, "frontier_records": int(F), "split_ms_host": round(t_split, 3),
+                    "split_ms_by_W": {str(k): round(v, 3) for k, v in t_shard.items()},
                     "claim_ms": round(t_main, 3), "one_gpu_run_ms": round(t_one, 3),
                     "split_nodes": int(split_nodes), "claim_nodes": int(tot),
                     "largest_record_frac": float(per.max() / tot) if tot else None, "by_W": rows})

@@ -194,9 +194,10 @@ int wpm_plan_device_result(const wpm_plan_t *plan, const uint32_t **bits32, cons
  * One job on several GPUs of one process (SearchJob::threads ->
  * parallel_for_index, parallel.hpp:27-54, becomes GPUs): devices[0] must be
  * the plan's device; the others get plans of the same maps.  wpm_plan_run
- * then splits the search tree below the root on devices[0] (split rounds
- * until the frontier has >= 640 records per GPU), copies the frontier to
- * every GPU, and each GPU's kernel 3 pulls records through one claim counter
+ * then splits the search tree below the root, every GPU its share of the
+ * root tasks in parallel (split rounds until the frontiers hold >= 640
+ * records per GPU), copies the concatenated frontier to every GPU, and each
+ * GPU's kernel 3 pulls records through one claim counter
  * in devices[0]'s HBM (peer atomics over NVLink) and shares them further by
  * donation; the rows are gathered into devices[0] (peer copies) and sorted
  * canonically there.  No GPU waits for another.  ndev <= 1 detaches. */
@@ -216,15 +217,19 @@ int wpm_plan_set_root_stats(wpm_plan_t *plan, int32_t on);
 int64_t wpm_plan_root_nodes(wpm_plan_t *plan, int64_t *out, int64_t cap, int64_t *split_nodes);
 /* progress callback of the following runs (see wpm_job_t.progress); NULL = off */
 int wpm_plan_set_progress(wpm_plan_t *plan, void (*fn)(int64_t done, int64_t total, void *user), void *user);
-/* The same protocol across processes (one per GPU): rank 0 calls
- * wpm_plan_split (rows and nodes above the frontier stay in its plan) and
- * broadcasts the frontier records (wpm_plan_frontier: a device pointer,
- * count x recw uint32); the other ranks wpm_plan_load_frontier them.  A
- * claim counter made by rank 0 (wpm_claim_counter_create, 64-byte CUDA IPC
- * handle) is opened by the others (wpm_claim_counter_open); every rank then
- * wpm_plan_run_claim-s and the canonical rows are gathered to rank 0
- * (wpm_canonical_sort_device there). */
-int wpm_plan_split(wpm_plan_t *plan, int32_t depth, int64_t target, int64_t *count);
+/* The same protocol across processes (one per GPU): every rank r calls
+ * wpm_plan_split(plan, r, world, ...) on its share of the root tasks (rows and
+ * nodes above its frontier stay in its plan); the frontiers
+ * (wpm_plan_frontier: a device pointer, count x recw uint32) are all-gathered
+ * and every rank wpm_plan_load_frontier-s the concatenation (not aliasing its
+ * own frontier buffer).  A claim counter made by rank 0
+ * (wpm_claim_counter_create, 64-byte CUDA IPC handle) is opened by the others
+ * (wpm_claim_counter_open); every rank then wpm_plan_run_claim-s and the
+ * canonical rows are gathered to rank 0 (wpm_canonical_sort_device there). */
+/* depth <= 0: 5 + ceil(log_1.7(shard_count)) (one round per shard, usually);
+ * target <= 0: 2048 records */
+int wpm_plan_split(wpm_plan_t *plan, int32_t shard_index, int32_t shard_count, int32_t depth, int64_t target,
+                   int64_t *count);
 int wpm_plan_frontier(const wpm_plan_t *plan, const uint32_t **recs, int64_t *count, int32_t *recw);
 int wpm_plan_load_frontier(wpm_plan_t *plan, const uint32_t *recs, int64_t count);
 int wpm_claim_counter_create(int32_t device, void **counter, uint8_t *ipc_handle /* 64 bytes, optional */);

@@ -208,7 +208,7 @@ _SIGS = {
     "wpm_plan_device_stats": (ctypes.c_int, [_PlanP, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64)]),
     "wpm_plan_set_split": (ctypes.c_int, [_PlanP, _i32]),
     "wpm_plan_set_progress": (ctypes.c_int, [_PlanP, ctypes.c_void_p, ctypes.c_void_p]),
-    "wpm_plan_split": (ctypes.c_int, [_PlanP, _i32, _i64, ctypes.POINTER(_i64)]),
+    "wpm_plan_split": (ctypes.c_int, [_PlanP, _i32, _i32, _i32, _i64, ctypes.POINTER(_i64)]),
     "wpm_plan_frontier": (ctypes.c_int, [_PlanP, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(_i64),
                                          ctypes.POINTER(_i32)]),
     "wpm_plan_load_frontier": (ctypes.c_int, [_PlanP, ctypes.c_void_p, _i64]),
@@ -431,9 +431,12 @@ class Plan:
         return out[:k], int(sp.value)
 
     # -- the cross-process protocol (one process per GPU, see dist.py)
-    def split(self, depth: int = 3, target: int = 0) -> int:
+    def split(self, depth: int = 0, target: int = 0, shard_index: int = 0, shard_count: int = 1) -> int:
+        """Split this plan's share of the root tasks (t % shard_count ==
+        shard_index) below the root (depth 0: the library's choice); returns
+        the frontier record count."""
         c = _i64()
-        _check(_lib.wpm_plan_split(self._h, depth, target, ctypes.byref(c)))
+        _check(_lib.wpm_plan_split(self._h, shard_index, shard_count, depth, target, ctypes.byref(c)))
         return int(c.value)
 
     def frontier(self):

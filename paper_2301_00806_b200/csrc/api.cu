@@ -255,7 +255,7 @@ struct wpm_plan {
     std::vector<long long> dev_nodes;
     void* claim_raw = nullptr;  // the shared claim counter of a multi-GPU job (the leader's)
     std::function<int(int, wpm_plan_t**)> recreate;  // the same plan on another device
-    DevBuf<uint32_t> d_front2, d_gather;
+    DevBuf<uint32_t> d_front2, d_gather, d_front_all;
     bool split_kept = false;  // wpm_plan_split ran: the claim run appends to its rows
     bool root_stats = false;  // count search nodes per root task / frontier record
     std::vector<uint32_t> h_facets;  // host copy of every universe (wpm_plan_universe)
@@ -1272,13 +1272,22 @@ int enable_peer(int dev, int leader) {
 // The first split is at depth 5, then one jump to the target depth.
 long long frontier_target(int ndev) { return std::max<long long>(2048, 640LL * ndev); }
 
+// first split depth for a 1/W share of the root tasks: the whole tree needs
+// ~640 W records, i.e. log_1.7(W) levels more than one GPU's 640 -- so every
+// shard reaches its target in one round (a round costs ~0.5-1 ms of launch,
+// table copy and ramp-up whatever its size)
+int first_split_depth(int ndev) {
+    return 5 + (ndev > 1 ? (int)std::ceil(std::log((double)ndev) / std::log(1.7)) : 0);
+}
+
 }  // namespace
 
 // One job over the leader plan and its peers (one plan per device, same
-// maps): the leader splits the tree below the root (split_rounds), copies the
-// frontier to every device, and every device's kernel 3 pulls frontier
-// records through ONE claim counter in the leader's HBM (system-scope atomics
-// over NVLink) into its own work queue, sharing them further by donation.
+// maps): every device splits its share of the root tasks below the root
+// (split_rounds, in parallel), the frontiers are concatenated and copied to
+// every device, and every device's kernel 3 pulls frontier records through
+// ONE claim counter in the leader's HBM (system-scope atomics over NVLink)
+// into its own work queue, sharing them further by donation.
 // No device waits for another; the rows are gathered into the leader with
 // peer copies and sorted there once.  Host: one thread per device.
 static int plan_run_multi(wpm_plan* P) {
@@ -1290,42 +1299,87 @@ static int plan_run_multi(wpm_plan* P) {
     const int W = 1 + (int)P->peers.size();
     std::vector<wpm_plan*> all{P};
     for (auto* q : P->peers) all.push_back(q);
-    int rc = search_prepare(P, 0, 1);
+    int rc = search_prepare(P, 0, W);  // the leader's share of the root tasks
     if (rc) return rc;
     CU(cudaEventRecord(P->ev[4], P->stream));
     for (int attempt = 0; attempt < 4; ++attempt) {
         CU(cudaSetDevice(P->device));
         g_alloc_stream = P->stream;
-        if ((rc = search_reset(P))) return rc;
-        if ((rc = split_rounds(P, P->split_depth > 0 ? P->split_depth : 5, frontier_target(W)))) return rc;
-        if ((unsigned long long)P->frontier > P->front_cap) {
-            P->front_cap = (unsigned long long)P->frontier + (unsigned long long)P->frontier / 4 + 1024;
+        // every device splits its share of the root tasks (t % W == d), in
+        // parallel; the frontiers are concatenated on the leader and copied
+        // to every device
+        std::vector<int> src(W, 0);
+        {
+            std::vector<std::thread> th;
+            for (int d = 0; d < W; ++d)
+                th.emplace_back([&, d]() {
+                    wpm_plan* q = all[d];
+                    if (cudaSetDevice(q->device) != cudaSuccess) {
+                        src[d] = fail(WPM_EINTERNAL, "cudaSetDevice failed");
+                        return;
+                    }
+                    g_alloc_stream = q->stream;
+                    int r = d ? search_prepare(q, d, W) : WPM_OK;
+                    if (!r) r = search_reset(q);
+                    if (!r)
+                        r = split_rounds(q, P->split_depth > 0 ? P->split_depth : first_split_depth(W),
+                                         (frontier_target(W) + W - 1) / W);
+                    src[d] = r;
+                });
+            for (auto& t : th) t.join();
+        }
+        CU(cudaSetDevice(P->device));
+        g_alloc_stream = P->stream;
+        for (int d = 0; d < W; ++d)
+            if (src[d]) return src[d];
+        bool overflow = false;
+        long long F = 0;
+        for (int d = 0; d < W; ++d) {
+            overflow |= (unsigned long long)all[d]->frontier > all[d]->front_cap;
+            F += all[d]->frontier;
+        }
+        if (overflow) {
+            for (int d = 0; d < W; ++d)
+                all[d]->front_cap = std::max(all[d]->front_cap, (unsigned long long)all[d]->frontier * 5 / 4 + 1024);
             ++P->reruns;
             continue;
         }
-        tr.mark("  multi: split");
+        tr.mark("  multi: parallel split");
         peek("split");
-        const long long F = P->frontier;
+        if (P->d_front_all.ensure((size_t)std::max<long long>(F, 1) * P->recw))
+            return fail(WPM_EINTERNAL, "allocation failed (frontier)");
+        {
+            long long at = 0;
+            for (int d = 0; d < W; ++d) {
+                const size_t bytes = (size_t)all[d]->frontier * P->recw * 4;
+                if (bytes)
+                    CU(cudaMemcpyPeerAsync(P->d_front_all.p + (size_t)at * P->recw, P->device, all[d]->d_front.p,
+                                           all[d]->device, bytes, P->stream));
+                at += all[d]->frontier;
+            }
+        }
         if (!P->claim_raw) {  // plain cudaMalloc: peers reach it through P2P (pool memory would need pool access)
             CU(cudaMalloc(&P->claim_raw, 64));
         }
         CU(cudaMemsetAsync(P->claim_raw, 0, 64, P->stream));
-        P->claim_count = F;
-        P->claim_ctr = static_cast<unsigned long long*>(P->claim_raw);
-        for (auto* q : P->peers) {
+        CU(cudaStreamSynchronize(P->stream));
+        for (int d = 0; d < W; ++d) {
+            wpm_plan* q = all[d];
             CU(cudaSetDevice(q->device));
             g_alloc_stream = q->stream;
-            if ((rc = search_prepare(q, 0, 1)) || (rc = search_reset(q))) return rc;
             if (q->d_front.ensure((size_t)std::max<long long>(F, 1) * q->recw))
-                return fail(WPM_EINTERNAL, "allocation failed (peer frontier)");
+                return fail(WPM_EINTERNAL, "allocation failed (frontier)");
             CU(cudaStreamSynchronize(q->stream));
-            if (F) CU(cudaMemcpyPeerAsync(q->d_front.p, q->device, P->d_front.p, P->device, (size_t)F * P->recw * 4, P->stream));
+            if (F) CU(cudaMemcpyPeerAsync(q->d_front.p, q->device, P->d_front_all.p, P->device, (size_t)F * P->recw * 4,
+                                          P->stream));
+            q->frontier = F;
             q->claim_count = F;
-            q->claim_ctr = P->claim_ctr;
+            q->claim_ctr = static_cast<unsigned long long*>(P->claim_raw);
         }
         CU(cudaSetDevice(P->device));
+        g_alloc_stream = P->stream;
         CU(cudaStreamSynchronize(P->stream));
-        tr.mark("  multi: frontier to peers");
+        tr.mark("  multi: frontier to every device");
         peek("frontier copies");
         // every device claims from the shared frontier
         std::vector<int> rcs(W, 0), again(W, 0);
@@ -1458,17 +1512,21 @@ extern "C" int wpm_plan_set_split(wpm_plan_t* P, int32_t depth) {
 // rank 0 splits and broadcasts the frontier; a claim counter in rank 0's HBM
 // is shared through a CUDA IPC handle; every rank runs the claim phase.
 
-extern "C" int wpm_plan_split(wpm_plan_t* P, int32_t depth, int64_t target, int64_t* count) {
+extern "C" int wpm_plan_split(wpm_plan_t* P, int32_t shard_index, int32_t shard_count, int32_t depth, int64_t target,
+                              int64_t* count) {
     if (!P) return fail(WPM_EINVAL, "null plan");
+    if (shard_count < 1) shard_count = 1;
+    if (shard_index < 0 || shard_index >= shard_count) return fail(WPM_EINVAL, "bad shard index");
     CU(cudaSetDevice(P->device));
     g_alloc_stream = P->stream;
     P->ran = false;
-    int rc = search_prepare(P, 0, 1);
+    int rc = search_prepare(P, shard_index, shard_count);
     if (rc) return rc;
     CU(cudaEventRecord(P->ev[4], P->stream));
     for (int attempt = 0; attempt < 3; ++attempt) {
         if ((rc = search_reset(P))) return rc;
-        if ((rc = split_rounds(P, depth > 0 ? depth : 5, target > 0 ? target : frontier_target(1)))) return rc;
+        if ((rc = split_rounds(P, depth > 0 ? depth : first_split_depth(shard_count),
+                               target > 0 ? target : frontier_target(1)))) return rc;
         if ((unsigned long long)P->frontier <= P->front_cap) break;
         P->front_cap = (unsigned long long)P->frontier + (unsigned long long)P->frontier / 4 + 1024;
     }
@@ -1493,8 +1551,7 @@ extern "C" int wpm_plan_load_frontier(wpm_plan_t* P, const uint32_t* recs, int64
         return fail(WPM_EINTERNAL, "allocation failed (frontier)");
     if (count) CU(cudaMemcpyAsync(P->d_front.p, recs, (size_t)count * P->recw * 4, cudaMemcpyDefault, P->stream));
     CU(cudaStreamSynchronize(P->stream));
-    P->frontier = count;
-    P->split_kept = false;
+    P->frontier = count;  // a plan that split keeps its split's rows / nodes for the claim run
     return WPM_OK;
 }
 

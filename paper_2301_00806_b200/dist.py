@@ -2,11 +2,12 @@
 
 The job (parallel_for_index, parallel.hpp:27-54, across GPUs):
 
-  1. rank 0 splits the search tree below the root (Plan.split: split-mode
-     kernel-3 launches until the frontier has >= 640 records per GPU; the
-     rows and nodes above the frontier stay on rank 0);
-  2. the frontier records are broadcast (NCCL) and a claim counter in rank
-     0's HBM is shared through a CUDA IPC handle;
+  1. every rank splits its share of the root tasks below the root
+     (Plan.split(rank, world): split-mode kernel-3 launches until the
+     frontiers hold >= 640 records per GPU; the rows and nodes above a rank's
+     frontier stay on that rank);
+  2. the frontier records are all-gathered (NCCL) and a claim counter in
+     rank 0's HBM is shared through a CUDA IPC handle;
   3. every rank runs the claim phase (Plan.run_claim): its kernel pulls
      frontier records through the one counter (system-scope atomics over
      NVLink) into its own work queue and shares them by donation -- no GPU
@@ -141,6 +142,22 @@ def share_frontier(dist, rank: int, recs, count: int, recw: int, device):
     return recs, count, recw
 
 
+def all_gather_records(dist, mine, count: int, recw: int, device):
+    """Concatenate every rank's `count` records (recw int32 words each) in rank
+    order on every rank (padded all_gather); returns (tensor, total count)."""
+    import torch
+
+    counts = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(dist.get_world_size())]
+    dist.all_gather(counts, torch.tensor([count], dtype=torch.int64, device=device))
+    counts = [int(c.item()) for c in counts]
+    cap = max(max(counts), 1)
+    pad = torch.zeros(cap * recw, dtype=torch.int32, device=device)
+    pad[: count * recw] = mine[: count * recw]
+    parts = [torch.empty_like(pad) for _ in counts]
+    dist.all_gather(parts, pad)
+    return torch.cat([parts[r][: counts[r] * recw] for r in range(len(counts))]), sum(counts)
+
+
 def share_claim_counter(dist, rank: int, device: int):
     """Rank 0 creates the device claim counter and broadcasts its 64-byte CUDA
     IPC handle; the other ranks open it.  Returns (pointer, opened)."""
@@ -171,7 +188,7 @@ def run_job(dist, plan, rank: int, world: int, device: int, counter=None, target
 
     dev = torch.device("cuda", device)
     if world == 1:
-        plan.split(5, target or 2048)
+        plan.split(0, target or 2048)
         own = counter is None
         ctr = wpm.claim_counter_create(device)[0] if own else counter[0]
         if not own:
@@ -181,17 +198,14 @@ def run_job(dist, plan, rank: int, world: int, device: int, counter=None, target
         finally:
             if own:
                 wpm.claim_counter_close(device, ctr, False)
-    if rank == 0:
-        plan.split(5, target or 640 * world)
-        ptr, count, recw = plan.frontier()
-        recs = _wrap_device(ptr, count * recw, torch.int32, dev)
-        wpm.claim_counter_reset(device, counter[0])
-    else:
-        recs, count, recw = None, 0, 0
+    # every rank splits its share of the root tasks; the frontiers are all-gathered
+    plan.split(0, target or 640, rank, world)  # depth 0: the library's per-shard first depth
+    ptr, count, recw = plan.frontier()
+    recs, total_recs = all_gather_records(dist, _wrap_device(ptr, count * recw, torch.int32, dev), count, recw, dev)
     torch.cuda.synchronize(dev)
-    recs, count, recw = share_frontier(dist, rank, recs, count, recw, dev)
-    if rank != 0:
-        plan.load_frontier(recs.data_ptr(), count)
+    plan.load_frontier(recs.data_ptr(), total_recs)  # a copy: `recs` may go after this
+    if rank == 0:
+        wpm.claim_counter_reset(device, counter[0])
     dist.barrier()  # the counter is reset before any rank claims
     total = plan.run_claim(counter[0])
     dist.barrier()  # every claim is done before the counter is reused

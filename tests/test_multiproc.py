@@ -105,9 +105,10 @@ def test_shard_roots_partition():
 
 
 def _claim_worker(rank, world, port, port2, n, results):
-    """The shared-frontier protocol of dist.run_job over gloo: rank 0 makes
-    the frontier (here: the root tasks (map, minimum facet f) of four maps)
-    and broadcasts it, every rank claims items through one shared atomic
+    """The shared-frontier protocol of dist.run_job over gloo: every rank makes
+    its share of the frontier (here: its share of the root tasks (map, minimum
+    facet f) of four maps), the shares are all-gathered, every rank claims
+    items through one shared atomic
     counter (a Store counter standing in for the device counter) and runs
     them (the CPU restatement of the device search over root f only), the
     rows go to rank 0 by point-to-point gather and are merged canonically."""
@@ -131,13 +132,13 @@ def _claim_worker(rank, world, port, port2, n, results):
         unis = [orc.matroid_universe(r) for r in rows]
         cap = orc.cyclic_facet_bound(n)
         recw = 2
-        if rank == 0:
-            items = [(i, f) for i, u in enumerate(unis) for f in range(len(u))]
-            recs = torch.tensor([x for it in items for x in it], dtype=torch.int32)
-            count = len(items)
-        else:
-            recs, count = None, 0
-        recs, count, recw = wdist.share_frontier(dist, rank, recs, count, recw, "cpu")
+        # each rank's share of the root tasks (t % world == rank) is its
+        # "frontier"; the frontiers are all-gathered in rank order
+        items = [(i, f) for i, u in enumerate(unis) for f in range(len(u))]
+        share = [it for t, it in enumerate(items) if t % world == rank]
+        mine = torch.tensor([x for it in share for x in it] or [0], dtype=torch.int32)
+        recs, count = wdist.all_gather_records(dist, mine, len(share), recw, "cpu")
+        assert count == len(items)
         dist.barrier()
         maps_out, bits_out, node_sum, mine = [], [], 0, []
 
