@@ -138,6 +138,9 @@ struct PinnedCache {
     }
 };
 PinnedCache g_pinned;
+// rows of the last run of each workload (plan signature): sizes the sort grid
+std::mutex g_rows_mu;
+std::map<std::string, long long> g_rows_seen;
 std::mutex g_block_mu;
 std::unordered_map<void*, size_t> g_block_size;
 
@@ -259,6 +262,9 @@ struct wpm_plan {
     bool split_kept = false;  // wpm_plan_split ran: the claim run appends to its rows
     bool root_stats = false;  // count search nodes per root task / frontier record
     std::vector<uint32_t> h_facets;  // host copy of every universe (wpm_plan_universe)
+    std::string signature;           // the workload: (m, n, cap, every universe's facet count)
+    unsigned long long h_dups = 0;   // sort results, read back with the run's synchronisation
+    std::vector<long long> h_first;
     DevBuf<unsigned long long> d_root_nodes;
     long long root_count = 0;
     int ntasks = 0, frame_cap = 64;
@@ -586,6 +592,9 @@ static int plan_build_tables(wpm_plan* P, const std::vector<uint32_t>& foff) {
         P->maxDepth = std::max(P->maxDepth, std::min(P->cap[i], P->M[i]) + 1);
     }
     CU(cudaMemcpyAsync(P->d_maps.p, P->desc.data(), K * sizeof(MapDesc), cudaMemcpyHostToDevice, P->stream));
+    P->signature = std::to_string(P->m) + "/" + std::to_string(P->n) + "/" + std::to_string(P->facet_cap) + "/" +
+                   std::to_string(P->has_pins ? 1 : 0);
+    for (int i = 0; i < K; ++i) P->signature += ":" + std::to_string(P->M[i]) + "," + std::to_string(P->N[i]);
     P->mw = (P->maxM + 31) / 32;
     P->w32 = 2 * ((P->maxM + 63) / 64);
     P->rw = rec_words(P->w32);
@@ -807,6 +816,8 @@ extern "C" int32_t wpm_plan_incidence(wpm_plan_t* P, int32_t map, uint64_t* ridg
 }
 
 static int plan_sort(wpm_plan* P);
+static int plan_sort_launch(wpm_plan* P, bool device_count);
+static int plan_sort_collect(wpm_plan* P);
 
 // ---- one kernel-3 launch on the plan's stream: seed (root tasks or task
 // records), optional frontier output (split mode) or shared-frontier claims
@@ -1140,60 +1151,90 @@ static int plan_search_phases(wpm_plan* P, int shard_index, int shard_count) {
             tr.mark("  run: split");
         }
         if ((rc = search_main(P, P->split_depth > 0 ? SRC_FRONTIER : SRC_ROOTS))) return rc;
-        tr.mark("  run: k3 launch");
+        // the sort follows kernel 3 on the stream, reading the row count on
+        // the device: one synchronisation per run (a stage that overflowed
+        // its buffers is discarded and rerun)
+        if (!P->node_budget && (rc = plan_sort_launch(P, true))) return rc;
+        tr.mark("  run: k3 + sort launch");
         int again = 0;
         if ((rc = search_finish(P, roots, &again))) return rc;
-        tr.mark("  run: k3 sync");
-        if (!again) break;
+        tr.mark("  run: k3 + sort sync");
+        if (!again) return P->node_budget ? plan_sort(P) : plan_sort_collect(P);
     }
-    return WPM_OK;
+    return fail(WPM_EINTERNAL, "search did not settle in 4 attempts");
 }
 
 static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
-    const int rc = plan_search_phases(P, shard_index, shard_count);
-    return rc ? rc : plan_sort(P);
+    return plan_search_phases(P, shard_index, shard_count);
 }
 
 // canonical sort of the key rows in d_out_keys (P->total of them), per-map
 // counts from the group boundaries; shared by the DFS and the odometer runs
-static int plan_sort(wpm_plan* P) {
-    Trace tr;
+// launch the sort on the plan's stream: rows = P->total, or -- device_count
+// -- the count kernel 3 left in out_ctl[0] (capped at out_cap), so the sort
+// follows the search without a host round trip
+static int plan_sort_launch(wpm_plan* P, bool device_count) {
     const int K = P->num_maps;
-    const long long total = P->total;
-    const size_t tb = canon_sort_temp_bytes(std::max<long long>(total, 1), P->w32);
-    if (P->d_temp.ensure(tb) || P->d_sorted_bits.ensure((size_t)total * P->w32 + 1) ||
-        P->d_sorted_map.ensure(total + 1))
+    const long long rows = device_count ? (long long)P->out_cap : P->total;
+    const size_t tb = canon_sort_temp_bytes(std::max<long long>(rows, 1), P->w32);
+    if (P->d_temp.ensure(tb) || P->d_sorted_bits.ensure((size_t)rows * P->w32 + 1) || P->d_sorted_map.ensure(rows + 1))
         return fail(WPM_EINTERNAL, "device allocation failed (sort)");
     CU(cudaMemsetAsync(P->d_out_ctl.p + 1, 0, 8, P->stream));
     CU(cudaMemsetAsync(P->d_per_map.p, 0xFF, K * 8, P->stream));  // first row per map, -1 = none
     CU(cudaEventRecord(P->ev[2], P->stream));
-    if (canon_sort_keys(P->d_out_keys.p, total, P->w32, P->d_sorted_bits.p, P->d_sorted_map.p, P->d_temp.p,
-                        P->d_temp.n, (long long*)P->d_per_map.p, P->d_out_ctl.p + 1, P->stream))
+    // grid sized from the rows this workload produced last time (this plan, or
+    // an earlier plan of the same maps: one-shot calls), else the capacity
+    long long hint = 0;
+    if (device_count) {
+        std::lock_guard<std::mutex> lk(g_rows_mu);
+        auto it = g_rows_seen.find(P->signature);
+        if (it != g_rows_seen.end()) hint = it->second + it->second / 8 + 64;
+    }
+    if (canon_sort_keys(P->d_out_keys.p, rows, P->w32, P->d_sorted_bits.p, P->d_sorted_map.p, P->d_temp.p,
+                        P->d_temp.n, (long long*)P->d_per_map.p, P->d_out_ctl.p + 1, P->stream,
+                        device_count ? P->d_out_ctl.p : nullptr, hint))
         return fail(WPM_EINTERNAL, std::string("canonical sort: ") + cudaGetErrorString(cudaGetLastError()));
     CU(cudaEventRecord(P->ev[3], P->stream));
-    tr.mark("  sort: alloc + launch");
-    unsigned long long dups = 0;
-    std::vector<long long> first(K);
-    CU(cudaMemcpyAsync(&dups, P->d_out_ctl.p + 1, 8, cudaMemcpyDeviceToHost, P->stream));
-    CU(cudaMemcpyAsync(first.data(), P->d_per_map.p, K * 8, cudaMemcpyDeviceToHost, P->stream));
-    CU(cudaStreamSynchronize(P->stream));
-    tr.mark("  sort: sync");
+    // results of the sort, read back with the next synchronisation
+    CU(cudaMemcpyAsync(&P->h_dups, P->d_out_ctl.p + 1, 8, cudaMemcpyDeviceToHost, P->stream));
+    P->h_first.resize(K);
+    CU(cudaMemcpyAsync(P->h_first.data(), P->d_per_map.p, K * 8, cudaMemcpyDeviceToHost, P->stream));
     P->d2h += 8 + 8LL * K;
-    P->dups = (long long)dups;
+    return WPM_OK;
+}
+
+// after the stream synchronised: duplicates, per-map counts, timings
+static int plan_sort_collect(wpm_plan* P) {
+    const int K = P->num_maps;
+    {
+        std::lock_guard<std::mutex> lk(g_rows_mu);
+        g_rows_seen[P->signature] = P->total;
+    }
+    P->dups = (long long)P->h_dups;
     // per-map counts from the group boundaries of the sorted map ids
     P->per_map.assign(K, 0);
     {
         long long next = P->total;
         for (int i = K - 1; i >= 0; --i)
-            if (first[i] >= 0) {
-                P->per_map[i] = (unsigned long long)(next - first[i]);
-                next = first[i];
+            if (P->h_first[i] >= 0) {
+                P->per_map[i] = (unsigned long long)(next - P->h_first[i]);
+                next = P->h_first[i];
             }
     }
     CU(cudaEventElapsedTime(&P->ms_search, P->ev[0], P->ev[1]));
     CU(cudaEventElapsedTime(&P->ms_sort, P->ev[2], P->ev[3]));
     CU(cudaEventElapsedTime(&P->ms_total, P->ev[4], P->ev[3]));
     return WPM_OK;
+}
+
+static int plan_sort(wpm_plan* P) {
+    Trace tr;
+    int rc = plan_sort_launch(P, false);
+    if (rc) return rc;
+    tr.mark("  sort: alloc + launch");
+    CU(cudaStreamSynchronize(P->stream));
+    tr.mark("  sort: sync");
+    return plan_sort_collect(P);
 }
 
 static int plan_run_multi(wpm_plan* P);

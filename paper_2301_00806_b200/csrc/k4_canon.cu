@@ -44,7 +44,8 @@ struct SortParams {
     const uint32_t* in;    // count * rw records (kernel-3 output)
     uint32_t* buf0;        // ping-pong record buffers (buf0 may alias nothing)
     uint32_t* buf1;
-    long long count;
+    long long count;                      // rows, or the cap of *count_dev
+    const unsigned long long* count_dev;  // optional: the row count on the device
     int w32, rw;
     int tile;              // records per phase-1 tile (power of two)
     int chunk;             // output records per merge chunk (<= tile)
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k4_sort(const __grid_constant
     extern __shared__ __align__(16) uint32_t sm[];
     cg::grid_group grid = cg::this_grid();
     const int T = p.tile, rw = p.rw, w32 = p.w32;
-    const long long N = p.count;
+    const long long N = p.count_dev ? min((long long)*p.count_dev, p.count) : p.count;
     uint32_t* recs = sm;                                       // T records
     uint16_t* idx = reinterpret_cast<uint16_t*>(sm + (size_t)T * rw);  // T indices (bitonic)
     const long long ntiles = (N + T - 1) / T;
@@ -259,7 +260,7 @@ size_t canon_sort_temp_bytes(long long count, int w32) {
 
 int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sorted_bits, uint16_t* d_sorted_map,
                     void* d_temp, size_t temp_bytes, long long* d_first_row, unsigned long long* d_dups,
-                    cudaStream_t st) {
+                    cudaStream_t st, const unsigned long long* d_count, long long grid_rows) {
     if (count <= 0) return 0;
     const int rw = rec_words(w32);
     if (temp_bytes < canon_sort_temp_bytes(count, w32)) return 1;
@@ -280,13 +281,17 @@ int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sort
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_sort, SORT_THREADS, smem) != cudaSuccess || per_sm < 1)
         return 1;
-    const long long work = std::max((count + T - 1) / T, (count + Cc - 1) / Cc);
+    // the kernel strides over its tiles / chunks, so any grid is correct; size
+    // it for the expected rows (fewer idle CTAs in every grid barrier)
+    const long long rows_for_grid = grid_rows > 0 ? std::min(grid_rows, count) : count;
+    const long long work = std::max((rows_for_grid + T - 1) / T, (rows_for_grid + Cc - 1) / Cc);
     const int grid = (int)std::min<long long>(work, (long long)per_sm * g_sort_sms[dev]);
     SortParams sp{};
     sp.in = d_keys;
     sp.buf0 = static_cast<uint32_t*>(d_temp);
     sp.buf1 = sp.buf0 + (size_t)count * rw;
     sp.count = count;
+    sp.count_dev = d_count;
     sp.w32 = w32;
     sp.rw = rw;
     sp.tile = T;

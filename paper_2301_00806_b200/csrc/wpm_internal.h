@@ -94,9 +94,11 @@ int key_words_for(int w32);
 // a whole number of 16-byte vectors
 __host__ __device__ inline int rec_words(int w32) { return (w32 + 1 + 3) & ~3; }
 size_t canon_sort_temp_bytes(long long count, int w32);
+// d_count (optional): the row count on the device (read by the kernel,
+// capped at `count`, which then only sizes the launch)
 int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sorted_bits, uint16_t* d_sorted_map,
                     void* d_temp, size_t temp_bytes, long long* d_first_row, unsigned long long* d_dups,
-                    cudaStream_t st);
+                    cudaStream_t st, const unsigned long long* d_count = nullptr, long long grid_rows = 0);
 // rows (w32 words) + uint16 map ids -> key rows
 int canon_pack(const uint32_t* d_bits, const uint16_t* d_map, long long count, int w32, uint32_t* d_keys,
                cudaStream_t st);
