@@ -1106,6 +1106,9 @@ static int search_finish(wpm_plan* P, long long progress_total, int* again) {
     P->total = (long long)octl[0];
     P->tasks = (long long)qc[3];  // kernel-3 launches of one attempt add up in qctl[3] / [4]
     P->nodes = (long long)qc[4];
+    if (std::getenv("WPM_POLLSTAT"))
+        std::fprintf(stderr, "[wpm] poll iterations %llu, waits %llu, wait cycles %llu (%.2f us per wait), tasks %llu, nodes %llu\n",
+                     qc[5], qc[6], qc[7], qc[6] ? qc[7] / 1965.0 / qc[6] : 0.0, qc[3], qc[4]);
     if (std::getenv("WPM_PROFILE") && (qc[5] | qc[6] | qc[7])) {
         const double all = (double)(qc[5] + qc[6] + qc[7]);
         std::fprintf(stderr, "[wpm] warp clocks: busy %.1f%%  waiting %.1f%%  final wait %.1f%%  (tasks %llu)\n",

@@ -271,9 +271,18 @@ int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sort
         return 1;
     // tile: a power of two with T records + T indices in <= 200 KB of shared
     // memory; merge chunks of the same size
-    int T = 2048;  // tile / chunk sweep 2048-8192 x 512-2048 at n = 5 and 8: 2048 / 2048 best
-    while (T > 64 && (size_t)T * rw * 4 + (size_t)T * 2 > 200u * 1024u) T >>= 1;
-    if (const char* e = std::getenv("WPM_SORT_TILE")) T = std::max(64, std::min(T, std::atoi(e)));
+    // tile = chunk = the largest power of two <= 2048 that still gives every
+    // SM a tile (N / SMs) and keeps a tile's records <= 100 KB of shared
+    // memory (two CTAs per SM).  Swept 256-4096 at n = 4, 5, 6, 8, 11: the best
+    // tile follows the row count (n = 4: 256, n = 5: 1024, n = 6 / 8: 2048)
+    // and the record width (n = 11, 128-byte records: 256-512).
+    const long long rows_hint = grid_rows > 0 ? std::min(grid_rows, count) : count;
+    int T = 2048;
+    while (T > 128 && ((long long)T > rows_hint / g_sort_sms[dev] || (size_t)T * rw * 4 > 100u * 1024u)) T >>= 1;
+    if (const char* e = std::getenv("WPM_SORT_TILE")) {
+        T = std::max(64, std::atoi(e));
+        while (T > 64 && (size_t)T * rw * 4 + (size_t)T * 2 > 200u * 1024u) T >>= 1;
+    }
     int Cc = T;
     if (const char* e = std::getenv("WPM_SORT_CHUNK")) Cc = std::max(32, std::min(T, std::atoi(e)));
     const size_t smem = (size_t)T * rw * 4 + (size_t)T * 2 + 16;
