@@ -226,7 +226,8 @@ int wpm_plan_set_progress(wpm_plan_t *plan, void (*fn)(int64_t done, int64_t tot
  * (wpm_claim_counter_create, 64-byte CUDA IPC handle) is opened by the others
  * (wpm_claim_counter_open); every rank then wpm_plan_run_claim-s and the
  * canonical rows are gathered to rank 0 (wpm_canonical_sort_device there). */
-/* depth <= 0: 5 + ceil(log_1.7(shard_count)) (one round per shard, usually);
+/* depth <= 0: 5 + ceil(log_1.7(shard_count)), then calibrated from the last
+ * split of the same workload (one round per shard, usually);
  * target <= 0: 2048 records */
 int wpm_plan_split(wpm_plan_t *plan, int32_t shard_index, int32_t shard_count, int32_t depth, int64_t target,
                    int64_t *count);

@@ -1264,10 +1264,29 @@ namespace {
 // split rounds on the plan: from the root tasks at `depth`, then (while the
 // frontier is smaller than `target`) from the frontier two levels deeper.
 // Rows and nodes of everything above the final frontier stay in the plan.
-int split_rounds(wpm_plan* P, int depth, long long target) {
+// (depth, records) of the last split of each workload and shard count: the
+// next split of the same job aims at its target in one round
+std::mutex g_split_mu;
+std::map<std::string, std::pair<int, long long>> g_split_seen;
+
+int split_rounds(wpm_plan* P, int depth, long long target, int shard_count, bool calibrate) {
     if (P->d_front2.ensure(1)) return fail(WPM_EINTERNAL, "allocation failed (frontier)");
+    const std::string key = P->signature + "#" + std::to_string(shard_count) + "#" + std::to_string(target);
+    if (calibrate) {
+        std::lock_guard<std::mutex> lk(g_split_mu);
+        auto it = g_split_seen.find(key);
+        if (it != g_split_seen.end() && it->second.second > 0) {
+            const double r = std::log((double)target / (double)it->second.second) / std::log(1.7);
+            depth = std::max(1, std::min(60, it->second.first + (int)std::lround(r)));
+        }
+    }
+    const int first_depth = depth;
     int rc = search_split(P, depth);
     if (rc) return rc;
+    {
+        std::lock_guard<std::mutex> lk(g_split_mu);
+        g_split_seen[key] = {first_depth, P->frontier};
+    }
     for (int round = 1; round < 8; ++round) {
         if ((unsigned long long)P->frontier > P->front_cap) return WPM_OK;  // caller reruns with room
         // within 2x of the target is enough (a round costs ~0.5-1.5 ms)
@@ -1367,7 +1386,7 @@ static int plan_run_multi(wpm_plan* P) {
                     if (!r) r = search_reset(q);
                     if (!r)
                         r = split_rounds(q, P->split_depth > 0 ? P->split_depth : first_split_depth(W),
-                                         (frontier_target(W) + W - 1) / W);
+                                         (frontier_target(W) + W - 1) / W, W, P->split_depth <= 0);
                     src[d] = r;
                 });
             for (auto& t : th) t.join();
@@ -1570,7 +1589,7 @@ extern "C" int wpm_plan_split(wpm_plan_t* P, int32_t shard_index, int32_t shard_
     for (int attempt = 0; attempt < 3; ++attempt) {
         if ((rc = search_reset(P))) return rc;
         if ((rc = split_rounds(P, depth > 0 ? depth : first_split_depth(shard_count),
-                               target > 0 ? target : frontier_target(1)))) return rc;
+                               target > 0 ? target : frontier_target(1), shard_count, depth <= 0))) return rc;
         if ((unsigned long long)P->frontier <= P->front_cap) break;
         P->front_cap = (unsigned long long)P->frontier + (unsigned long long)P->frontier / 4 + 1024;
     }
