@@ -53,12 +53,13 @@ struct SortParams {
     uint16_t* out_map;
     long long* first_row;  // per map (may be null)
     unsigned long long* dups;
+    int tie;               // >= 0: a payload word that breaks ties (a total order over equal rows)
+    uint32_t* out_payload; // optional: that payload word of every sorted record
 };
 
 // canonical record order: map, then the facet-list order on the bitsets
-__device__ __forceinline__ bool rec_less(const uint32_t* A, const uint32_t* B, int w32) {
-    const int mp = rec_words(w32) - 1;  // the map id
-    const uint32_t ma = A[mp], mb = B[mp];
+__device__ __forceinline__ bool rec_less(const uint32_t* A, const uint32_t* B, int w32, int mp, int tie) {
+    const uint32_t ma = A[mp], mb = B[mp];  // the map id (the record's last word)
     if (ma != mb) return ma < mb;
     for (int w = 0; w < w32; ++w) {
         const uint32_t a = A[w], b = B[w];
@@ -71,7 +72,7 @@ __device__ __forceinline__ bool rec_less(const uint32_t* A, const uint32_t* B, i
         for (int v = w + 1; v < w32 && !more; ++v) more = O[v] != 0u;
         return a_has ? more : !more;
     }
-    return false;
+    return tie >= 0 && A[tie] < B[tie];
 }
 
 // copy nw words (a multiple of 4; 16-byte aligned) global -> shared in
@@ -95,12 +96,12 @@ __device__ __forceinline__ void stage16(uint32_t* dst, const uint32_t* src, long
 // merge-path split of diagonal d between sorted A[0..na) and B[0..nb):
 // the number of A elements among the first d outputs (A wins ties)
 __device__ __forceinline__ long long merge_split(const uint32_t* A, long long na, const uint32_t* B, long long nb,
-                                                 long long d, int w32, int rw) {
+                                                 long long d, int w32, int rw, int tie) {
     long long lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
     while (lo < hi) {
         const long long a = (lo + hi) >> 1;  // take a from A, d - a from B
         // A[a] vs B[d - a - 1]: if B[d-a-1] < A[a] then fewer A needed
-        if (rec_less(B + (size_t)(d - a - 1) * rw, A + (size_t)a * rw, w32)) hi = a;
+        if (rec_less(B + (size_t)(d - a - 1) * rw, A + (size_t)a * rw, w32, rw - 1, tie)) hi = a;
         else lo = a + 1;
     }
     return lo;
@@ -110,14 +111,14 @@ __device__ __forceinline__ long long merge_split(const uint32_t* A, long long na
 // search), so a merge-path search over L2-resident runs costs log33 rounds
 // of dependent loads instead of log2
 __device__ __forceinline__ long long merge_split_warp(const uint32_t* A, long long na, const uint32_t* B, long long nb,
-                                                      long long d, int w32, int rw, int lane) {
+                                                      long long d, int w32, int rw, int tie, int lane) {
     long long lo = d > nb ? d - nb : 0, hi = d < na ? d : na;  // answer in [lo, hi]
     while (hi - lo > 0) {
         const long long span = hi - lo;
         // probe a_i = lo + (i + 1) * span / 33 for lanes i < 32 (distinct once span >= 33)
         const long long a = lo + ((long long)(lane + 1) * span) / 33;
         bool pred = true;  // pred(a): B[d-a-1] < A[a]  (monotone in a)
-        if (a < hi) pred = rec_less(B + (size_t)(d - a - 1) * rw, A + (size_t)a * rw, w32);
+        if (a < hi) pred = rec_less(B + (size_t)(d - a - 1) * rw, A + (size_t)a * rw, w32, rw - 1, tie);
         const unsigned t = __ballot_sync(0xFFFFFFFFu, pred);
         const int f = t ? __ffs(t) - 1 : 32;
         // the answer lies in (a_{f-1}, a_f]: a_{-1} = lo - 1, a_32 = hi
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k4_sort(const __grid_constant
                         const int a = idx[i], b = idx[l];
                         // indices >= cnt are +inf padding
                         const bool b_lt_a = a >= cnt ? b < cnt || b < a
-                                                     : (b < cnt && rec_less(recs + (size_t)b * rw, recs + (size_t)a * rw, w32));
+                                                     : (b < cnt && rec_less(recs + (size_t)b * rw, recs + (size_t)a * rw, w32, rw - 1, p.tie));
                         const bool up = (i & k) == 0;
                         if (up == b_lt_a) {
                             idx[i] = (uint16_t)b;
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k4_sort(const __grid_constant
             const uint32_t* B = A + (size_t)na * rw;
             const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
             if (warp < 2) {
-                const long long r = merge_split_warp(A, na, B, nb, (warp ? o1 : o0) - rbase, w32, rw, lane);
+                const long long r = merge_split_warp(A, na, B, nb, (warp ? o1 : o0) - rbase, w32, rw, p.tie, lane);
                 if (lane == 0) s_rng[warp] = r;
             }
             __syncthreads();
@@ -203,10 +204,10 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k4_sort(const __grid_constant
             const int per = (total + blockDim.x - 1) / blockDim.x;
             const int d0 = min(total, (int)threadIdx.x * per), d1 = min(total, d0 + per);
             if (d0 < d1) {  // each thread: its merge-path diagonal, then `per` sources
-                int ia = (int)merge_split(SA, ca, SB, cb, d0, w32, rw);
+                int ia = (int)merge_split(SA, ca, SB, cb, d0, w32, rw, p.tie);
                 int ib = d0 - ia;
                 for (int d = d0; d < d1; ++d) {
-                    const bool take_a = ib >= cb || (ia < ca && !rec_less(SB + (size_t)ib * rw, SA + (size_t)ia * rw, w32));
+                    const bool take_a = ib >= cb || (ia < ca && !rec_less(SB + (size_t)ib * rw, SA + (size_t)ia * rw, w32, rw - 1, p.tie));
                     idx[d] = (uint16_t)(take_a ? ia++ : ca + ib++);
                 }
             }
@@ -235,7 +236,8 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k4_sort(const __grid_constant
     for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += stride) {
         const uint32_t* R = src + (size_t)r * rw;
         const uint32_t* Q = R - rw;  // the previous record (r > 0)
-        p.out_map[r] = (uint16_t)R[rw - 1];
+        if (p.out_map) p.out_map[r] = (uint16_t)R[rw - 1];
+        if (p.out_payload) p.out_payload[r] = R[p.tie];
         if (r == 0 || Q[rw - 1] != R[rw - 1]) {
             if (p.first_row) p.first_row[R[rw - 1]] = r;
         } else {
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k4_sort(const __grid_constant
             nd += same;
         }
     }
-    if (nd) atomicAdd(p.dups, nd);
+    if (nd && p.dups) atomicAdd(p.dups, nd);
 }
 
 int g_sort_sms[64] = {0};
@@ -261,16 +263,22 @@ size_t canon_sort_temp_bytes(long long count, int w32) {
 int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sorted_bits, uint16_t* d_sorted_map,
                     void* d_temp, size_t temp_bytes, long long* d_first_row, unsigned long long* d_dups,
                     cudaStream_t st, const unsigned long long* d_count, long long grid_rows) {
+    return canon_sort_records(d_keys, count, w32, rec_words(w32), -1, d_sorted_bits, d_sorted_map, nullptr, d_temp,
+                              temp_bytes, d_first_row, d_dups, st, d_count, grid_rows);
+}
+
+int canon_sort_records(uint32_t* d_keys, long long count, int w32, int rw, int tie, uint32_t* d_sorted_bits,
+                       uint16_t* d_sorted_map, uint32_t* d_payload, void* d_temp, size_t temp_bytes,
+                       long long* d_first_row, unsigned long long* d_dups, cudaStream_t st,
+                       const unsigned long long* d_count, long long grid_rows) {
     if (count <= 0) return 0;
-    const int rw = rec_words(w32);
-    if (temp_bytes < canon_sort_temp_bytes(count, w32)) return 1;
+    if (rw % 4 || rw < w32 + 1) return 1;
+    if (temp_bytes < (size_t)2 * (size_t)count * (size_t)rw * 4) return 1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64) return 1;
     if (!g_sort_sms[dev] && cudaDeviceGetAttribute(&g_sort_sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
         return 1;
-    // tile: a power of two with T records + T indices in <= 200 KB of shared
-    // memory; merge chunks of the same size
     // tile = chunk = the largest power of two <= 2048 that still gives every
     // SM a tile (N / SMs) and keeps a tile's records <= 100 KB of shared
     // memory (two CTAs per SM).  Swept 256-4096 at n = 4, 5, 6, 8, 11: the best
@@ -309,6 +317,8 @@ int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sort
     sp.out_map = d_sorted_map;
     sp.first_row = d_first_row;
     sp.dups = d_dups;
+    sp.tie = tie;
+    sp.out_payload = d_payload;
     void* args[] = {&sp};
     if (cudaLaunchCooperativeKernel((const void*)k4_sort, dim3(grid), dim3(SORT_THREADS), args, smem, st) != cudaSuccess)
         return 1;

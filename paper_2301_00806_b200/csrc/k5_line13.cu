@@ -30,7 +30,6 @@
 // swapped facet in the list).  The oracle restates the reference literally
 // (oracle/line13_port.c) and the tests check both against the reference's
 // own is_seed (oracle/_ref).
-#include <cub/device/device_select.cuh>
 
 #include <algorithm>
 #include <cstdint>
@@ -266,10 +265,8 @@ int l13_remap(const uint32_t* d_rows, const uint16_t* d_map, long long count, in
 }
 
 size_t l13_select_temp_bytes(long long count) {
-    size_t a = 0;
-    cub::DeviceSelect::Flagged(nullptr, a, (const uint32_t*)nullptr, (const uint8_t*)nullptr, (uint32_t*)nullptr,
-                               (int*)nullptr, (int)count);
-    return a;
+    (void)count;
+    return compact_temp_bytes();
 }
 
 int l13_unique(const uint32_t* d_sorted, long long count, int gw, uint8_t* d_flags, uint32_t* d_iota,
@@ -278,9 +275,9 @@ int l13_unique(const uint32_t* d_sorted, long long count, int gw, uint8_t* d_fla
     const unsigned g = (unsigned)((count + 255) / 256);
     run_heads<<<g, 256, 0, st>>>(d_sorted, count, gw, d_flags);
     iota32<<<g, 256, 0, st>>>(d_iota, count);
-    size_t b = temp_bytes;
-    if (cub::DeviceSelect::Flagged(d_temp, b, d_iota, d_flags, d_uidx, d_num, (int)count, st) != cudaSuccess)
-        return 1;
+    (void)temp_bytes;
+    (void)d_iota;
+    if (compact_flagged(nullptr, d_flags, count, d_uidx, d_num, d_temp, st)) return 1;  // the heads' indices
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
@@ -297,11 +294,10 @@ int l13_filter(const uint32_t* d_sorted, int gw, const uint32_t* d_uidx, const i
     filter_rows<<<(unsigned)blocks, 32 * L13_WARPS, smem, st>>>(d_sorted, gw, d_uidx, d_num, d_unrank, m, maxf,
                                                                 d_keep);
     if (cudaGetLastError() != cudaSuccess) return 1;
-    size_t b = temp_bytes;
+    (void)temp_bytes;
     // the unique count lives on the device: select over the upper bound, the
     // tail flags beyond *d_num are cleared first by the caller
-    if (cub::DeviceSelect::Flagged(d_temp, b, d_uidx, d_keep, d_sidx, d_num13, (int)max_count, st) != cudaSuccess)
-        return 1;
+    if (compact_flagged(d_uidx, d_keep, max_count, d_sidx, d_num13, d_temp, st)) return 1;
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

@@ -46,8 +46,6 @@
 // Parity: oracle/line15_port.c restates refine_classes / canonical_form
 // literally; the tests check the device against it and against the
 // reference itself (oracle/_ref plseeds_ref classes / line15).
-#include <cub/device/device_merge_sort.cuh>
-#include <cub/device/device_select.cuh>
 
 #include <algorithm>
 #include <cstdint>
@@ -729,37 +727,32 @@ __global__ void __launch_bounds__(32 * L15_WARPS, 8) l15_canon(L15Src src, L15Ou
 }
 
 // ---- first-appearance dedupe of the canonical rows (pipeline.hpp:97-100):
-// sort survivor indices by (row, index), keep the first of each run, then
-// select the kept indices in ascending order
-struct CanonIdxLess {
-    const uint32_t* rows;
-    int gw;
-    __device__ __forceinline__ bool operator()(const uint32_t& a, const uint32_t& b) const {
-        const uint32_t* A = rows + (size_t)a * gw;
-        const uint32_t* B = rows + (size_t)b * gw;
-        for (int w = 0; w < gw; ++w)
-            if (A[w] != B[w]) return A[w] < B[w];
-        return a < b;
-    }
-};
+// kernel 4's record sort orders (row, survivor index) -- the index rides in
+// the record as a payload word that breaks ties -- so the head of each run of
+// equal rows carries the run's first appearance; heads mark is_rep[index];
+// compacting is_rep over the survivor order gives the representatives in
+// order of first appearance.  No library code.
+__global__ void pack_rows_payload(const uint32_t* __restrict__ rows, int gw, long long n, int rw,
+                                  uint32_t* __restrict__ recs) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * rw) return;
+    const long long r = t / rw;
+    const int w = (int)(t - r * rw);
+    recs[t] = w < gw ? rows[(size_t)r * gw + w] : (w == gw ? (uint32_t)r : 0u);  // payload, padding, map 0
+}
 
 __global__ void iota_idx(uint32_t* idx, long long n) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) idx[i] = (uint32_t)i;
 }
 
-__global__ void first_flags(const uint32_t* __restrict__ rows, int gw, const uint32_t* __restrict__ sidx, long long n,
-                            uint8_t* __restrict__ first) {
+__global__ void mark_first(const uint32_t* __restrict__ sorted, int gw, const uint32_t* __restrict__ payload,
+                           long long n, uint8_t* __restrict__ is_rep) {
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
-    const uint32_t i = sidx[p];
     bool head = p == 0;
-    if (!head) {
-        const uint32_t* A = rows + (size_t)i * gw;
-        const uint32_t* Bp = rows + (size_t)sidx[p - 1] * gw;
-        for (int w = 0; w < gw && !head; ++w) head = A[w] != Bp[w];
-    }
-    first[i] = head ? 1 : 0;
+    for (int w = 0; w < gw && !head; ++w) head = sorted[(size_t)p * gw + w] != sorted[(size_t)(p - 1) * gw + w];
+    if (head) is_rep[payload[p]] = 1;
 }
 
 __global__ void gather_rows15(const uint32_t* __restrict__ rows, int gw, const uint32_t* __restrict__ idx,
@@ -860,29 +853,34 @@ int l15_launch(const L15Layout& L, const uint32_t* d_rows, const uint32_t* d_idx
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+// temp: the records, the sort's two record buffers, the sorted rows, the
+// compaction's block counts
 size_t l15_dedupe_temp_bytes(long long count, int gw) {
-    size_t a = 0, b = 0;
-    cub::DeviceMergeSort::SortKeys(nullptr, a, (uint32_t*)nullptr, (int)count, CanonIdxLess{nullptr, gw});
-    cub::DeviceSelect::Flagged(nullptr, b, (const uint32_t*)nullptr, (const uint8_t*)nullptr, (uint32_t*)nullptr,
-                               (int*)nullptr, (int)count);
-    return std::max(a, b);
+    const size_t rw = (size_t)rec_words(gw + 1);
+    return (size_t)count * rw * 4 * 3 + (size_t)count * gw * 4 + compact_temp_bytes() + 1024;
 }
 
 // rows: count canonical rows; out: d_rep (indices of the first appearances,
-// ascending), *d_nrep; scratch d_sidx (count), d_first (count)
+// ascending), *d_nrep; scratch d_sidx (count: the sorted payloads), d_first
+// (count: is_rep)
 int l15_dedupe(const uint32_t* d_rows, long long count, int gw, uint32_t* d_sidx, uint32_t* d_iota, uint8_t* d_first,
                uint32_t* d_rep, int* d_nrep, void* d_temp, size_t temp_bytes, cudaStream_t st) {
     if (count <= 0) return cudaMemsetAsync(d_nrep, 0, sizeof(int), st) == cudaSuccess ? 0 : 1;
-    const unsigned g = (unsigned)((count + 255) / 256);
-    iota_idx<<<g, 256, 0, st>>>(d_sidx, count);
-    iota_idx<<<g, 256, 0, st>>>(d_iota, count);
-    size_t b = temp_bytes;
-    if (cub::DeviceMergeSort::SortKeys(d_temp, b, d_sidx, (int)count, CanonIdxLess{d_rows, gw}, st) != cudaSuccess)
+    iota_idx<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(d_iota, count);  // the survivor order (fetch 14)
+    if (temp_bytes < l15_dedupe_temp_bytes(count, gw)) return 1;
+    const int rw = rec_words(gw + 1);
+    uint32_t* recs = static_cast<uint32_t*>(d_temp);
+    uint32_t* sort_tmp = recs + (size_t)count * rw;
+    uint32_t* sorted = sort_tmp + (size_t)count * rw * 2;
+    void* ctemp = sorted + (size_t)count * gw;
+    const long long t = count * rw;
+    pack_rows_payload<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(d_rows, gw, count, rw, recs);
+    if (canon_sort_records(recs, count, gw, rw, gw, sorted, nullptr, d_sidx, sort_tmp,
+                           (size_t)count * rw * 4 * 2, nullptr, nullptr, st))
         return 1;
-    first_flags<<<g, 256, 0, st>>>(d_rows, gw, d_sidx, count, d_first);
-    b = temp_bytes;
-    if (cub::DeviceSelect::Flagged(d_temp, b, d_iota, d_first, d_rep, d_nrep, (int)count, st) != cudaSuccess)
-        return 1;
+    if (cudaMemsetAsync(d_first, 0, (size_t)count, st) != cudaSuccess) return 1;
+    mark_first<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(sorted, gw, d_sidx, count, d_first);
+    if (compact_flagged(nullptr, d_first, count, d_rep, d_nrep, ctemp, st)) return 1;
     return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

@@ -99,6 +99,20 @@ size_t canon_sort_temp_bytes(long long count, int w32);
 int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sorted_bits, uint16_t* d_sorted_map,
                     void* d_temp, size_t temp_bytes, long long* d_first_row, unsigned long long* d_dups,
                     cudaStream_t st, const unsigned long long* d_count = nullptr, long long grid_rows = 0);
+// the general form: records of rw words (a multiple of 4, >= w32 + 1; the
+// map id last), compared on (map, w32 bitset words) and then -- tie >= 0 --
+// on word `tie` (a payload carried through the sort, written to d_payload);
+// temp >= 2 * count * rw * 4 bytes; d_sorted_map / d_payload may be null
+int canon_sort_records(uint32_t* d_keys, long long count, int w32, int rw, int tie, uint32_t* d_sorted_bits,
+                       uint16_t* d_sorted_map, uint32_t* d_payload, void* d_temp, size_t temp_bytes,
+                       long long* d_first_row, unsigned long long* d_dups, cudaStream_t st,
+                       const unsigned long long* d_count = nullptr, long long grid_rows = 0);
+// stream compaction (one cooperative launch, hand-written): out[j] = the j-th
+// i < n (ascending) with flags[i] != 0, as in[i] (in = null: i itself);
+// *d_num = the count.  temp: compact_temp_bytes() bytes
+size_t compact_temp_bytes();
+int compact_flagged(const uint32_t* in, const uint8_t* flags, long long n, uint32_t* out, int* d_num, void* d_temp,
+                    cudaStream_t st);
 // rows (w32 words) + uint16 map ids -> key rows
 int canon_pack(const uint32_t* d_bits, const uint16_t* d_map, long long count, int w32, uint32_t* d_keys,
                cudaStream_t st);
