@@ -193,6 +193,8 @@ struct wpm_plan {
     DevBuf<unsigned long long> d_qready, d_qctl;
     int qcap = 0, recw = 0;
     DevBuf<int32_t> d_task_map, d_task_f, d_task_kind;
+    DevBuf<int32_t> d_map_first;  // root tasks per map, prefix (the per-map queues)
+    std::vector<int32_t> h_map_first;
     // outputs
     DevBuf<uint32_t> d_out_keys, d_sorted_bits;  // key rows from kernel 3; canonical rows
     DevBuf<uint16_t> d_sorted_map;
@@ -841,20 +843,9 @@ struct K3Launch {
 static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
     const long long nseed = L.d_recs ? L.nrecs : L.ntasks;
     const long long nroots = L.claim_recs ? L.claim_count : nseed;
-    int qcap = 1 << 16;
-    while (qcap < 2 * nseed) qcap <<= 1;
-    if (qcap > P->qcap) {
-        P->qcap = qcap;
-        if (P->d_qrec.ensure((size_t)qcap * P->recw) || P->d_qready.ensure(qcap))
-            return fail(WPM_EINTERNAL, "device allocation failed (queue)");
-    }
     const bool prog = L.progress && P->progress_fn;
     if (prog && P->d_root_pend.ensure((size_t)std::max<long long>(nroots, 1)))
         return fail(WPM_EINTERNAL, "device allocation failed (progress)");
-    unsigned long long ctl[3] = {(unsigned long long)nseed << 32, 0, (unsigned long long)nseed};
-    CU(cudaMemcpyAsync(P->d_qctl.p, ctl, sizeof(ctl), cudaMemcpyHostToDevice, P->stream));  // [3], [4] add up
-    CU(cudaMemsetAsync(P->d_qready.p, 0, (size_t)P->qcap * 8, P->stream));
-    P->h2d += (long long)sizeof(ctl);
     SearchParams sp{};
     sp.num_maps = P->num_maps;
     sp.max_M = P->maxM;
@@ -867,10 +858,6 @@ static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
     sp.fr_words = P->fr_words;
     sp.rp_words = P->rp_words;
     sp.npar = P->d_npar.p;
-    sp.qrec = P->d_qrec.p;
-    sp.qready = P->d_qready.p;
-    sp.qctl = P->d_qctl.p;
-    sp.qcap = P->qcap;
     sp.recw = P->recw;
     sp.mw = P->mw;
     sp.out_keys = P->d_out_keys.p;
@@ -886,6 +873,44 @@ static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
     sp.claim_recs = L.claim_recs;
     sp.claim_count = L.claim_count;
     sp.claim_ctr = L.claim_ctr;
+    // the queue: one ring, or one per map when the kernel keeps a single map's
+    // tables per CTA (k3_map_queues); the root tasks' map-major order gives
+    // each map its seed slots
+    int ma_tab = 0;
+    for (const MapDesc& d : P->desc)
+        ma_tab = std::max(ma_tab, ((2 * d.M * d.fr_stride + 15) & ~15) + ((2 * d.N * d.rp_stride + 15) & ~15));
+    sp.ma_tab_bytes = ma_tab;
+    sp.map_first = P->d_map_first.p;
+    sp.map_queues = !L.d_recs && L.ntasks > 0 && !P->has_pins && k3_map_queues(sp);
+    const int nq = sp.map_queues ? P->num_maps : 1;
+    long long qcap = sp.map_queues ? 1 << 14 : 1 << 16;  // > pending: 2 x warps + seeds
+    while (qcap < 2 * (sp.map_queues ? P->maxM : nseed)) qcap <<= 1;
+    if (P->d_qrec.ensure((size_t)nq * qcap * P->recw) || P->d_qready.ensure((size_t)nq * qcap) ||
+        P->d_qctl.ensure(8 * (size_t)(nq + 1)))
+        return fail(WPM_EINTERNAL, "device allocation failed (queue)");
+    P->qcap = (int)qcap;
+    sp.qrec = P->d_qrec.p;
+    sp.qready = P->d_qready.p;
+    sp.qctl = P->d_qctl.p;
+    sp.qcap = P->qcap;
+    {
+        unsigned long long ctl[3] = {(unsigned long long)nseed << 32, 0, (unsigned long long)nseed};
+        if (sp.map_queues) ctl[0] = ctl[2] = 0;  // plan-wide words only
+        CU(cudaMemcpyAsync(P->d_qctl.p, ctl, sizeof(ctl), cudaMemcpyHostToDevice, P->stream));  // [3], [4] add up
+        P->h2d += (long long)sizeof(ctl);
+        if (sp.map_queues) {
+            const std::vector<int32_t>& first = P->h_map_first;
+            std::vector<unsigned long long> qc(8 * (size_t)nq, 0);
+            for (int q = 0; q < nq; ++q) {
+                const unsigned long long c = (unsigned long long)(first[q + 1] - first[q]);
+                qc[8 * q] = c << 32;
+                qc[8 * q + 2] = c;
+            }
+            CU(cudaMemcpyAsync(P->d_qctl.p + 8, qc.data(), qc.size() * 8, cudaMemcpyHostToDevice, P->stream));
+            P->h2d += (long long)qc.size() * 8;
+        }
+        CU(cudaMemsetAsync(P->d_qready.p, 0, (size_t)nq * qcap * 8, P->stream));
+    }
     if (prog) {
         sp.root_pend = P->d_root_pend.p;
         sp.roots_done = P->d_acc.p;
@@ -903,6 +928,7 @@ static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
     }
     const int est_warps = P->num_sms * 16;
     sp.hungry = std::max(64, est_warps / 2);
+    if (sp.map_queues) sp.hungry = 128;  // per map queue (measured 8..128: within 1 %, 128 best at n = 7, 8)
     sp.backoff_min = 32;
     sp.backoff_max = 8192;
     if (const char* e = std::getenv("WPM_BACKOFF_MIN")) sp.backoff_min = std::max(1, std::atoi(e));
@@ -979,7 +1005,7 @@ static int search_prepare(wpm_plan* P, int shard_index, int shard_count) {
     root_tasks(P, shard_index, shard_count, &tm, &tf, &tk);
     const int ntasks = (int)tm.size();
     P->ntasks = ntasks;
-    if (P->d_qctl.ensure(8) || P->d_acc.ensure(4) || P->d_task_map.ensure(ntasks + 1) ||
+    if (P->d_qctl.ensure(8 * (size_t)(K + 1)) || P->d_acc.ensure(4) || P->d_task_map.ensure(ntasks + 1) ||
         P->d_task_f.ensure(ntasks + 1) || P->d_task_kind.ensure(ntasks + 1) || P->d_out_ctl.ensure(4) ||
         P->d_per_map.ensure(K) || P->d_front_ctl.ensure(2))
         return fail(WPM_EINTERNAL, "device allocation failed (queue)");
@@ -990,6 +1016,15 @@ static int search_prepare(wpm_plan* P, int shard_index, int shard_count) {
         CU(cudaMemcpyAsync(P->d_pin_out.p, P->pin_out.data(), P->mw * 4, cudaMemcpyHostToDevice, P->stream));
     }
     tr.mark("    prepare: small buffers");
+    {  // root tasks are map-major: map q's are [first[q], first[q + 1])
+        std::vector<int32_t> first(K + 1, 0);
+        for (int t = 0; t < ntasks; ++t) ++first[tm[t] + 1];
+        for (int q = 0; q < K; ++q) first[q + 1] += first[q];
+        if (P->d_map_first.ensure(K + 1)) return fail(WPM_EINTERNAL, "device allocation failed (queue)");
+        P->h_map_first = first;
+        CU(cudaMemcpyAsync(P->d_map_first.p, P->h_map_first.data(), (K + 1) * 4, cudaMemcpyHostToDevice, P->stream));
+        P->h2d += 4LL * (K + 1);
+    }
     if (ntasks) {
         CU(cudaMemcpyAsync(P->d_task_map.p, tm.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
         CU(cudaMemcpyAsync(P->d_task_f.p, tf.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));

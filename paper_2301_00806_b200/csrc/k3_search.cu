@@ -77,10 +77,16 @@ constexpr int a16(int x) { return (x + 15) & ~15; }
 // shared memory at kernel start and read with LDS (they are the L1-missing
 // loads of the global-table layout: 20-27 % long-scoreboard stalls); the CTA
 // then holds WPBV warps sharing one copy.  Used when every map's tables fit.
-template <int NMAX, int MMAX, int DMAX, bool TSM = false, int WPBV = 4, int MINBV = 0>
+// MAV (map-affine, TSM layouts only): one work queue per map; a CTA works on
+// one map at a time with only THAT map's tables in shared memory, and moves to
+// the map with the most pending tasks per CTA once its map is finished -- the
+// TS layout for plans whose maps' tables do not fit together (n = 7, 8).
+template <int NMAX, int MMAX, int DMAX, bool TSM = false, int WPBV = 4, int MINBV = 0, bool MAV = false>
 struct LC {
     static constexpr int kN = NMAX, kM = MMAX, kDepth = DMAX;
     static constexpr bool TS = TSM;
+    static constexpr bool MA = MAV;
+    static_assert(!MAV || TSM, "map-affine layouts keep the tables in shared memory");
     static constexpr int WPB = WPBV;
     static constexpr int NP = a16(NMAX + 32), MP = a16(MMAX + 32);
     static constexpr int NW = (NMAX + 31) / 32, MW = (MMAX + 31) / 32;
@@ -128,8 +134,11 @@ using C11T = LC<2688, 840, FRAME_CAP, true, 24, 1>;  // n = 11: ~48 KB
 // any (m, n) = (15, 11) universe (the synthetic band, up to all 1365 11-subsets)
 using C15 = LC<3008, 1368, FRAME_CAP>;
 using C15T = LC<3008, 1368, FRAME_CAP, true, 18, 1>;
+using C7M = LC<420, 208, FRAME_CAP, true, 20, 2, true>;   // n = 7: one map's tables (~8 KB) per CTA
+using C8M = LC<720, 312, FRAME_CAP, true, 20, 2, true>;   // n = 8: ~14 KB
+// (10 x 4 and 8 x 5 warps x CTAs measured within 1 % of 20 x 2 at n = 7, 8)
 // (n = 9's seven maps need ~140 KB of tables: 16 warps per SM measured 34 %
-// slower than the global-table layout at 32 -- no TS variant for n = 7..9)
+// slower than the global-table layout at 32 -- no all-maps TS variant for n = 7..9)
 using CGF = LC<4096, 2048, 2050>;         // full depth: the rerun after a frame overflow
 
 struct MapView {
@@ -174,6 +183,23 @@ struct WS {
 };
 
 __device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) - 1u; }
+
+// the work queue of map q: its control words ([0] tail << 32 | head, [1] CTAs
+// on the map, [2] pending), ready flags and record ring.  Map-affine layouts
+// keep one queue per map after the plan-wide counters (qctl[0..7]); the others
+// one queue in qctl[0..7] itself
+template <class C>
+__device__ __forceinline__ unsigned long long* q_ctl(const SearchParams& p, int q) {
+    return C::MA ? p.qctl + 8 * (q + 1) : p.qctl;
+}
+template <class C>
+__device__ __forceinline__ unsigned long long* q_ready(const SearchParams& p, int q) {
+    return C::MA ? p.qready + (size_t)q * p.qcap : p.qready;
+}
+template <class C>
+__device__ __forceinline__ uint32_t* q_rec(const SearchParams& p, int q) {
+    return C::MA ? p.qrec + (size_t)q * p.qcap * p.recw : p.qrec;
+}
 
 // per-map table reads: the k-th ridge of a facet (fr), the q-th candidate
 // facet of a ridge (rp); LDS for the shared-memory layouts, LDG otherwise
@@ -733,13 +759,14 @@ __device__ __forceinline__ bool try_donate(WS<C>& w, const MapView& mp, const Se
         if (!any) continue;
         // claim a push ticket (high half of the queue word)
         unsigned long long t = 0;
+        unsigned long long* qc = q_ctl<C>(p, mp.map);
         if (lane == 0) {
-            atomicAdd(&p.qctl[2], 1ull);  // pending, before publishing
+            atomicAdd(&qc[2], 1ull);  // pending, before publishing
             if (p.root_pend) atomicAdd(&p.root_pend[w.root()], 1u);
-            t = atomicAdd(&p.qctl[0], 1ull << 32) >> 32;
+            t = atomicAdd(&qc[0], 1ull << 32) >> 32;
         }
         t = __shfl_sync(FULL, t, 0);
-        uint32_t* rec = p.qrec + (t % (unsigned long long)p.qcap) * (unsigned long long)p.recw;
+        uint32_t* rec = q_rec<C>(p, mp.map) + (t % (unsigned long long)p.qcap) * (unsigned long long)p.recw;
         if (lane == 0) {
             rec[0] = (uint32_t)mp.map | ((ridge == CLOSED_FRAME ? (uint32_t)T_CLOSED : (uint32_t)T_OPEN) << 24);
             rec[1] = ridge;
@@ -765,7 +792,7 @@ __device__ __forceinline__ bool try_donate(WS<C>& w, const MapView& mp, const Se
         __threadfence();
         __syncwarp();
         if (lane == 0) {
-            atomicExch(&p.qready[t % (unsigned long long)p.qcap], t + 1ull);
+            atomicExch(&q_ready<C>(p, mp.map)[t % (unsigned long long)p.qcap], t + 1ull);
             w.frames()[d].x = ridge | (POS_DONE << 16);  // exhausted here
         }
         __syncwarp();
@@ -774,13 +801,82 @@ __device__ __forceinline__ bool try_donate(WS<C>& w, const MapView& mp, const Se
     return false;
 }
 
+// map-affine layouts: the CTA's next map, chosen by warp 0 while the CTA
+// waits -- first the map whose seeds hold this CTA's share of all root tasks,
+// later the unfinished map with the most pending tasks per CTA on it -- and
+// its tables loaded into shared memory.  -1: no map has work left (or the
+// node budget is spent).
+template <class C>
+__device__ int ma_next_map(const SearchParams& p, int prev, uint8_t* smem, int* s_map) {
+    __syncthreads();  // every warp is done with the previous map's tables
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int pick = -1;
+        if (prev < 0) {
+            if (lane == 0) {
+                const long long total = p.map_first[p.num_maps];
+                const long long target = ((2LL * blockIdx.x + 1) * total) / (2LL * gridDim.x);
+                int q = 0;
+                while (q + 1 < p.num_maps && p.map_first[q + 1] <= target) ++q;
+                pick = q;
+            }
+        } else {
+            if (lane == 0) atomicAdd(&q_ctl<C>(p, prev)[1], (unsigned long long)-1ll);
+            const bool stop = p.node_budget && ld_relaxed_u64(&p.out_ctl[3]);
+            unsigned long long bp = 0, bo = 1;
+            int bq = -1;
+            #pragma unroll 1
+            for (int q = lane; q < p.num_maps && !stop; q += 32) {
+                const unsigned long long pend = ld_relaxed_u64(&q_ctl<C>(p, q)[2]);
+                if (!pend) continue;
+                const unsigned long long on = ld_relaxed_u64(&q_ctl<C>(p, q)[1]) + 1ull;
+                if (bq < 0 || pend * bo > bp * on) {
+                    bp = pend;
+                    bo = on;
+                    bq = q;
+                }
+            }
+            #pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const unsigned long long op = __shfl_down_sync(FULL, bp, o), oo = __shfl_down_sync(FULL, bo, o);
+                const int oq = __shfl_down_sync(FULL, bq, o);
+                if (oq >= 0 && (bq < 0 || op * bo > bp * oo)) {
+                    bp = op;
+                    bo = oo;
+                    bq = oq;
+                }
+            }
+            pick = bq;
+        }
+        if (lane == 0) {
+            if (pick >= 0) atomicAdd(&q_ctl<C>(p, pick)[1], 1ull);
+            *s_map = pick;
+        }
+    }
+    __syncthreads();
+    const int q = *s_map;
+    if (q >= 0) {
+        const MapDesc md = p.maps[q];
+        const int nf = md.M * md.fr_stride, nr = md.N * md.rp_stride;
+        uint16_t* dfr = reinterpret_cast<uint16_t*>(smem);
+        uint16_t* drp = reinterpret_cast<uint16_t*>(smem + a16(2 * nf));
+        #pragma unroll 1
+        for (int i = threadIdx.x; i < nf; i += blockDim.x) dfr[i] = __ldg(p.fr + md.fr_off + i);
+        #pragma unroll 1
+        for (int i = threadIdx.x; i < nr; i += blockDim.x) drp[i] = __ldg(p.rp + md.rp_off + i);
+    }
+    __syncthreads();
+    return q;
+}
+
 template <class C>
 __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __grid_constant__ SearchParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    // TS layouts: every map's fr then rp tables at the CTA's base, then the warps
-    const int tab_bytes = C::TS ? 16 * (((p.fr_words + 7) >> 3) + ((p.rp_words + 7) >> 3)) : 0;
-    if constexpr (C::TS) {
+    // TS layouts: every map's fr then rp tables at the CTA's base, then the
+    // warps; map-affine layouts: the current map's tables only
+    const int tab_bytes = C::TS ? (C::MA ? p.ma_tab_bytes : 16 * (((p.fr_words + 7) >> 3) + ((p.rp_words + 7) >> 3))) : 0;
+    if constexpr (C::TS && !C::MA) {
         const uint4* src_fr = reinterpret_cast<const uint4*>(p.fr);
         const uint4* src_rp = reinterpret_cast<const uint4*>(p.rp);
         uint4* dfr = reinterpret_cast<uint4*>(smem);
@@ -801,6 +897,13 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
     unsigned long long prof_busy = 0, prof_wait = 0, prof_t = clock64();
 #endif
 
+    __shared__ int s_map;
+    int cur = 0;  // the CTA's map (map-affine layouts); queue 0 otherwise
+    if constexpr (C::MA) cur = ma_next_map<C>(p, -1, smem, &s_map);
+    while (cur >= 0) {
+    unsigned long long* const qc = q_ctl<C>(p, cur);
+    unsigned long long* const qrdy = q_ready<C>(p, cur);
+    uint32_t* const qrec = q_rec<C>(p, cur);
     for (;;) {
         // ---- pop: a ticket queue.  One atomicAdd on the low half of the
         // queue word claims ticket t; the warp waits on ITS slot until the
@@ -811,14 +914,14 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
         // queue while this GPU runs low (pending < claim_low), and leaves only
         // once the shared frontier is exhausted too.
         unsigned long long tk = 0;
-        if (lane == 0) tk = atomicAdd(&p.qctl[0], 1ull) & 0xFFFFFFFFull;
+        if (lane == 0) tk = atomicAdd(&qc[0], 1ull) & 0xFFFFFFFFull;
         long long t = -1;
         bool exhausted = p.claim_recs == nullptr;
         for (;;) {
             long long claim = -1;
             if (lane == 0) {
-                volatile unsigned long long* rdy = p.qready + (tk % (unsigned long long)p.qcap);
-                volatile unsigned long long* pend = p.qctl + 2;
+                volatile unsigned long long* rdy = qrdy + (tk % (unsigned long long)p.qcap);
+                volatile unsigned long long* pend = qc + 2;
                 unsigned backoff = (unsigned)p.backoff_min;
                 if (exhausted) {  // no shared frontier to claim from: the tight ticket wait
                     for (;;) {
@@ -843,7 +946,7 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
                         // (a plain read first: idle warps polling must not hammer the
                         // pending counter the busy warps update -- measured +30 % claim
                         // time at 12.7 k records without it)
-                        if (atomicAdd(&p.qctl[2], 1ull) < (unsigned long long)p.claim_low) {
+                        if (atomicAdd(&qc[2], 1ull) < (unsigned long long)p.claim_low) {
                             const unsigned long long i = atomicAdd_system(p.claim_ctr, 1ull);
                             if (i < (unsigned long long)p.claim_count) {
                                 claim = (long long)i;  // pending already counts it
@@ -851,7 +954,7 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
                             }
                             exhausted = true;
                         }
-                        atomicAdd(&p.qctl[2], (unsigned long long)-1ll);
+                        atomicAdd(&qc[2], (unsigned long long)-1ll);
                         if (!exhausted) {
                             unsigned long long c;
                             asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(c) : "l"(p.claim_ctr));
@@ -871,14 +974,14 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
             if (claim < 0) break;
             // push the claimed frontier record (root id = its frontier index)
             unsigned long long pt = 0;
-            if (lane == 0) pt = atomicAdd(&p.qctl[0], 1ull << 32) >> 32;
+            if (lane == 0) pt = atomicAdd(&qc[0], 1ull << 32) >> 32;
             pt = __shfl_sync(FULL, pt, 0);
             const uint32_t* src = p.claim_recs + (unsigned long long)claim * p.recw;
-            uint32_t* dst = p.qrec + (pt % (unsigned long long)p.qcap) * (unsigned long long)p.recw;
+            uint32_t* dst = qrec + (pt % (unsigned long long)p.qcap) * (unsigned long long)p.recw;
             for (int i = lane; i < p.recw; i += 32) dst[i] = i == 3 ? (uint32_t)claim : __ldcg(src + i);
             __threadfence();
             __syncwarp();
-            if (lane == 0) atomicExch(&p.qready[pt % (unsigned long long)p.qcap], pt + 1ull);
+            if (lane == 0) atomicExch(&qrdy[pt % (unsigned long long)p.qcap], pt + 1ull);
         }
         t = __shfl_sync(FULL, t, 0);
 #ifdef WPM_PROFILE
@@ -901,7 +1004,7 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
             if (lane == 0) spent = ld_relaxed_u64(&p.out_ctl[3]) != 0ull;
             if (__shfl_sync(FULL, spent, 0)) break;
         }
-        const uint32_t* rec = p.qrec + slot * (unsigned long long)p.recw;
+        const uint32_t* rec = qrec + slot * (unsigned long long)p.recw;
         const uint32_t h0 = __ldcg(rec), h1 = __ldcg(rec + 1), h2 = __ldcg(rec + 2), h3 = __ldcg(rec + 3);
         if (lane == 0) {
             reinterpret_cast<int*>(w.base + C::META)[0] = (int)(h2 >> 16);
@@ -922,8 +1025,13 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
         mp.lpf_shift = md.n <= 4 ? 2 : (md.n <= 8 ? 3 : 4);
         mp.fr = p.fr + md.fr_off;
         mp.rp = p.rp + md.rp_off;
-        mp.frs = tab_s + 2u * md.fr_off;
-        mp.rps = rp_s + 2u * md.rp_off;
+        if constexpr (C::MA) {  // map == cur: its tables alone, fr then rp
+            mp.frs = tab_s;
+            mp.rps = tab_s + (uint32_t)a16(2 * md.M * md.fr_stride);
+        } else {
+            mp.frs = tab_s + 2u * md.fr_off;
+            mp.rps = rp_s + 2u * md.rp_off;
+        }
         mp.fs = md.fr_stride;
         mp.ps = md.rp_stride;
         ++tasks;
@@ -950,7 +1058,7 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
             }
         }
         // ---- the DFS over branch frames
-        unsigned long long qword = ld_relaxed_u64(&p.qctl[0]);  // prefetched queue state
+        unsigned long long qword = ld_relaxed_u64(&qc[0]);  // prefetched queue state
         unsigned long long next_check = nodes + (unsigned)p.check_every;
         unsigned long long flushed = nodes;  // node-budget mode: count already in qctl[1]
         while (w.depth > 0) {
@@ -1010,7 +1118,7 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
                     for (int i = 0; i < k; ++i)
                         if (!try_donate(w, mp, p, lane)) break;
                 }
-                qword = ld_relaxed_u64(&p.qctl[0]);  // consumed at the next check
+                qword = ld_relaxed_u64(&qc[0]);  // consumed at the next check
                 if (p.node_budget) {
                     int stop = 0;
                     if (lane == 0) {
@@ -1032,7 +1140,7 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
                 if (p.progress_host)  // host takes the max of what it sees
                     asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p.progress_host), "l"(d) : "memory");
             }
-            atomicAdd(&p.qctl[2], (unsigned long long)-1ll);
+            atomicAdd(&qc[2], (unsigned long long)-1ll);
         }
 #ifdef WPM_PROFILE
         {
@@ -1041,6 +1149,9 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
             prof_t = now;
         }
 #endif
+    }
+    if constexpr (C::MA) cur = ma_next_map<C>(p, cur, smem, &s_map);
+    else break;
     }
     if (lane == 0) {
         atomicAdd(&p.qctl[3], tasks);
@@ -1060,7 +1171,9 @@ __global__ void seed_tasks(SearchParams p, int ntasks, const int32_t* __restrict
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (t >= ntasks) return;
     const int map = task_map[t], f = task_f[t], kind = task_kind[t];
-    uint32_t* rec = p.qrec + (size_t)t * p.recw;
+    // map queues: task t is slot t - map_first[map] of its map's queue
+    const size_t slot = p.map_queues ? (size_t)map * p.qcap + (size_t)(t - p.map_first[map]) : (size_t)t;
+    uint32_t* rec = p.qrec + slot * p.recw;
     if (lane == 0) {
         rec[0] = (uint32_t)map | ((uint32_t)kind << 24);
         rec[1] = (uint32_t)f;
@@ -1080,7 +1193,7 @@ __global__ void seed_tasks(SearchParams p, int ntasks, const int32_t* __restrict
         rec[4 + i] = in;
         rec[4 + p.mw + i] = out;
     }
-    if (lane == 0) p.qready[t] = (unsigned long long)t + 1ull;
+    if (lane == 0) p.qready[slot] = (unsigned long long)(p.map_queues ? t - p.map_first[map] : t) + 1ull;
 }
 
 // seed the queue with task records (a frontier): record i -> ticket i, root id i
@@ -1101,7 +1214,7 @@ template <class C>
 int launch_class(const SearchParams& p, int num_sms, cudaStream_t st, int* warps_out) {
     const int wpb = C::WPB;  // warps per CTA
     // fr and rp each padded to 16 bytes (the kernel's layout)
-    const size_t tab = C::TS ? (size_t)16 * (((p.fr_words + 7) >> 3) + ((p.rp_words + 7) >> 3)) : 0;
+    const size_t tab = !C::TS ? 0 : C::MA ? (size_t)p.ma_tab_bytes : (size_t)16 * (((p.fr_words + 7) >> 3) + ((p.rp_words + 7) >> 3));
     const size_t smem = tab + (size_t)C::BYTES * wpb;
     if (cudaFuncSetAttribute(k3_search<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return 0;
@@ -1152,8 +1265,22 @@ int launch_seed_records(const SearchParams& p, const uint32_t* d_recs, long long
 // a TS layout fits if its CTAs (tables + warps) fit the SM's shared memory
 template <class C>
 bool ts_fits(const SearchParams& p) {
-    const size_t tab = (size_t)16 * (((p.fr_words + 7) >> 3) + ((p.rp_words + 7) >> 3));
-    return (size_t)C::MIN_BLOCKS * (tab + (size_t)C::BYTES * C::WPB) <= 227u * 1024u;
+    const size_t tab = C::MA ? (size_t)p.ma_tab_bytes : (size_t)16 * (((p.fr_words + 7) >> 3) + ((p.rp_words + 7) >> 3));
+    return (size_t)C::MIN_BLOCKS * (tab + (size_t)C::BYTES * C::WPB + 64) <= 227u * 1024u;
+}
+
+// the layout the plan's kernel 3 would use takes one queue per map (the host
+// then seeds the map queues: SearchParams::map_queues)
+bool k3_map_queues(const SearchParams& p) {
+    const char* e = std::getenv("WPM_MAPQ");
+    if (e && std::atoi(e) == 0) return false;
+    const char* ts_env = std::getenv("WPM_TS");
+    if (ts_env && std::atoi(ts_env) == 0) return false;
+    if (p.max_depth > FRAME_CAP || p.cutoff > 0 || p.claim_recs) return false;
+    const int N = p.max_N, M = p.max_M;
+    if (N > C6::kN && N <= C7M::kN && M <= C7M::kM) return ts_fits<C7M>(p);
+    if (N > C7::kN && N <= C8M::kN && M <= C8M::kM) return ts_fits<C8M>(p);
+    return false;
 }
 
 // the smallest size class that holds the plan (max_depth > FRAME_CAP asks for
@@ -1166,6 +1293,10 @@ int launch_k3_search(const SearchParams& p, int num_sms, cudaStream_t st, int* w
     const bool ts_on = !ts_env || std::atoi(ts_env) != 0;
     if (ts_on) {
         if (N <= C5T::kN && M <= C5T::kM && ts_fits<C5T>(p)) return launch_class<C5T>(p, num_sms, st, warps_out);
+        if (p.map_queues) {
+            if (N <= C7M::kN && M <= C7M::kM) return launch_class<C7M>(p, num_sms, st, warps_out);
+            return launch_class<C8M>(p, num_sms, st, warps_out);
+        }
         if (N <= C6T::kN && M <= C6T::kM && N > C5T::kN && ts_fits<C6T>(p))
             return launch_class<C6T>(p, num_sms, st, warps_out);
         if (N <= C10T::kN && M <= C10T::kM && N > C9::kN && ts_fits<C10T>(p))

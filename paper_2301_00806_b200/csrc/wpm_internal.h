@@ -68,7 +68,14 @@ struct SearchParams {
     unsigned long long* roots_done;
     unsigned long long* progress_host;
     unsigned long long* root_nodes;  // optional: search nodes per root task / frontier record
+    // one queue per map (k3_map_queues): queue q = qctl[8 (q + 1) ..], qready
+    // / qrec from q * qcap; root task t of map q is slot t - map_first[q]
+    int map_queues;
+    int ma_tab_bytes;          // shared bytes of the largest map's fr + rp tables (16-byte padded each)
+    const int32_t* map_first;  // num_maps + 1 prefix of root tasks per map
 };
+// kernel 3 for this plan runs one queue per map (see SearchParams::map_queues)
+bool k3_map_queues(const SearchParams& p);
 
 // task record header (queue, frontier): [0] map | kind << 24, [1] facet or
 // ridge, [2] resume position | absolute branch depth << 16, [3] root task id;
