@@ -598,8 +598,8 @@ static int plan_build_tables(wpm_plan* P, const std::vector<uint32_t>& foff) {
                    std::to_string(P->has_pins ? 1 : 0);
     for (int i = 0; i < K; ++i) P->signature += ":" + std::to_string(P->M[i]) + "," + std::to_string(P->N[i]);
     P->mw = (P->maxM + 31) / 32;
-    P->w32 = 2 * ((P->maxM + 63) / 64);
-    P->rw = rec_words(P->w32);
+    P->w32 = 2 * ((P->maxM + 63) / 64);  // C-ABI rows: whole 64-bit words
+    P->rw = rec_words(P->mw);             // emitted records: the mw words the bitsets use + the map id
     P->recw = 4 + 2 * P->mw;
     CU(cudaStreamSynchronize(P->stream));
     return WPM_OK;
@@ -1214,7 +1214,7 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
 static int plan_sort_launch(wpm_plan* P, bool device_count) {
     const int K = P->num_maps;
     const long long rows = device_count ? (long long)P->out_cap : P->total;
-    const size_t tb = canon_sort_temp_bytes(std::max<long long>(rows, 1), P->w32);
+    const size_t tb = canon_sort_temp_bytes(std::max<long long>(rows, 1), P->mw);
     if (P->d_temp.ensure(tb) || P->d_sorted_bits.ensure((size_t)rows * P->w32 + 1) || P->d_sorted_map.ensure(rows + 1))
         return fail(WPM_EINTERNAL, "device allocation failed (sort)");
     CU(cudaMemsetAsync(P->d_out_ctl.p + 1, 0, 8, P->stream));
@@ -1228,9 +1228,9 @@ static int plan_sort_launch(wpm_plan* P, bool device_count) {
         auto it = g_rows_seen.find(P->signature);
         if (it != g_rows_seen.end()) hint = it->second + it->second / 8 + 64;
     }
-    if (canon_sort_keys(P->d_out_keys.p, rows, P->w32, P->d_sorted_bits.p, P->d_sorted_map.p, P->d_temp.p,
+    if (canon_sort_keys(P->d_out_keys.p, rows, P->mw, P->d_sorted_bits.p, P->d_sorted_map.p, P->d_temp.p,
                         P->d_temp.n, (long long*)P->d_per_map.p, P->d_out_ctl.p + 1, P->stream,
-                        device_count ? P->d_out_ctl.p : nullptr, hint))
+                        device_count ? P->d_out_ctl.p : nullptr, hint, P->w32))
         return fail(WPM_EINTERNAL, std::string("canonical sort: ") + cudaGetErrorString(cudaGetLastError()));
     CU(cudaEventRecord(P->ev[3], P->stream));
     // results of the sort, read back with the next synchronisation

@@ -47,6 +47,7 @@ struct SortParams {
     long long count;                      // rows, or the cap of *count_dev
     const unsigned long long* count_dev;  // optional: the row count on the device
     int w32, rw;
+    int ow;                // words per output row (>= w32; zero beyond w32)
     int tile;              // records per phase-1 tile (power of two)
     int chunk;             // output records per merge chunk (<= tile)
     uint32_t* out_bits;    // count * w32
@@ -228,9 +229,10 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k4_sort(const __grid_constant
     }
     // ---- phase 3: the C-ABI layout, group boundaries, duplicates
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N * w32; i += stride) {
-        const long long r = i / w32, c = i - r * w32;
-        p.out_bits[i] = src[(size_t)r * rw + c];
+    const int ow = p.ow;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < N * ow; i += stride) {
+        const long long r = i / ow, c = i - r * ow;
+        p.out_bits[i] = c < w32 ? src[(size_t)r * rw + c] : 0u;
     }
     unsigned long long nd = 0;
     for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += stride) {
@@ -262,16 +264,18 @@ size_t canon_sort_temp_bytes(long long count, int w32) {
 
 int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sorted_bits, uint16_t* d_sorted_map,
                     void* d_temp, size_t temp_bytes, long long* d_first_row, unsigned long long* d_dups,
-                    cudaStream_t st, const unsigned long long* d_count, long long grid_rows) {
+                    cudaStream_t st, const unsigned long long* d_count, long long grid_rows, int out_words) {
     return canon_sort_records(d_keys, count, w32, rec_words(w32), -1, d_sorted_bits, d_sorted_map, nullptr, d_temp,
-                              temp_bytes, d_first_row, d_dups, st, d_count, grid_rows);
+                              temp_bytes, d_first_row, d_dups, st, d_count, grid_rows, out_words);
 }
 
 int canon_sort_records(uint32_t* d_keys, long long count, int w32, int rw, int tie, uint32_t* d_sorted_bits,
                        uint16_t* d_sorted_map, uint32_t* d_payload, void* d_temp, size_t temp_bytes,
                        long long* d_first_row, unsigned long long* d_dups, cudaStream_t st,
-                       const unsigned long long* d_count, long long grid_rows) {
+                       const unsigned long long* d_count, long long grid_rows, int out_words) {
     if (count <= 0) return 0;
+    if (out_words <= 0) out_words = w32;
+    if (out_words < w32) return 1;
     if (rw % 4 || rw < w32 + 1) return 1;
     if (temp_bytes < (size_t)2 * (size_t)count * (size_t)rw * 4) return 1;
     int dev = 0;
@@ -311,6 +315,7 @@ int canon_sort_records(uint32_t* d_keys, long long count, int w32, int rw, int t
     sp.count_dev = d_count;
     sp.w32 = w32;
     sp.rw = rw;
+    sp.ow = out_words;
     sp.tile = T;
     sp.chunk = Cc;
     sp.out_bits = d_sorted_bits;

@@ -93,7 +93,8 @@ __device__ __forceinline__ void flush_queue(const OdoParams& p, const uint32_t* 
         if (slot < p.out_cap) {
             uint32_t* row = p.out_keys + slot * (unsigned long long)p.rw;
 #pragma unroll
-            for (int w = 0; w < W; ++w) row[w] = K[w];
+            for (int w = 0; w < W; ++w)
+                if (w < p.rw - 1) row[w] = K[w];  // (words past the plan's mw are zero)
             for (int w = W; w < p.rw - 1; ++w) row[w] = 0u;
             row[p.rw - 1] = (uint32_t)map;
         }

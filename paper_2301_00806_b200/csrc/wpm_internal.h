@@ -105,7 +105,8 @@ size_t canon_sort_temp_bytes(long long count, int w32);
 // capped at `count`, which then only sizes the launch)
 int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sorted_bits, uint16_t* d_sorted_map,
                     void* d_temp, size_t temp_bytes, long long* d_first_row, unsigned long long* d_dups,
-                    cudaStream_t st, const unsigned long long* d_count = nullptr, long long grid_rows = 0);
+                    cudaStream_t st, const unsigned long long* d_count = nullptr, long long grid_rows = 0,
+                    int out_words = 0);
 // the general form: records of rw words (a multiple of 4, >= w32 + 1; the
 // map id last), compared on (map, w32 bitset words) and then -- tie >= 0 --
 // on word `tie` (a payload carried through the sort, written to d_payload);
@@ -113,7 +114,11 @@ int canon_sort_keys(uint32_t* d_keys, long long count, int w32, uint32_t* d_sort
 int canon_sort_records(uint32_t* d_keys, long long count, int w32, int rw, int tie, uint32_t* d_sorted_bits,
                        uint16_t* d_sorted_map, uint32_t* d_payload, void* d_temp, size_t temp_bytes,
                        long long* d_first_row, unsigned long long* d_dups, cudaStream_t st,
-                       const unsigned long long* d_count = nullptr, long long grid_rows = 0);
+                       const unsigned long long* d_count = nullptr, long long grid_rows = 0,
+                       int out_words = 0);
+// (out_words > w32: sorted_bits rows of out_words words, zero beyond w32 --
+// kernel 3 emits only the mw words a plan's bitsets use, the C-ABI rows are
+// whole 64-bit words)
 // stream compaction (one cooperative launch, hand-written): out[j] = the j-th
 // i < n (ascending) with flags[i] != 0, as in[i] (in = null: i itself);
 // *d_num = the count.  temp: compact_temp_bytes() bytes
