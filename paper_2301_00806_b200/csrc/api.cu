@@ -197,6 +197,8 @@ struct wpm_plan {
     std::vector<int32_t> h_map_first;
     // outputs
     DevBuf<uint32_t> d_out_keys, d_sorted_bits;  // key rows from kernel 3; canonical rows
+    DevBuf<uint32_t> d_bucket;  // bucketed-sort scratch (its count block stays zero between sorts)
+    long long bucket_cap = -1, bucket_facets = -1;  // the layout the zeroed count block belongs to
     DevBuf<uint16_t> d_sorted_map;
     DevBuf<unsigned long long> d_out_ctl, d_per_map;
     DevBuf<uint8_t> d_temp;
@@ -1228,10 +1230,32 @@ static int plan_sort_launch(wpm_plan* P, bool device_count) {
         auto it = g_rows_seen.find(P->signature);
         if (it != g_rows_seen.end()) hint = it->second + it->second / 8 + 64;
     }
-    if (canon_sort_keys(P->d_out_keys.p, rows, P->mw, P->d_sorted_bits.p, P->d_sorted_map.p, P->d_temp.p,
-                        P->d_temp.n, (long long*)P->d_per_map.p, P->d_out_ctl.p + 1, P->stream,
-                        device_count ? P->d_out_ctl.p : nullptr, hint, P->w32))
+    const char* se = std::getenv("WPM_SORT");
+    if (se && std::strcmp(se, "bucket") == 0) {
+        // bucketed by (map, three lowest facets), then sorted per bucket
+        // (measured slower than the merge sort: DESIGN.md, kernel 4)
+        long long tf = 0;
+        for (const MapDesc& d : P->desc) tf = std::max<long long>(tf, (long long)d.facet_off + d.M);
+        const size_t sw = bucket_sort_scratch_words(rows, tf);
+        const bool fresh = P->d_bucket.n < sw || P->bucket_cap != rows || P->bucket_facets != tf;
+        if (P->d_bucket.ensure(sw)) return fail(WPM_EINTERNAL, "device allocation failed (sort)");
+        if (fresh) {
+            CU(cudaMemsetAsync(P->d_bucket.p + bucket_sort_count_offset(rows), 0, (size_t)tf * 64 * 4, P->stream));
+            P->bucket_cap = rows;
+            P->bucket_facets = tf;
+        }
+        if (canon_sort_bucketed(P->d_out_keys.p, rows, device_count ? P->d_out_ctl.p : nullptr, P->mw, P->rw, P->w32,
+                                P->d_maps.p, K, tf, P->d_sorted_bits.p, P->d_sorted_map.p, (long long*)P->d_per_map.p,
+                                P->d_out_ctl.p + 1, P->d_temp.p, P->d_temp.n, P->d_bucket.p, P->d_bucket.n, P->stream,
+                                hint)) {
+            P->bucket_cap = -1;  // the count block is in an unknown state
+            return fail(WPM_EINTERNAL, std::string("canonical sort: ") + cudaGetErrorString(cudaGetLastError()));
+        }
+    } else if (canon_sort_keys(P->d_out_keys.p, rows, P->mw, P->d_sorted_bits.p, P->d_sorted_map.p, P->d_temp.p,
+                               P->d_temp.n, (long long*)P->d_per_map.p, P->d_out_ctl.p + 1, P->stream,
+                               device_count ? P->d_out_ctl.p : nullptr, hint, P->w32)) {
         return fail(WPM_EINTERNAL, std::string("canonical sort: ") + cudaGetErrorString(cudaGetLastError()));
+    }
     CU(cudaEventRecord(P->ev[3], P->stream));
     // results of the sort, read back with the next synchronisation
     CU(cudaMemcpyAsync(&P->h_dups, P->d_out_ctl.p + 1, 8, cudaMemcpyDeviceToHost, P->stream));

@@ -119,6 +119,18 @@ int canon_sort_records(uint32_t* d_keys, long long count, int w32, int rw, int t
 // (out_words > w32: sorted_bits rows of out_words words, zero beyond w32 --
 // kernel 3 emits only the mw words a plan's bitsets use, the C-ABI rows are
 // whole 64-bit words)
+// the bucketed form for kernel-3 rows of a plan (k4_bucket): rows bucketed
+// by (map, three lowest facets) and sorted per bucket; output as above.
+// scratch: bucket_sort_scratch_words(cap, total_facets) uint32 words whose
+// count block (bucket_sort_count_offset(cap), B = 64 x total_facets words)
+// is zero before the first sort (each sort leaves it zero)
+size_t bucket_sort_scratch_words(long long cap, long long total_facets);
+size_t bucket_sort_count_offset(long long cap);
+int canon_sort_bucketed(const uint32_t* d_keys, long long cap, const unsigned long long* d_count, int w32, int rw,
+                        int out_words, const MapDesc* d_maps, int num_maps, long long total_facets,
+                        uint32_t* d_sorted_bits, uint16_t* d_sorted_map, long long* d_first_row,
+                        unsigned long long* d_dups, void* d_temp, size_t temp_bytes, uint32_t* d_scratch,
+                        size_t scratch_words, cudaStream_t st, long long grid_rows = 0);
 // stream compaction (one cooperative launch, hand-written): out[j] = the j-th
 // i < n (ascending) with flags[i] != 0, as in[i] (in = null: i itself);
 // *d_num = the count.  temp: compact_temp_bytes() bytes

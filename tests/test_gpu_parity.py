@@ -356,3 +356,20 @@ def test_canonical_sort_device_shuffled(wpm, n):
             assert torch.equal(out_r, rows) and torch.equal(out_m, maps) and count == total
         else:
             assert torch.equal(out_r[0::2], rows) and torch.equal(out_r[1::2], rows)
+
+
+@pytest.mark.parametrize("n", [3, 5, 8, 11])
+def test_bucketed_sort_variant(wpm, golden, n, monkeypatch):
+    """The bucketed kernel-4 variant (WPM_SORT=bucket, opt-in: measured
+    slower) gives the same bytes as the merge sort."""
+    with wpm.Plan.orbits(n) as p:
+        p.run()
+        res = p.fetch()
+        want = _digest_plan(wpm, p, res, n)
+    monkeypatch.setenv("WPM_SORT", "bucket")
+    with wpm.Plan.orbits(n) as p:
+        for _ in range(2):  # the second run reuses the zeroed count block
+            p.run()
+            res = p.fetch()
+            assert res.duplicates == 0 and res.counts == [m["wpms"] for m in golden["dfs"][str(n)]["maps"]]
+            assert _digest_plan(wpm, p, res, n) == want
