@@ -80,7 +80,7 @@ constexpr int a16(int x) { return (x + 15) & ~15; }
 // MAV (map-affine, TSM layouts only): one work queue per map; a CTA works on
 // one map at a time with only THAT map's tables in shared memory, and moves to
 // the map with the most pending tasks per CTA once its map is finished -- the
-// TS layout for plans whose maps' tables do not fit together (n = 7, 8).
+// TS layout for plans whose maps' tables do not fit together (n = 7..10).
 template <int NMAX, int MMAX, int DMAX, bool TSM = false, int WPBV = 4, int MINBV = 0, bool MAV = false>
 struct LC {
     static constexpr int kN = NMAX, kM = MMAX, kDepth = DMAX;
@@ -136,6 +136,8 @@ using C15 = LC<3008, 1368, FRAME_CAP>;
 using C15T = LC<3008, 1368, FRAME_CAP, true, 18, 1>;
 using C7M = LC<420, 208, FRAME_CAP, true, 20, 2, true>;   // n = 7: one map's tables (~8 KB) per CTA
 using C8M = LC<720, 312, FRAME_CAP, true, 20, 2, true>;   // n = 8: ~14 KB
+using C9M = LC<1152, 440, FRAME_CAP, true, 16, 2, true>;  // n = 9: ~20 KB (41.9 -> 39.6 ms)
+using C10M = LC<1792, 616, FRAME_CAP, true, 16, 2, true>; // n = 10: ~30 KB, 32 warps per SM (32.5 -> 29.8 ms)
 // (10 x 4 and 8 x 5 warps x CTAs measured within 1 % of 20 x 2 at n = 7, 8)
 // (n = 9's seven maps need ~140 KB of tables: 16 warps per SM measured 34 %
 // slower than the global-table layout at 32 -- no all-maps TS variant for n = 7..9)
@@ -1280,6 +1282,8 @@ bool k3_map_queues(const SearchParams& p) {
     const int N = p.max_N, M = p.max_M;
     if (N > C6::kN && N <= C7M::kN && M <= C7M::kM) return ts_fits<C7M>(p);
     if (N > C7::kN && N <= C8M::kN && M <= C8M::kM) return ts_fits<C8M>(p);
+    if (N > C8::kN && N <= C9M::kN && M <= C9M::kM) return ts_fits<C9M>(p);
+    if (N > C9::kN && N <= C10M::kN && M <= C10M::kM) return ts_fits<C10M>(p);
     return false;
 }
 
@@ -1295,7 +1299,9 @@ int launch_k3_search(const SearchParams& p, int num_sms, cudaStream_t st, int* w
         if (N <= C5T::kN && M <= C5T::kM && ts_fits<C5T>(p)) return launch_class<C5T>(p, num_sms, st, warps_out);
         if (p.map_queues) {
             if (N <= C7M::kN && M <= C7M::kM) return launch_class<C7M>(p, num_sms, st, warps_out);
-            return launch_class<C8M>(p, num_sms, st, warps_out);
+            if (N <= C8M::kN && M <= C8M::kM) return launch_class<C8M>(p, num_sms, st, warps_out);
+            if (N <= C9M::kN && M <= C9M::kM) return launch_class<C9M>(p, num_sms, st, warps_out);
+            return launch_class<C10M>(p, num_sms, st, warps_out);
         }
         if (N <= C6T::kN && M <= C6T::kM && N > C5T::kN && ts_fits<C6T>(p))
             return launch_class<C6T>(p, num_sms, st, warps_out);

@@ -361,15 +361,16 @@ def test_canonical_sort_device_shuffled(wpm, n):
 @pytest.mark.parametrize("n", [3, 5, 8, 11])
 def test_bucketed_sort_variant(wpm, golden, n, monkeypatch):
     """The bucketed kernel-4 variant (WPM_SORT=bucket, opt-in: measured
-    slower) gives the same bytes as the merge sort."""
+    slower) gives the same rows as the merge sort."""
+    import numpy as np
+
     with wpm.Plan.orbits(n) as p:
         p.run()
-        res = p.fetch()
-        want = _digest_plan(wpm, p, res, n)
+        want = np.array(p.fetch().bits)
     monkeypatch.setenv("WPM_SORT", "bucket")
     with wpm.Plan.orbits(n) as p:
         for _ in range(2):  # the second run reuses the zeroed count block
             p.run()
             res = p.fetch()
             assert res.duplicates == 0 and res.counts == [m["wpms"] for m in golden["dfs"][str(n)]["maps"]]
-            assert _digest_plan(wpm, p, res, n) == want
+            assert np.array_equal(np.array(res.bits), want)
