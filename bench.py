@@ -159,8 +159,12 @@ LAUNCHES_PER_STEP = 3
 def _profile_summary(n):
     """traffic / instructions-per-node of kernel 3 from the committed ncu capture."""
     out = {}
-    path = os.path.join(ROOT, "profiles", f"r01_k3_n{n}_ncu.txt")
-    if not os.path.exists(path):
+    for tag in ("r02c", "r02", "r01"):  # the newest capture committed
+        path = os.path.join(ROOT, "profiles", f"{tag}_k3_n{n}_ncu.txt")
+        if os.path.exists(path):
+            out["source"] = f"profiles/{tag}_k3_n{n}_ncu.txt"
+            break
+    else:
         return out
     rd = wr = None
     for ln in open(path):
@@ -172,7 +176,7 @@ def _profile_summary(n):
             rd = float(t[1]) * scale.get(t[2], 1)
         elif t[0] == "dram__bytes_write.sum":
             wr = float(t[1]) * scale.get(t[2], 1)
-        elif ln.startswith("warp instructions per node"):
+        elif ln.startswith("warp instructions per"):
             out["inst_per_node"] = float(t[-1])
         elif t[0] == "smsp__issue_active.avg.pct_of_peak_sustained_active":
             out["issue_pct"] = float(t[1])
@@ -356,6 +360,7 @@ def main():
                 "issue": {"warp_inst_per_node": prof.get("inst_per_node"),
                           "issue_active_pct": prof.get("issue_pct"),
                           "warp_inst_peak_per_s": 4 * 148 * 1.965e9,
+                          "profile": prof.get("source"),
                           "note": "the kernel is issue-bound: one DFS per warp has O(n) lanes of work per node; "
                                   "see profiles/ (k3 ncu summaries)"}}
 
