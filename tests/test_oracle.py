@@ -350,3 +350,36 @@ def test_charmap_of_dcm_general_branch(wpm, oracle):
         assert wpm.charmap_of_dcm(dd) == want, rows
         checked += 1
     assert checked > 100
+
+
+def test_alg1_n10_chunks_recorded(golden):
+    """The exhaustive Algorithm-1 chunks recorded at n = 10 (tools/alg1_full.py
+    on the device): every chunk's accepted set equals the DFS rows sharing its
+    prefix, chunks are distinct, and a map whose chunks are all recorded adds
+    up to its golden WPM count and to its whole combination space."""
+    import json
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "tools"))
+    from alg1_full import chunks_of
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "alg1_n10_chunks.jsonl")
+    recs = [json.loads(ln) for ln in open(path) if ln.strip()]
+    assert recs, "no recorded chunks"
+    seen = set()
+    for r in recs:
+        assert r["n"] == 10 and r["equal"] and r["odometer"] == r["dfs"]
+        key = (r["map"], tuple(r["prefix"]))
+        assert key not in seen
+        seen.add(key)
+    # the chunking: fix outer blocks until a chunk has <= the leaf budget
+    j, pre = chunks_of([4, 4, 3, 1], 100)  # 11 * 11 * 7 * 2 leaves
+    assert j == 2 and len(pre) == 121 and pre[0] == (0, 0) and pre[-1] == (10, 10)
+    assert chunks_of([2, 1], 100) == (0, [()])
+    for m, mrec in enumerate(golden["dfs"]["10"]["maps"]):
+        mine = [r for r in recs if r["map"] == m]
+        # the widest two blocks have width 4 at n = 10: 11 x 11 chunks cover the map
+        if len(mine) == 121:
+            assert sum(r["odometer"] for r in mine) == mrec["wpms"]
+            assert len({r["leaves"] for r in mine}) == 1
