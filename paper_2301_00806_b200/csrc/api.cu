@@ -50,9 +50,33 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
+// WPM_TRACE=2: every CUDA runtime call made through CU() that takes >= 2 us
+// of host time is reported with its source line (e2e engineering)
+const bool g_trace_calls = [] {
+    const char* e = std::getenv("WPM_TRACE");
+    return e && std::atoi(e) >= 2;
+}();
+struct CallTimer {
+    const char* what;
+    int line;
+    std::chrono::steady_clock::time_point t0;
+    CallTimer(const char* w, int l) : what(w), line(l) {
+        if (g_trace_calls) t0 = std::chrono::steady_clock::now();
+    }
+    ~CallTimer() {
+        if (!g_trace_calls) return;
+        const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        if (us >= 2.0) std::fprintf(stderr, "[wpm]   call %8.1f us  api.cu:%d  %.60s\n", us, line, what);
+    }
+};
+
 #define CU(call)                                                                                  \
     do {                                                                                          \
-        cudaError_t e_ = (call);                                                                  \
+        cudaError_t e_;                                                                           \
+        {                                                                                         \
+            CallTimer ct_(#call, __LINE__);                                                       \
+            e_ = (call);                                                                          \
+        }                                                                                         \
         if (e_ != cudaSuccess)                                                                    \
             return fail(WPM_EINTERNAL, std::string(#call) + ": " + cudaGetErrorString(e_));       \
     } while (0)
@@ -86,7 +110,12 @@ struct DevBuf {
         n = 0;
         s = g_alloc_stream;
         const size_t c = std::max<size_t>(count, 1);
-        if (cudaMallocAsync(reinterpret_cast<void**>(&p), c * sizeof(T), s) != cudaSuccess) {
+        cudaError_t e;
+        {
+            CallTimer ct("cudaMallocAsync (DevBuf::ensure)", __LINE__);
+            e = cudaMallocAsync(reinterpret_cast<void**>(&p), c * sizeof(T), s);
+        }
+        if (e != cudaSuccess) {
             p = nullptr;
             return 1;
         }
@@ -627,16 +656,27 @@ static int create_from_cols(int32_t n, int32_t m, int32_t K, const uint32_t* col
         delete P;
         return fail(WPM_EINTERNAL, "device allocation failed (universes)");
     }
-    cudaMemcpyAsync(d_cols.p, cols, (size_t)K * m * sizeof(uint32_t), cudaMemcpyHostToDevice, P->stream);
+    { CallTimer ct_("H2D cols (pageable)", __LINE__);
+    cudaMemcpyAsync(d_cols.p, cols, (size_t)K * m * sizeof(uint32_t), cudaMemcpyHostToDevice, P->stream); }
     P->h2d += (long long)K * m * 4;
-    if (launch_k1_universe(n, m, K, d_cols.p, P->d_facets.p, stride, P->d_tmpi.p, P->stream)) {
+    int k1rc;
+    {
+        CallTimer ct_("launch_k1_universe", __LINE__);
+        k1rc = launch_k1_universe(n, m, K, d_cols.p, P->d_facets.p, stride, P->d_tmpi.p, P->stream);
+    }
+    if (k1rc) {
         delete P;
         return fail(WPM_EINTERNAL, "kernel 1 launch failed");
     }
     P->M.assign(K, 0);
     cudaMemcpyAsync(P->M.data(), P->d_tmpi.p, K * sizeof(int32_t), cudaMemcpyDeviceToHost, P->stream);
     P->d2h += (long long)K * 4;
-    if (cudaStreamSynchronize(P->stream) != cudaSuccess) {
+    cudaError_t s1;
+    {
+        CallTimer ct_("sync after kernel 1", __LINE__);
+        s1 = cudaStreamSynchronize(P->stream);
+    }
+    if (s1 != cudaSuccess) {
         delete P;
         return fail(WPM_EINTERNAL, std::string("kernel 1: ") + cudaGetErrorString(cudaGetLastError()));
     }
@@ -955,7 +995,12 @@ static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
         sp.root_nodes = P->d_root_nodes.p;
         P->root_count = nroots;
     }
-    if ((nseed > 0 || L.claim_recs) && !launch_k3_search(sp, P->num_sms, P->stream, &P->warps))
+    int k3ok = 1;
+    {
+        CallTimer ct_("launch_k3_search", __LINE__);
+        if (nseed > 0 || L.claim_recs) k3ok = launch_k3_search(sp, P->num_sms, P->stream, &P->warps);
+    }
+    if (!k3ok)
         return fail(WPM_EINTERNAL, std::string("kernel 3 launch: ") + cudaGetErrorString(cudaGetLastError()));
     return WPM_OK;
 }
@@ -1214,6 +1259,7 @@ static int plan_search(wpm_plan* P, int shard_index, int shard_count) {
 // -- the count kernel 3 left in out_ctl[0] (capped at out_cap), so the sort
 // follows the search without a host round trip
 static int plan_sort_launch(wpm_plan* P, bool device_count) {
+    Trace tr;
     const int K = P->num_maps;
     const long long rows = device_count ? (long long)P->out_cap : P->total;
     const size_t tb = canon_sort_temp_bytes(std::max<long long>(rows, 1), P->mw);
@@ -1222,6 +1268,7 @@ static int plan_sort_launch(wpm_plan* P, bool device_count) {
     CU(cudaMemsetAsync(P->d_out_ctl.p + 1, 0, 8, P->stream));
     CU(cudaMemsetAsync(P->d_per_map.p, 0xFF, K * 8, P->stream));  // first row per map, -1 = none
     CU(cudaEventRecord(P->ev[2], P->stream));
+    tr.mark("    sort: buffers");
     // grid sized from the rows this workload produced last time (this plan, or
     // an earlier plan of the same maps: one-shot calls), else the capacity
     long long hint = 0;
@@ -1257,6 +1304,7 @@ static int plan_sort_launch(wpm_plan* P, bool device_count) {
         return fail(WPM_EINTERNAL, std::string("canonical sort: ") + cudaGetErrorString(cudaGetLastError()));
     }
     CU(cudaEventRecord(P->ev[3], P->stream));
+    tr.mark("    sort: launch");
     // results of the sort, read back with the next synchronisation
     CU(cudaMemcpyAsync(&P->h_dups, P->d_out_ctl.p + 1, 8, cudaMemcpyDeviceToHost, P->stream));
     P->h_first.resize(K);

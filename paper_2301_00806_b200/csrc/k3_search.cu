@@ -146,6 +146,7 @@ using CGF = LC<4096, 2048, 2050>;         // full depth: the rerun after a frame
 struct MapView {
     int M, N, n, cap, map, nw;
     int lpf_shift;  // lanes per facet in flattened passes: 1 << lpf_shift >= n
+    unsigned nmag;  // ceil(2^20 / n): j / n = (j * nmag) >> 20 for every pair index j < 2^20 / n
     const uint16_t* fr;
     const uint16_t* rp;
     uint32_t frs, rps;  // the same tables in shared memory (TS layouts)
@@ -276,12 +277,33 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 // open: c == 1.  b1: c == 1 && a == 1.  dead: c == 1 && a == 0.
 
 // a -= 1 on every ridge of the facets trail[lo..hi) (already marked OUT)
+// Flattened (decision, ridge) pairs of trail[lo..hi): body(act, e, k) per
+// lane, k = the ridge slot of trail entry e.  Up to n = 8 a facet takes a
+// power-of-two lane group (n = 5: 4 facets x 8 lanes per pass); the n >= 9
+// size classes pack the pairs n per facet over all 32 lanes (trail entry
+// lo + j / n, slot j % n, j / n by a multiply-shift): n = 11 -5 % search time,
+// n = 8 +4 % (the division costs more than it saves when 8 lanes fit a facet)
+template <class C, class F>
+__device__ __forceinline__ void for_pairs(const MapView& mp, int lo, int hi, int lane, F&& body) {
+    if constexpr (C::kN > 720) {
+        const int tot = (hi - lo) * mp.n;
+        for (int j0 = lane; j0 < tot + lane; j0 += 32) {
+            const int q = (int)(((unsigned)j0 * mp.nmag) >> 20), k = j0 - q * mp.n;
+            body(j0 < tot, lo + q, k);
+        }
+    } else {
+        const int sh_l = mp.lpf_shift, k = lane & ((1 << sh_l) - 1), per = 32 >> sh_l;
+        for (int e0 = lo; e0 < hi; e0 += per) {
+            const int e = e0 + (lane >> sh_l);
+            body(e < hi && k < mp.n, e, k);
+        }
+    }
+}
+
+// a -= 1 on every ridge of the facets trail[lo..hi) (already marked OUT)
 template <class C>
 __device__ __forceinline__ void apply_exclusions(WS<C>& w, const MapView& mp, int lo, int hi, int lane) {
-    const int sh_l = mp.lpf_shift, k = lane & ((1 << sh_l) - 1), per = 32 >> sh_l;
-    for (int e0 = lo; e0 < hi; e0 += per) {
-        const int e = e0 + (lane >> sh_l);
-        const bool act = e < hi && k < mp.n;
+    for_pairs<C>(mp, lo, hi, lane, [&](bool act, int e, int k) {
         const int g = act ? (w.trail()[e] & 0x7FFF) : 0;
         const int r = act ? ldfr<C>(mp, g * mp.fs + k) : 0;
         const unsigned sh = (r & 3) * 8;
@@ -289,7 +311,7 @@ __device__ __forceinline__ void apply_exclusions(WS<C>& w, const MapView& mp, in
         // (1,1) -> (1,0): dead and leaves the forced set; (1,2) -> (1,1): enters it
         red_xor_if(w.a_b1(r), 1u << (r & 31), act && (ob == 5u || ob == 9u));
         w.ndead |= (int)__any_sync(FULL, act && ob == 5u);
-    }
+    });
 }
 
 // exclude one facet (a tried sibling)
@@ -403,10 +425,7 @@ __device__ __forceinline__ void undo_to(WS<C>& w, const MapView& mp, int mark, i
         red_and_if(w.a_inb(g), ~(1u << (g & 31)), inc);
         w.size -= __popc(__ballot_sync(FULL, inc));
     }
-    const int sh_l = mp.lpf_shift, k = lane & ((1 << sh_l) - 1), per = 32 >> sh_l;
-    for (int e0 = lo; e0 < hi; e0 += per) {
-        const int e = e0 + (lane >> sh_l);
-        const bool act = e < hi && k < mp.n;
+    for_pairs<C>(mp, lo, hi, lane, [&](bool act, int e, int k) {
         const unsigned t = act ? (unsigned)w.trail()[e] : 0u;
         const int g = (int)(t & 0x7FFFu);
         const int r = act ? ldfr<C>(mp, g * mp.fs + k) : 0;
@@ -417,7 +436,7 @@ __device__ __forceinline__ void undo_to(WS<C>& w, const MapView& mp, int mark, i
         const unsigned bit = 1u << (r & 31);
         red_xor_if(w.a_open(r), bit, act && (((ob & 3u) == 1u) != ((nb & 3u) == 1u)));
         red_xor_if(w.a_b1(r), bit, act && ((ob == 5u) != (nb == 5u)));
-    }
+    });
     w.nopen = nopen_mark;
     w.ndead = 0;
     w.tl = mark;
@@ -1025,6 +1044,7 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
         mp.map = map;
         mp.nw = (md.N + 31) >> 5;
         mp.lpf_shift = md.n <= 4 ? 2 : (md.n <= 8 ? 3 : 4);
+        mp.nmag = ((1u << 20) + (unsigned)md.n - 1u) / (unsigned)md.n;
         mp.fr = p.fr + md.fr_off;
         mp.rp = p.rp + md.rp_off;
         if constexpr (C::MA) {  // map == cur: its tables alone, fr then rp

@@ -3,7 +3,7 @@ import os
 import sys
 import time
 
-os.environ["WPM_TRACE"] = "1"
+os.environ.setdefault("WPM_TRACE", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2301_00806_b200 as wpm  # noqa: E402
 
