@@ -35,7 +35,10 @@
 #include <cstdint>
 #include <cstdlib>
 #include <functional>
+#include <atomic>
+#include <condition_variable>
 #include <initializer_list>
+#include <mutex>
 #include <ostream>
 #include <stdexcept>
 #include <string>
@@ -185,6 +188,102 @@ inline std::vector<VertexSet> universe_of(wpm_plan_t* p, int map) {
     return out;
 }
 
+// A persistent host worker pool for building the reference's return objects
+// (one std::vector<VertexSet> per WPM: 242,043 heap vectors at n = 5).
+// Spawning threads per call cost ~20 us each; these wait on a condition
+// variable between calls.  run(items, fn) calls fn(i) for every i < items,
+// dynamically scheduled over the workers and the calling thread.
+class HostPool {
+public:
+    static HostPool& get() {
+        static HostPool pool;
+        return pool;
+    }
+    void run(std::size_t items, const std::function<void(std::size_t)>& fn) {
+        if (items == 0) return;
+        if (workers_.empty() || items == 1) {
+            for (std::size_t i = 0; i < items; ++i) fn(i);
+            return;
+        }
+        std::lock_guard<std::mutex> call(call_mu_);  // one parallel region at a time
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &fn;
+            items_ = items;
+            next_.store(0);
+            busy_ = workers_.size();
+            ++gen_;
+        }
+        cv_.notify_all();
+        drain();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [&] { return busy_ == 0; });
+        fn_ = nullptr;
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+
+private:
+    HostPool() {
+        const unsigned hc = std::thread::hardware_concurrency();
+        const unsigned n = hc > 1 ? hc - 1 : 0;
+        for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    void drain() {
+        for (std::size_t i; (i = next_.fetch_add(1)) < items_;) (*fn_)(i);
+    }
+    void loop() {
+        unsigned long long seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+            }
+            drain();
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--busy_ == 0) done_.notify_one();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_, call_mu_;
+    std::condition_variable cv_, done_;
+    const std::function<void(std::size_t)>* fn_ = nullptr;
+    std::size_t items_ = 0, busy_ = 0;
+    std::atomic<std::size_t> next_{0};
+    unsigned long long gen_ = 0;
+    bool stop_ = false;
+};
+
+// rows [lo, hi) of map `map` -> the PureComplex objects out[lo..hi)
+// (search.hpp:247-253): facets in ascending order, each vector sized once
+inline void fill_complexes(const wpm_result_t* r, int map, int m, int n, const std::vector<VertexSet>& u,
+                           std::vector<PureComplex>& out, std::size_t lo, std::size_t hi) {
+    const int W = r->words;
+    const std::uint64_t* row = r->bits + (static_cast<std::size_t>(r->offsets[map]) + lo) * W;
+    for (std::size_t j = lo; j < hi; ++j) {
+        PureComplex& K = out[j];
+        K.m = m;
+        K.n = n;
+        K.embedded = true;
+        int k = 0;
+        for (int w = 0; w < W; ++w) k += __builtin_popcountll(row[w]);
+        K.facets.resize(static_cast<std::size_t>(k));
+        VertexSet* f = K.facets.data();
+        for (int w = 0; w < W; ++w)
+            for (std::uint64_t x = row[w]; x; x &= x - 1) *f++ = u[static_cast<std::size_t>(w * 64 + __builtin_ctzll(x))];
+        row += W;
+    }
+}
+
 // rows of map `map` -> PureComplex (search.hpp:247-253): facets in
 // ascending order, each vector sized once
 inline std::vector<PureComplex> complexes_of(const wpm_result_t* r, int map, int m, int n,
@@ -283,16 +382,22 @@ inline std::vector<std::vector<PureComplex>> enumerate_orbits(int n, int p = 4, 
     const int K = R.r->num_maps;
     std::vector<std::vector<VertexSet>> uni(static_cast<std::size_t>(K));
     for (int i = 0; i < K; ++i) uni[static_cast<std::size_t>(i)] = detail::universe_of(P.p, i);
-    // the reference's return objects, built in parallel over the maps
+    // the reference's return objects, built on the persistent host pool:
+    // every map's vector sized (one item per map), then filled in chunks of
+    // 2048 rows (the maps hold 2,043-17,606 WPMs at n = 5)
     std::vector<std::vector<PureComplex>> out(static_cast<std::size_t>(K));
-    const int T = std::max(1, std::min<int>(K, static_cast<int>(std::thread::hardware_concurrency())));
-    std::vector<std::thread> pool;
-    for (int t = 0; t < T; ++t)
-        pool.emplace_back([&, t]() {
-            for (int i = t; i < K; i += T)
-                out[static_cast<std::size_t>(i)] = detail::complexes_of(R.r, i, n + p, n, uni[static_cast<std::size_t>(i)]);
-        });
-    for (auto& th : pool) th.join();
+    detail::HostPool& pool = detail::HostPool::get();
+    pool.run(static_cast<std::size_t>(K), [&](std::size_t i) { out[i].resize(static_cast<std::size_t>(R.r->counts[i])); });
+    constexpr std::size_t kChunk = 2048;
+    std::vector<std::pair<int, std::size_t>> chunks;  // (map, first row)
+    for (int i = 0; i < K; ++i)
+        for (std::size_t lo = 0; lo < static_cast<std::size_t>(R.r->counts[i]); lo += kChunk) chunks.emplace_back(i, lo);
+    pool.run(chunks.size(), [&](std::size_t c) {
+        const int i = chunks[c].first;
+        const std::size_t lo = chunks[c].second, cnt = static_cast<std::size_t>(R.r->counts[i]);
+        detail::fill_complexes(R.r, i, n + p, n, uni[static_cast<std::size_t>(i)], out[static_cast<std::size_t>(i)], lo,
+                               std::min(cnt, lo + kChunk));
+    });
     return out;
 }
 

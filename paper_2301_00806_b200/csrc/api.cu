@@ -98,11 +98,52 @@ void init_pool(int device) {
     done[device] = true;
 }
 
+// Buffers of a destroyed plan (its stream synchronised first) are kept per
+// device and handed to the next plan's DevBuf::ensure: a one-shot call
+// allocates ~20 buffers, and each cudaMallocAsync / cudaFreeAsync pair cost
+// ~2.5 us of host time (WPM_TRACE=2).  Local DevBufs of API functions free
+// through the stream as before (g_recycle is only set inside
+// wpm_plan_destroy).
+thread_local bool g_recycle = false;
+struct BlockCache {
+    std::mutex mu;
+    std::vector<std::pair<void*, size_t>> blocks[64];
+    size_t bytes[64] = {};
+    static constexpr size_t kMaxBytes = size_t(8) << 30;
+    void* take(int dev, size_t want, size_t* got) {
+        if (dev < 0 || dev >= 64) return nullptr;
+        std::lock_guard<std::mutex> lk(mu);
+        auto& v = blocks[dev];
+        size_t best = SIZE_MAX;
+        for (size_t i = 0; i < v.size(); ++i)  // best fit, at most 2x (+64 KB) the request
+            if (v[i].second >= want && v[i].second <= 2 * want + (64 << 10) &&
+                (best == SIZE_MAX || v[i].second < v[best].second))
+                best = i;
+        if (best == SIZE_MAX) return nullptr;
+        void* p = v[best].first;
+        *got = v[best].second;
+        bytes[dev] -= v[best].second;
+        v[best] = v.back();
+        v.pop_back();
+        return p;
+    }
+    bool put(int dev, void* p, size_t sz) {
+        if (dev < 0 || dev >= 64) return false;
+        std::lock_guard<std::mutex> lk(mu);
+        if (bytes[dev] + sz > kMaxBytes) return false;
+        blocks[dev].emplace_back(p, sz);
+        bytes[dev] += sz;
+        return true;
+    }
+};
+BlockCache g_blocks;
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
     cudaStream_t s = nullptr;
+    int dev = -1;
     int ensure(size_t count) {
         if (count <= n && p) return 0;
         if (p) cudaFreeAsync(p, s);
@@ -110,6 +151,13 @@ struct DevBuf {
         n = 0;
         s = g_alloc_stream;
         const size_t c = std::max<size_t>(count, 1);
+        if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+        size_t got = 0;
+        if (void* q = g_blocks.take(dev, c * sizeof(T), &got)) {
+            p = static_cast<T*>(q);
+            n = got / sizeof(T);
+            return 0;
+        }
         cudaError_t e;
         {
             CallTimer ct("cudaMallocAsync (DevBuf::ensure)", __LINE__);
@@ -129,9 +177,12 @@ struct DevBuf {
         std::swap(p, o.p);
         std::swap(n, o.n);
         std::swap(s, o.s);
+        std::swap(dev, o.dev);
     }
     ~DevBuf() {
-        if (p) cudaFreeAsync(p, s);
+        if (!p) return;
+        if (g_recycle && g_blocks.put(dev, p, n * sizeof(T))) return;
+        cudaFreeAsync(p, s);
     }
 };
 
@@ -298,12 +349,55 @@ struct wpm_plan {
     std::string signature;           // the workload: (m, n, cap, every universe's facet count)
     unsigned long long h_dups = 0;   // sort results, read back with the run's synchronisation
     std::vector<long long> h_first;
+    // Pinned staging for the small copies of create / run: a pageable
+    // cudaMemcpyAsync stages through the driver, and a pageable D2H blocks the
+    // host until the stream drains -- one round trip per small read.  H2D
+    // sources are bump-allocated (reset only after a synchronisation of the
+    // stream); D2H results land in the mailbox at the end of the block.
+    uint8_t* stage = nullptr;
+    size_t stage_cap = 0, stage_used = 0;
+    ~wpm_plan();
     DevBuf<unsigned long long> d_root_nodes;
     long long root_count = 0;
     int ntasks = 0, frame_cap = 64;
     int fr_words = 0, rp_words = 0;  // uint16 entries of the fr / rp tables over every map
     bool full_depth = false;
 };
+
+namespace {
+constexpr size_t kStageBytes = 1 << 20;
+constexpr size_t kMailBytes = 64 << 10;  // >= 128 + 8 (K + 1) for K <= 4096 maps
+// mailbox slots (D2H): out_ctl[0..3], qctl[0..7], duplicates, then per map
+constexpr size_t kMailOctl = 0, kMailQc = 32, kMailDups = 96, kMailMaps = 128;
+
+int stage_init(wpm_plan* P) {
+    size_t got = 0;
+    P->stage = static_cast<uint8_t*>(g_pinned.get(kStageBytes, &got));
+    if (!P->stage) return fail(WPM_EINTERNAL, "pinned host allocation failed (staging)");
+    P->stage_cap = got;
+    P->stage_used = 0;
+    return WPM_OK;
+}
+uint8_t* mail(wpm_plan* P, size_t off) { return P->stage + P->stage_cap - kMailBytes + off; }
+// H2D of a small host array through the pinned staging block (pageable when
+// the block is full: correct, just slower)
+cudaError_t h2d_async(wpm_plan* P, void* dst, const void* src, size_t bytes) {
+    if (!bytes) return cudaSuccess;
+    const size_t off = (P->stage_used + 15) & ~size_t(15);
+    if (P->stage && off + bytes <= P->stage_cap - kMailBytes) {
+        std::memcpy(P->stage + off, src, bytes);
+        P->stage_used = off + bytes;
+        src = P->stage + off;
+    }
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, P->stream);
+}
+// the stream is idle: staged sources may be reused
+void stage_reset(wpm_plan* P) { P->stage_used = 0; }
+}  // namespace
+
+wpm_plan::~wpm_plan() {
+    if (stage) g_pinned.put(stage, stage_cap);
+}
 
 // ------------------------------------------------------------------ host
 
@@ -394,17 +488,24 @@ extern "C" int32_t wpm_idcm_orbits(int32_t n, int32_t p, uint32_t* rows_out, int
     if (W == 1 && !T.byte_img.empty()) {  // p <= 5: one-word masks, straight-line minimum
         const size_t Q = T.img.size();
         const uint64_t* tab = T.byte_img.data();
+        // p <= 4: a row set is a 16-bit mask; every image of a processed set
+        // is marked, so each orbit's p! images are computed once (35 orbits x
+        // 24 images at n = 5 instead of 462 subsets x 24)
+        std::vector<uint64_t> seen(p <= 4 ? 1024 : 0, 0ull);
         for (;;) {
             uint64_t c = 0;
             for (int i = 0; i < n; ++i) c |= 1ull << pool[idx[i]];
-            uint64_t bm = 0;
-            for (size_t q = 0; q < Q; ++q) {
-                uint64_t im = 0;
-                for (int ch = 0; ch < chunks; ++ch) im |= tab[((q * chunks) + ch) * 256 + ((c >> (8 * ch)) & 0xFFu)];
-                const uint64_t x = im ^ bm;
-                if (q == 0 || (im & x & (0 - x))) bm = im;
+            if (seen.empty() || !((seen[c >> 6] >> (c & 63)) & 1ull)) {
+                uint64_t bm = 0;
+                for (size_t q = 0; q < Q; ++q) {
+                    uint64_t im = 0;
+                    for (int ch = 0; ch < chunks; ++ch) im |= tab[((q * chunks) + ch) * 256 + ((c >> (8 * ch)) & 0xFFu)];
+                    if (!seen.empty()) seen[im >> 6] |= 1ull << (im & 63);
+                    const uint64_t x = im ^ bm;
+                    if (q == 0 || (im & x & (0 - x))) bm = im;
+                }
+                reps.push_back(bm);
             }
-            reps.push_back(bm);
             int pos = n - 1;
             while (pos >= 0 && idx[pos] == P - (n - pos)) --pos;
             if (pos < 0) break;
@@ -560,7 +661,7 @@ static int plan_init(wpm_plan* P, int device) {
         for (auto& e : P->ev) CU(cudaEventCreate(&e));
     }
     g_alloc_stream = P->stream;
-    return WPM_OK;
+    return stage_init(P);
 }
 
 static int resolve_cap(int64_t facet_cap, int n, int M) {
@@ -604,16 +705,18 @@ static int plan_build_tables(wpm_plan* P, const std::vector<uint32_t>& foff) {
     if (P->d_maps.ensure(K) || P->d_ridges.ensure(r_tot) || P->d_fr.ensure(fr_tot * P->n + 8) ||
         P->d_rp.ensure(r_tot * WPM_MAX_PARENTS + 8) || P->d_npar.ensure(r_tot) || P->d_tmpi.ensure(K + 1))
         return fail(WPM_EINTERNAL, "device allocation failed (tables)");
-    CU(cudaMemcpyAsync(P->d_maps.p, P->desc.data(), K * sizeof(MapDesc), cudaMemcpyHostToDevice, P->stream));
+    CU(h2d_async(P, P->d_maps.p, P->desc.data(), K * sizeof(MapDesc)));
     CU(cudaMemsetAsync(P->d_tmpi.p, 0, (K + 1) * sizeof(int32_t), P->stream));
     if (launch_k2_incidence(K, P->d_maps.p, P->m, P->n, P->d_facets.p, P->d_ridges.p, P->d_fr.p, P->d_rp.p,
                             P->d_npar.p, P->d_tmpi.p, P->d_tmpi.p + K, P->stream))
         return fail(WPM_EINTERNAL, std::string("kernel 2 launch: ") + cudaGetErrorString(cudaGetLastError()));
     P->h2d += 2LL * K * (long long)sizeof(MapDesc);
-    std::vector<int32_t> hN(K + 1);
-    CU(cudaMemcpyAsync(hN.data(), P->d_tmpi.p, (K + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaMemcpyAsync(mail(P, kMailMaps), P->d_tmpi.p, (K + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, P->stream));
     P->d2h += (long long)(K + 1) * 4;
     CU(cudaStreamSynchronize(P->stream));
+    stage_reset(P);
+    std::vector<int32_t> hN(K + 1);
+    std::memcpy(hN.data(), mail(P, kMailMaps), (K + 1) * sizeof(int32_t));
     if (hN[K]) return fail(WPM_EINVAL, "a ridge has more than WPM_MAX_PARENTS candidate facets");
     P->N.assign(hN.begin(), hN.begin() + K);
     P->maxN = 0;
@@ -624,7 +727,7 @@ static int plan_build_tables(wpm_plan* P, const std::vector<uint32_t>& foff) {
         P->maxN = std::max(P->maxN, P->N[i]);
         P->maxDepth = std::max(P->maxDepth, std::min(P->cap[i], P->M[i]) + 1);
     }
-    CU(cudaMemcpyAsync(P->d_maps.p, P->desc.data(), K * sizeof(MapDesc), cudaMemcpyHostToDevice, P->stream));
+    CU(h2d_async(P, P->d_maps.p, P->desc.data(), K * sizeof(MapDesc)));
     P->signature = std::to_string(P->m) + "/" + std::to_string(P->n) + "/" + std::to_string(P->facet_cap) + "/" +
                    std::to_string(P->has_pins ? 1 : 0);
     for (int i = 0; i < K; ++i) P->signature += ":" + std::to_string(P->M[i]) + "," + std::to_string(P->N[i]);
@@ -632,8 +735,7 @@ static int plan_build_tables(wpm_plan* P, const std::vector<uint32_t>& foff) {
     P->w32 = 2 * ((P->maxM + 63) / 64);  // C-ABI rows: whole 64-bit words
     P->rw = rec_words(P->mw);             // emitted records: the mw words the bitsets use + the map id
     P->recw = 4 + 2 * P->mw;
-    CU(cudaStreamSynchronize(P->stream));
-    return WPM_OK;
+    return WPM_OK;  // the desc upload is staged (pinned); the run orders after it on the stream
 }
 
 static int create_from_cols(int32_t n, int32_t m, int32_t K, const uint32_t* cols, int64_t facet_cap,
@@ -656,8 +758,10 @@ static int create_from_cols(int32_t n, int32_t m, int32_t K, const uint32_t* col
         delete P;
         return fail(WPM_EINTERNAL, "device allocation failed (universes)");
     }
-    { CallTimer ct_("H2D cols (pageable)", __LINE__);
-    cudaMemcpyAsync(d_cols.p, cols, (size_t)K * m * sizeof(uint32_t), cudaMemcpyHostToDevice, P->stream); }
+    if (h2d_async(P, d_cols.p, cols, (size_t)K * m * sizeof(uint32_t)) != cudaSuccess) {
+        delete P;
+        return fail(WPM_EINTERNAL, "H2D of the characteristic maps failed");
+    }
     P->h2d += (long long)K * m * 4;
     int k1rc;
     {
@@ -669,7 +773,7 @@ static int create_from_cols(int32_t n, int32_t m, int32_t K, const uint32_t* col
         return fail(WPM_EINTERNAL, "kernel 1 launch failed");
     }
     P->M.assign(K, 0);
-    cudaMemcpyAsync(P->M.data(), P->d_tmpi.p, K * sizeof(int32_t), cudaMemcpyDeviceToHost, P->stream);
+    cudaMemcpyAsync(mail(P, kMailMaps), P->d_tmpi.p, K * sizeof(int32_t), cudaMemcpyDeviceToHost, P->stream);
     P->d2h += (long long)K * 4;
     cudaError_t s1;
     {
@@ -680,6 +784,8 @@ static int create_from_cols(int32_t n, int32_t m, int32_t K, const uint32_t* col
         delete P;
         return fail(WPM_EINTERNAL, std::string("kernel 1: ") + cudaGetErrorString(cudaGetLastError()));
     }
+    stage_reset(P);
+    std::memcpy(P->M.data(), mail(P, kMailMaps), K * sizeof(int32_t));
     for (int i = 0; i < K; ++i)
         if (P->M[i] < 0) {
             delete P;
@@ -714,10 +820,16 @@ extern "C" int wpm_plan_create_orbits(int32_t n, int32_t p, int64_t facet_cap, i
     *out = nullptr;
     Trace tr;
     const int m = n + p;
-    std::vector<uint32_t> rows((size_t)4096 * m);
-    const int32_t K = wpm_idcm_orbits(n, p, rows.data(), 4096);
+    // at most one orbit per n-subset of the 2^p - 1 - p non-unit rows
+    const int pool = p >= 1 && p <= 8 ? (1 << p) - 1 - p : 0;
+    uint64_t choose = n >= 0 && n <= pool ? 1 : 4096;  // C(pool, n), saturated: C(pool - n + i, i) grows with i
+    for (int i = 1; i <= n && n <= pool && choose <= 4096; ++i) choose = choose * (uint64_t)(pool - n + i) / (uint64_t)i;
+    const int32_t bound = (int32_t)std::min<uint64_t>(4096, std::max<uint64_t>(choose, 1));
+    std::vector<uint32_t> rows((size_t)std::max(bound, 1) * std::max(m, 1));
+    const int32_t K = wpm_idcm_orbits(n, p, rows.data(), bound);
     if (K < 0) return -K;
-    if (K > 4096) return fail(WPM_EINVAL, "too many orbits");
+    tr.mark("orbits (host)");
+    if (K > bound) return fail(WPM_EINVAL, "too many orbits");
     std::vector<uint32_t> cols((size_t)K * m);
     for (int i = 0; i < K; ++i)
         if (wpm_charmap_of_dcm(m, p, rows.data() + (size_t)i * m, cols.data() + (size_t)i * m) < 0)
@@ -779,7 +891,7 @@ extern "C" int wpm_plan_create_universes(int32_t m, int32_t n, int32_t K, const 
     P->cap.resize(K);
     for (int i = 0; i < K; ++i) P->cap[i] = resolve_cap(facet_cap, n, P->M[i]);
     if (P->d_facets.ensure(h.size())) { delete P; return fail(WPM_EINTERNAL, "device allocation failed"); }
-    cudaMemcpyAsync(P->d_facets.p, h.data(), h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, P->stream);
+    h2d_async(P, P->d_facets.p, h.data(), h.size() * sizeof(uint32_t));
     P->h2d += (long long)h.size() * 4;
     rc = plan_build_tables(P, foff);
     if (rc) { delete P; return rc; }
@@ -938,7 +1050,7 @@ static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
     {
         unsigned long long ctl[3] = {(unsigned long long)nseed << 32, 0, (unsigned long long)nseed};
         if (sp.map_queues) ctl[0] = ctl[2] = 0;  // plan-wide words only
-        CU(cudaMemcpyAsync(P->d_qctl.p, ctl, sizeof(ctl), cudaMemcpyHostToDevice, P->stream));  // [3], [4] add up
+        CU(h2d_async(P, P->d_qctl.p, ctl, sizeof(ctl)));  // [3], [4] add up
         P->h2d += (long long)sizeof(ctl);
         if (sp.map_queues) {
             const std::vector<int32_t>& first = P->h_map_first;
@@ -948,7 +1060,7 @@ static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
                 qc[8 * q] = c << 32;
                 qc[8 * q + 2] = c;
             }
-            CU(cudaMemcpyAsync(P->d_qctl.p + 8, qc.data(), qc.size() * 8, cudaMemcpyHostToDevice, P->stream));
+            CU(h2d_async(P, P->d_qctl.p + 8, qc.data(), qc.size() * 8));
             P->h2d += (long long)qc.size() * 8;
         }
         CU(cudaMemsetAsync(P->d_qready.p, 0, (size_t)nq * qcap * 8, P->stream));
@@ -1059,8 +1171,8 @@ static int search_prepare(wpm_plan* P, int shard_index, int shard_count) {
     if (P->has_pins) {
         if (P->d_pin_in.ensure(P->mw) || P->d_pin_out.ensure(P->mw))
             return fail(WPM_EINTERNAL, "device allocation failed (pins)");
-        CU(cudaMemcpyAsync(P->d_pin_in.p, P->pin_in.data(), P->mw * 4, cudaMemcpyHostToDevice, P->stream));
-        CU(cudaMemcpyAsync(P->d_pin_out.p, P->pin_out.data(), P->mw * 4, cudaMemcpyHostToDevice, P->stream));
+        CU(h2d_async(P, P->d_pin_in.p, P->pin_in.data(), P->mw * 4));
+        CU(h2d_async(P, P->d_pin_out.p, P->pin_out.data(), P->mw * 4));
     }
     tr.mark("    prepare: small buffers");
     {  // root tasks are map-major: map q's are [first[q], first[q + 1])
@@ -1069,13 +1181,13 @@ static int search_prepare(wpm_plan* P, int shard_index, int shard_count) {
         for (int q = 0; q < K; ++q) first[q + 1] += first[q];
         if (P->d_map_first.ensure(K + 1)) return fail(WPM_EINTERNAL, "device allocation failed (queue)");
         P->h_map_first = first;
-        CU(cudaMemcpyAsync(P->d_map_first.p, P->h_map_first.data(), (K + 1) * 4, cudaMemcpyHostToDevice, P->stream));
+        CU(h2d_async(P, P->d_map_first.p, P->h_map_first.data(), (K + 1) * 4));
         P->h2d += 4LL * (K + 1);
     }
     if (ntasks) {
-        CU(cudaMemcpyAsync(P->d_task_map.p, tm.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
-        CU(cudaMemcpyAsync(P->d_task_f.p, tf.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
-        CU(cudaMemcpyAsync(P->d_task_kind.p, tk.data(), ntasks * 4, cudaMemcpyHostToDevice, P->stream));
+        CU(h2d_async(P, P->d_task_map.p, tm.data(), ntasks * 4));
+        CU(h2d_async(P, P->d_task_f.p, tf.data(), ntasks * 4));
+        CU(h2d_async(P, P->d_task_kind.p, tk.data(), ntasks * 4));
         P->h2d += 12LL * ntasks;
     }
     if (P->out_cap == 0) {
@@ -1167,8 +1279,8 @@ static int search_main(wpm_plan* P, MainSrc src) {
 static int search_finish(wpm_plan* P, long long progress_total, int* again) {
     *again = 0;
     unsigned long long octl[4], qc[8];
-    CU(cudaMemcpyAsync(octl, P->d_out_ctl.p, 32, cudaMemcpyDeviceToHost, P->stream));
-    CU(cudaMemcpyAsync(qc, P->d_qctl.p, 64, cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaMemcpyAsync(mail(P, kMailOctl), P->d_out_ctl.p, 32, cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaMemcpyAsync(mail(P, kMailQc), P->d_qctl.p, 64, cudaMemcpyDeviceToHost, P->stream));
     if (P->progress_fn) {
         // the reference's progress(done, total) (search.hpp:54, :244): root
         // tasks finished, published by the kernel to host-mapped memory
@@ -1183,6 +1295,9 @@ static int search_finish(wpm_plan* P, long long progress_total, int* again) {
         }
     }
     CU(cudaStreamSynchronize(P->stream));
+    stage_reset(P);
+    std::memcpy(octl, mail(P, kMailOctl), sizeof(octl));
+    std::memcpy(qc, mail(P, kMailQc), sizeof(qc));
     if (P->progress_fn) P->progress_fn((int64_t)progress_total, (int64_t)progress_total, P->progress_user);
     P->d2h += 96;
     P->total = (long long)octl[0];
@@ -1306,9 +1421,8 @@ static int plan_sort_launch(wpm_plan* P, bool device_count) {
     CU(cudaEventRecord(P->ev[3], P->stream));
     tr.mark("    sort: launch");
     // results of the sort, read back with the next synchronisation
-    CU(cudaMemcpyAsync(&P->h_dups, P->d_out_ctl.p + 1, 8, cudaMemcpyDeviceToHost, P->stream));
-    P->h_first.resize(K);
-    CU(cudaMemcpyAsync(P->h_first.data(), P->d_per_map.p, K * 8, cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaMemcpyAsync(mail(P, kMailDups), P->d_out_ctl.p + 1, 8, cudaMemcpyDeviceToHost, P->stream));
+    CU(cudaMemcpyAsync(mail(P, kMailMaps), P->d_per_map.p, K * 8, cudaMemcpyDeviceToHost, P->stream));
     P->d2h += 8 + 8LL * K;
     return WPM_OK;
 }
@@ -1320,6 +1434,9 @@ static int plan_sort_collect(wpm_plan* P) {
         std::lock_guard<std::mutex> lk(g_rows_mu);
         g_rows_seen[P->signature] = P->total;
     }
+    std::memcpy(&P->h_dups, mail(P, kMailDups), 8);
+    P->h_first.resize(K);
+    std::memcpy(P->h_first.data(), mail(P, kMailMaps), K * 8);
     P->dups = (long long)P->h_dups;
     // per-map counts from the group boundaries of the sorted map ids
     P->per_map.assign(K, 0);
@@ -1973,7 +2090,11 @@ extern "C" void wpm_plan_destroy(wpm_plan_t* P) {
     b.s = P->stream;
     for (int i = 0; i < 5; ++i) b.ev[i] = P->ev[i];
     const int dev = P->device;
-    delete P;  // buffers go back to the pool, ordered on the stream
+    // every buffer's last use is complete once the stream is idle: they go to
+    // the block cache for the next plan on this device (the pool otherwise)
+    g_recycle = b.s && cudaStreamSynchronize(b.s) == cudaSuccess;
+    delete P;
+    g_recycle = false;
     trace_pending("destroy (buffers)");
     if (b.s) {
         std::lock_guard<std::mutex> lk(g_dev[dev].mu);

@@ -130,7 +130,13 @@ using CG = LC<4096, 2048, FRAME_CAP>;     // any universe within the device limi
 using C5T = LC<128, 128, FRAME_CAP, true, 20, 2>;    // n <= 5: all 35 maps' tables ~70 KB per CTA
 using C6T = LC<232, 136, FRAME_CAP, true, 32, 1>;    // n = 6: ~137 KB
 using C10T = LC<1792, 616, FRAME_CAP, true, 24, 1>;  // n = 10: ~90 KB
-using C11T = LC<2688, 840, FRAME_CAP, true, 24, 1>;  // n = 11: ~48 KB
+#ifndef K3_C11_WARPS
+#define K3_C11_WARPS 24
+#endif
+#ifndef K3_C11_DEPTH
+#define K3_C11_DEPTH FRAME_CAP
+#endif
+using C11T = LC<2688, 840, K3_C11_DEPTH, true, K3_C11_WARPS, 1>;  // n = 11: ~48 KB
 // any (m, n) = (15, 11) universe (the synthetic band, up to all 1365 11-subsets)
 using C15 = LC<3008, 1368, FRAME_CAP>;
 using C15T = LC<3008, 1368, FRAME_CAP, true, 18, 1>;
@@ -1238,15 +1244,11 @@ int launch_class(const SearchParams& p, int num_sms, cudaStream_t st, int* warps
     // fr and rp each padded to 16 bytes (the kernel's layout)
     const size_t tab = !C::TS ? 0 : C::MA ? (size_t)p.ma_tab_bytes : (size_t)16 * (((p.fr_words + 7) >> 3) + ((p.rp_words + 7) >> 3));
     const size_t smem = tab + (size_t)C::BYTES * wpb;
-    if (cudaFuncSetAttribute(k3_search<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return 0;
     // experiment knob: the L1 / shared split (percent of the max shared carveout)
     if (const char* e = std::getenv("WPM_CARVEOUT"))
         cudaFuncSetAttribute(k3_search<C>, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(e));
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_search<C>, 32 * wpb, smem) != cudaSuccess ||
-        per_sm < 1)
-        return 0;
+    int per_sm = occupancy_cached(reinterpret_cast<const void*>(k3_search<C>), 32 * wpb, smem);
+    if (per_sm < 1) return 0;
     if (const char* e = std::getenv("WPM_BLOCKS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
     const int grid = per_sm * num_sms;
     k3_search<C><<<grid, 32 * wpb, smem, st>>>(p);

@@ -638,10 +638,8 @@ int canon_sort_records(uint32_t* d_keys, long long count, int w32, int rw, int t
     int Cc = T;
     if (const char* e = std::getenv("WPM_SORT_CHUNK")) Cc = std::max(32, std::min(T, std::atoi(e)));
     const size_t smem = (size_t)T * rw * 4 + (size_t)T * 2 + 16;
-    if (cudaFuncSetAttribute(k4_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 1;
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_sort, SORT_THREADS, smem) != cudaSuccess || per_sm < 1)
-        return 1;
+    const int per_sm = occupancy_cached(reinterpret_cast<const void*>(k4_sort), SORT_THREADS, smem);
+    if (per_sm < 1) return 1;
     // the kernel strides over its tiles / chunks, so any grid is correct; size
     // it for the expected rows (fewer idle CTAs in every grid barrier)
     const long long rows_for_grid = grid_rows > 0 ? std::min(grid_rows, count) : count;

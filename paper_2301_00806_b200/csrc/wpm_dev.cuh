@@ -47,11 +47,15 @@ __host__ __device__ inline uint32_t binom_small(int a, int b) {
     return r;
 }
 
-inline Binom make_binom() {
-    Binom b;
-    for (int a = 0; a <= 16; ++a)
-        for (int k = 0; k <= 16; ++k) b.c[a][k] = binom_small(a, k);
-    return b;
+// built once per process (a kernel argument of every launch that ranks subsets)
+inline const Binom& make_binom() {
+    static const Binom tab = [] {
+        Binom b;
+        for (int a = 0; a <= 16; ++a)
+            for (int k = 0; k <= 16; ++k) b.c[a][k] = binom_small(a, k);
+        return b;
+    }();
+    return tab;
 }
 
 }  // namespace wpm

@@ -3,10 +3,40 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "wpm_dev.cuh"
 
 namespace wpm {
+
+// Resident CTAs per SM of kernel `fn` at (threads, dynamic smem) on the
+// current device, with its dynamic-smem limit raised to at least `smem`: the
+// per-launch cudaFuncSetAttribute + occupancy query pair cost ~3-5 us of host
+// time per launch (WPM_TRACE=2), paid by every one-shot call.  The limit only
+// ever grows (a later launch with less smem must not lower it under an
+// earlier, larger one).  0 on error.
+inline int occupancy_cached(const void* fn, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, size_t, int>, int> memo;
+    static std::map<std::pair<const void*, int>, size_t> limit;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& lim = limit[std::make_pair(fn, dev)];
+    if (lim < smem) {
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+        lim = smem;
+    }
+    const auto key = std::make_tuple(fn, threads, smem, dev);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) return 0;
+    memo[key] = per_sm;
+    return per_sm;
+}
 
 // kernel 1: universes of num_maps characteristic maps (m columns each)
 int launch_k1_universe(int n, int m, int num_maps, const uint32_t* d_cols, uint32_t* d_facets,
