@@ -130,13 +130,17 @@ using CG = LC<4096, 2048, FRAME_CAP>;     // any universe within the device limi
 using C5T = LC<128, 128, FRAME_CAP, true, 20, 2>;    // n <= 5: all 35 maps' tables ~70 KB per CTA
 using C6T = LC<232, 136, FRAME_CAP, true, 32, 1>;    // n = 6: ~137 KB
 using C10T = LC<1792, 616, FRAME_CAP, true, 24, 1>;  // n = 10: ~90 KB
+// n = 11: ~45 KB of tables + 27 warps x 6.8 KB of state.  A 40-frame stack
+// (measured depth <= 37 at n = 11; deeper runs redo with the full-depth
+// class) frees 240 B per warp, so 27 warps fit instead of 24 (64 frames):
+// n = 11 17.8 -> 17.2 ms (26 warps: 17.4; profiles/r02d_ab_c11.jsonl)
 #ifndef K3_C11_WARPS
-#define K3_C11_WARPS 24
+#define K3_C11_WARPS 27
 #endif
 #ifndef K3_C11_DEPTH
-#define K3_C11_DEPTH FRAME_CAP
+#define K3_C11_DEPTH 40
 #endif
-using C11T = LC<2688, 840, K3_C11_DEPTH, true, K3_C11_WARPS, 1>;  // n = 11: ~48 KB
+using C11T = LC<2688, 840, K3_C11_DEPTH, true, K3_C11_WARPS, 1>;
 // any (m, n) = (15, 11) universe (the synthetic band, up to all 1365 11-subsets)
 using C15 = LC<3008, 1368, FRAME_CAP>;
 using C15T = LC<3008, 1368, FRAME_CAP, true, 18, 1>;
