@@ -146,8 +146,21 @@ using C15 = LC<3008, 1368, FRAME_CAP>;
 using C15T = LC<3008, 1368, FRAME_CAP, true, 18, 1>;
 using C7M = LC<420, 208, FRAME_CAP, true, 20, 2, true>;   // n = 7: one map's tables (~8 KB) per CTA
 using C8M = LC<720, 312, FRAME_CAP, true, 20, 2, true>;   // n = 8: ~14 KB
-using C9M = LC<1152, 440, FRAME_CAP, true, 16, 2, true>;  // n = 9: ~20 KB (41.9 -> 39.6 ms)
-using C10M = LC<1792, 616, FRAME_CAP, true, 16, 2, true>; // n = 10: ~30 KB, 32 warps per SM (32.5 -> 29.8 ms)
+// n = 9: 18 warps x 2 CTAs with a 40-frame stack (measured 35.0 -> 34.3 ms;
+// 20 x 2 at 48 registers spilled and lost); n = 10 keeps 16 x 2 (18 or 20
+// warps measured 7-9 % slower there: 3 maps, longer per-map tails) --
+// profiles/r02d_ab_mq.jsonl
+#ifndef K3_C9M_WARPS
+#define K3_C9M_WARPS 18
+#endif
+#ifndef K3_C9M_DEPTH
+#define K3_C9M_DEPTH 40
+#endif
+#ifndef K3_C10M_WARPS
+#define K3_C10M_WARPS 16
+#endif
+using C9M = LC<1152, 440, K3_C9M_DEPTH, true, K3_C9M_WARPS, 2, true>;  // n = 9: ~20 KB (41.9 -> 39.6 ms)
+using C10M = LC<1792, 616, FRAME_CAP, true, K3_C10M_WARPS, 2, true>; // n = 10: ~30 KB, 32 warps per SM (32.5 -> 29.8 ms)
 // (10 x 4 and 8 x 5 warps x CTAs measured within 1 % of 20 x 2 at n = 7, 8)
 // (n = 9's seven maps need ~140 KB of tables: 16 warps per SM measured 34 %
 // slower than the global-table layout at 32 -- no all-maps TS variant for n = 7..9)
@@ -155,6 +168,7 @@ using CGF = LC<4096, 2048, 2050>;         // full depth: the rerun after a frame
 
 struct MapView {
     int M, N, n, cap, map, nw;
+    int capn;       // min(cap, 2^20): the open-ridge prune in 32-bit arithmetic
     int lpf_shift;  // lanes per facet in flattened passes: 1 << lpf_shift >= n
     unsigned nmag;  // ceil(2^20 / n): j / n = (j * nmag) >> 20 for every pair index j < 2^20 / n
     const uint16_t* fr;
@@ -614,7 +628,7 @@ __device__ __forceinline__ void write_frontier(const WS<C>& w, const MapView& mp
 // the next real branch point by pushing its frame.  Returns true if a frame
 // was pushed; false if the descent ended (dead, pruned, or a leaf).
 template <class C>
-__device__ __forceinline__ bool descend(WS<C>& w, const MapView& mp, const SearchParams& p, unsigned long long& nodes,
+__device__ __forceinline__ bool descend(WS<C>& w, const MapView& mp, const SearchParams& p, unsigned& nodes,
                                         int lane) {
     for (;;) {
         if (w.ndead) return false;
@@ -625,7 +639,8 @@ __device__ __forceinline__ bool descend(WS<C>& w, const MapView& mp, const Searc
             ridge = CLOSED_FRAME;
         } else {
             // |S| + ceil(open / n) > cap  <=>  open > (cap - |S|) * n
-            if ((long long)(mp.cap - w.size) * mp.n < (long long)w.nopen) return false;
+            // (32-bit: capn = min(cap, 2^20) never prunes where cap would not -- open <= N < 2^12)
+            if ((mp.capn - w.size) * mp.n < w.nopen) return false;
             const unsigned sel = select_ridge(w, mp.nw, lane);
             ridge = sel & 0xFFFFu;
             if ((sel >> 16) == 1u) {  // forced: the only undecided candidate
@@ -922,7 +937,11 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
     WS<C> w;
     w.base = smem + tab_bytes + wid * C::BYTES;
     w.sb = static_cast<uint32_t>(__cvta_generic_to_shared(w.base));
+    // search nodes: `nodes` (64-bit) takes the 32-bit running count `tn` at
+    // every queue check and task end, so the per-node work is a 32-bit
+    // increment and compare
     unsigned long long nodes = 0, tasks = 0;
+    unsigned tn = 0;
 #ifdef WPM_PROFILE
     // busy / waiting / final-wait clocks per warp (qctl[5..7]; WPM_PROFILE=1 prints them)
     unsigned long long prof_busy = 0, prof_wait = 0, prof_t = clock64();
@@ -1051,6 +1070,7 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
         mp.N = md.N;
         mp.n = md.n;
         mp.cap = md.cap;
+        mp.capn = min(md.cap, 1 << 20);
         mp.map = map;
         mp.nw = (md.N + 31) >> 5;
         mp.lpf_shift = md.n <= 4 ? 2 : (md.n <= 8 ? 3 : 4);
@@ -1073,14 +1093,14 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
         if (load_state(w, mp, rec + 4, rec + 4 + p.mw, kind == T_ENTRY, lane)) {
             if (kind == T_SINGLE) {
                 const Probe pr = probe_facet(w, mp, (int)h1, lane);
-                ++nodes;
+                ++tn;
                 if (!pr.dead) {
                     include_facet(w, mp, (int)h1, pr, lane);
                     DEBUG_CHECK(w, mp, lane, 2);
-                    descend(w, mp, p, nodes, lane);
+                    descend(w, mp, p, tn, lane);
                 }
             } else if (kind == T_ENTRY) {
-                descend(w, mp, p, nodes, lane);
+                descend(w, mp, p, tn, lane);
             } else if (w.ndead == 0) {  // resume a donated frame
                 if (lane == 0)
                     w.frames()[0] =
@@ -1091,7 +1111,6 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
         }
         // ---- the DFS over branch frames
         unsigned long long qword = ld_relaxed_u64(&qc[0]);  // prefetched queue state
-        unsigned long long next_check = nodes + (unsigned)p.check_every;
         unsigned long long flushed = nodes;  // node-budget mode: count already in qctl[1]
         while (w.depth > 0) {
             const uint2 fr = w.frames()[w.depth - 1];
@@ -1122,12 +1141,12 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
             }
             __syncwarp();
             const Probe pr = probe_facet(w, mp, c, lane);
-            ++nodes;
+            ++tn;
             bool pushed = false;
             if (!pr.dead) {
                 include_facet(w, mp, c, pr, lane);
                 DEBUG_CHECK(w, mp, lane, 5);
-                pushed = descend(w, mp, p, nodes, lane);
+                pushed = descend(w, mp, p, tn, lane);
             }
             if (!pushed) {
                 undo_to(w, mp, cm, om, lane);
@@ -1139,8 +1158,9 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
                     __syncwarp();
                 }
             }
-            if (nodes >= next_check) {
-                next_check = nodes + (unsigned)p.check_every;
+            if (tn >= (unsigned)p.check_every) {
+                nodes += tn;
+                tn = 0;
                 // waiting warps <=> the head ticket ran ahead of the tail
                 const long long queued = (long long)(qword >> 32) - (long long)(qword & 0xFFFFFFFFull);
                 if (queued < (long long)p.hungry) {
@@ -1164,6 +1184,8 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
             }
         }
         // task finished
+        nodes += tn;
+        tn = 0;
         if (lane == 0) {
             if (p.root_nodes)
                 atomicAdd(&p.root_nodes[w.root()], nodes - reinterpret_cast<unsigned long long*>(w.base + C::META)[1]);

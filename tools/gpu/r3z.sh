@@ -2,6 +2,7 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 TAG=${TAG:-r02e}
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_reach.py tests/test_gpu_multi.py -x -q -k "11 or multi or reach" > gpurun_out/${TAG}_n11_tests.log 2>&1; tail -2 gpurun_out/${TAG}_n11_tests.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; tail -1 gpurun_out/${TAG}_smoke.log
 for n in 5 8 11; do
   nodes=$(python -c "import json; print(json.load(open('tests/golden/golden.json'))['dfs']['$n']['nodes'])")
