@@ -1083,7 +1083,10 @@ static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
     const int est_warps = P->num_sms * 16;
     sp.hungry = std::max(64, est_warps / 2);
     if (sp.map_queues) sp.hungry = 128;  // per map queue (measured 8..128: within 1 %, 128 best at n = 7, 8)
-    sp.backoff_min = 32;
+    // first poll sleep of a waiting warp: 1 us (32 ns before this round) --
+    // idle warps' polls took issue slots from the busy ones: n = 4 -5 %,
+    // n = 5 -2..-4 %, n >= 6 within noise (profiles/r02d_ab_backoff*.jsonl)
+    sp.backoff_min = 1024;
     sp.backoff_max = 8192;
     if (const char* e = std::getenv("WPM_BACKOFF_MIN")) sp.backoff_min = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("WPM_HUNGRY")) sp.hungry = std::atoi(e);
