@@ -1096,6 +1096,8 @@ static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
     // O(N) per donated task) -- measured sweep in DESIGN.md
     sp.check_every = P->maxN <= 256 ? 16 : 32;
     if (const char* e = std::getenv("WPM_CHECK_EVERY")) sp.check_every = std::max(1, std::atoi(e));
+    sp.first_check = sp.check_every;
+    if (const char* e = std::getenv("WPM_FIRST_CHECK")) sp.first_check = std::max(1, std::min(sp.check_every, std::atoi(e)));
     sp.donate_max = 1;
     if (const char* e = std::getenv("WPM_DONATE_MAX")) sp.donate_max = std::max(1, std::atoi(e));
     // claims: while fewer tasks than warps are pending on this GPU, waiting

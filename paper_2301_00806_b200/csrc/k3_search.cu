@@ -1112,6 +1112,7 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
         // ---- the DFS over branch frames
         unsigned long long qword = ld_relaxed_u64(&qc[0]);  // prefetched queue state
         unsigned long long flushed = nodes;  // node-budget mode: count already in qctl[1]
+        unsigned chk = (unsigned)p.first_check;  // nodes before the next look at the queue
         while (w.depth > 0) {
             const uint2 fr = w.frames()[w.depth - 1];
             int npos = 0;
@@ -1158,9 +1159,10 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
                     __syncwarp();
                 }
             }
-            if (tn >= (unsigned)p.check_every) {
+            if (tn >= chk) {
                 nodes += tn;
                 tn = 0;
+                chk = (unsigned)p.check_every;
                 // waiting warps <=> the head ticket ran ahead of the tail
                 const long long queued = (long long)(qword >> 32) - (long long)(qword & 0xFFFFFFFFull);
                 if (queued < (long long)p.hungry) {
