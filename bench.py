@@ -595,18 +595,19 @@ def e2e_dropin(n, dev):
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
-def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)), max_w=8):
+def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)), max_w=8, per_gpu=None):
     """1-GPU PROJECTION of the multi-GPU job (labelled as such; the driver's
     SCALE run measures the real thing).  The job as max_w GPUs would run it:
-    every GPU splits its share of the root tasks below the root until >= 640
-    records (each shard timed here one after another; T_W takes the slowest
+    every GPU splits its share of the root tasks below the root until >= per_gpu
+    records (the library's frontier_target; each shard timed here one after another; T_W takes the slowest
     shard of W), then the claim phase over the concatenated frontier with
     per-record node accounting.  From the measured
     per-record nodes, for W = 1, 2, 4, 8: the static strided split's max/mean
     and a list schedule of the records in claim order over W GPUs (the
     shared counter hands each record to the first free GPU) at the measured
     single-GPU rate; projected T_W = t_split + makespan_W / rate (and, as a
-    conservative bound, with the static strided split's largest share)."""
+    conservative bound, with the static strided split's largest share).
+    Speed-ups are against the measured direct 1-GPU run (one_gpu_run_ms)."""
     import heapq
     import sys as _sys
 
@@ -618,6 +619,8 @@ def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)
 
     from paper_2301_00806_b200 import dist as wpm_dist
 
+    if per_gpu is None:
+        per_gpu = int(os.environ.get("WPM_SPLIT_PER_GPU", "640"))
     out = []
     for n, d in cases:
         if d is None:
@@ -643,13 +646,13 @@ def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)
                     for rep in range(2):  # the first pass sizes the frontier / queue buffers
                         torch.cuda.synchronize(dev)
                         t0 = time.perf_counter()
-                        p.split(0, 640, sidx, W)
+                        p.split(0, per_gpu, sidx, W)
                         dt = (time.perf_counter() - t0) * 1e3
                     times.append(dt)
                 t_shard[W] = max(times)
             parts = []
             for sidx in range(max_w):
-                p.split(0, 640, sidx, max_w)
+                p.split(0, per_gpu, sidx, max_w)
                 ptr, cnt, recw = p.frontier()
                 parts.append(torch.as_tensor(wpm_dist._wrap_device(ptr, cnt * recw, torch.int32, dev)).clone())
             recs = torch.cat(parts)
@@ -684,9 +687,9 @@ def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)
             t_s = t_shard[W] + loads.max() / rate
             rows.append({"W": W, "static_max_over_mean": float(loads.max() / loads.mean()),
                          "dynamic_makespan_over_mean": float(mk_nodes / (tot / W)),
-                         "projected_ms": round(t_w, 3), "projected_speedup": round((t_split + t_main) / t_w, 3),
-                         "projected_speedup_static_split": round((t_split + t_main) / t_s, 3)})
-        out.append({"case": name, "frontier_records": int(F), "split_ms_host": round(t_split, 3),
+                         "projected_ms": round(t_w, 3), "projected_speedup": round(t_one / t_w, 3),
+                         "projected_speedup_static_split": round(t_one / t_s, 3)})
+        out.append({"case": name, "per_gpu_target": per_gpu, "frontier_records": int(F), "split_ms_host": round(t_split, 3),
                     "split_ms_by_W": {str(k): round(v, 3) for k, v in t_shard.items()},
                     "claim_ms": round(t_main, 3), "one_gpu_run_ms": round(t_one, 3),
                     "split_nodes": int(split_nodes), "claim_nodes": int(tot),

@@ -330,6 +330,7 @@ struct wpm_plan {
     int split_depth = 0;          // > 0: split at this branch depth, then search the frontier
     long long claim_count = 0;
     unsigned long long* claim_ctr = nullptr;
+    int claim_devices = 1;        // GPUs claiming from the shared frontier (fair-share claim cap)
     // progress callback (search.hpp:54): root tasks finished / root tasks
     void (*progress_fn)(int64_t, int64_t, void*) = nullptr;
     void* progress_user = nullptr;
@@ -1104,6 +1105,15 @@ static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
     // warps pull records (measured at 1 GPU: a quarter of the warps starved
     // the claim phase 2-5x; >= the warp count matches the seeded run)
     sp.claim_low = P->num_sms * 40;
+    // Several GPUs: at most a fair share (frontier / GPUs) pending per GPU
+    // while it claims.  With ~5 k records and ~4 k warps per GPU every
+    // waiting warp would otherwise pull a record at launch, and the GPU
+    // launched first would take up to its warp count of them -- a
+    // first-come partition instead of a balanced one.  A GPU past its share
+    // claims again once its pending tasks drop under the share.
+    if (L.claim_recs && P->claim_devices > 1)
+        sp.claim_low = (int)std::max<long long>(
+            2LL * P->num_sms, std::min<long long>(sp.claim_low, (L.claim_count + P->claim_devices - 1) / P->claim_devices));
     if (const char* e = std::getenv("WPM_CLAIM_LOW")) sp.claim_low = std::max(1, std::atoi(e));
     if (L.progress && P->root_stats) {  // nodes per root task / frontier record (the scaling projection)
         if (P->d_root_nodes.ensure((size_t)std::max<long long>(nroots, 1)))
@@ -1562,14 +1572,21 @@ int enable_peer(int dev, int leader) {
 // per-record cost stays invisible (1 GPU, n = 11: the claim phase over 5 k
 // records = the direct run, over 12.7 k +28 %, tools/gpu/split_probe.py).
 // The first split is at depth 5, then one jump to the target depth.
-long long frontier_target(int ndev) { return std::max<long long>(2048, 640LL * ndev); }
+long long frontier_target(int ndev) {
+    long long per = 640;
+    if (const char* e = std::getenv("WPM_SPLIT_PER_GPU")) per = std::max(1, std::atoi(e));
+    return std::max<long long>(std::min<long long>(2048, 4 * per), per * ndev);
+}
 
 // first split depth for a 1/W share of the root tasks: the whole tree needs
 // ~640 W records, i.e. log_1.7(W) levels more than one GPU's 640 -- so every
 // shard reaches its target in one round (a round costs ~0.5-1 ms of launch,
 // table copy and ramp-up whatever its size)
-int first_split_depth(int ndev) {
-    return 5 + (ndev > 1 ? (int)std::ceil(std::log((double)ndev) / std::log(1.7)) : 0);
+// (a shard's target of `per` records: depth 5 gave ~640 records for a whole
+// workload, and every 1.7x more records per shard is one level deeper)
+int first_split_depth(int ndev, long long per) {
+    const double levels = std::log((double)std::max(1, ndev) * (double)std::max<long long>(per, 1) / 640.0) / std::log(1.7);
+    return std::max(1, 5 + (int)std::ceil(levels - 1e-9));
 }
 
 }  // namespace
@@ -1614,7 +1631,8 @@ static int plan_run_multi(wpm_plan* P) {
                     int r = d ? search_prepare(q, d, W) : WPM_OK;
                     if (!r) r = search_reset(q);
                     if (!r)
-                        r = split_rounds(q, P->split_depth > 0 ? P->split_depth : first_split_depth(W),
+                        r = split_rounds(q, P->split_depth > 0 ? P->split_depth
+                                                               : first_split_depth(W, (frontier_target(W) + W - 1) / W),
                                          (frontier_target(W) + W - 1) / W, W, P->split_depth <= 0);
                     src[d] = r;
                 });
@@ -1666,6 +1684,7 @@ static int plan_run_multi(wpm_plan* P) {
                                           P->stream));
             q->frontier = F;
             q->claim_count = F;
+            q->claim_devices = W;
             q->claim_ctr = static_cast<unsigned long long*>(P->claim_raw);
         }
         CU(cudaSetDevice(P->device));
@@ -1817,12 +1836,14 @@ extern "C" int wpm_plan_split(wpm_plan_t* P, int32_t shard_index, int32_t shard_
     CU(cudaEventRecord(P->ev[4], P->stream));
     for (int attempt = 0; attempt < 3; ++attempt) {
         if ((rc = search_reset(P))) return rc;
-        if ((rc = split_rounds(P, depth > 0 ? depth : first_split_depth(shard_count),
-                               target > 0 ? target : frontier_target(1), shard_count, depth <= 0))) return rc;
+        const long long tgt = target > 0 ? target : frontier_target(1);
+        if ((rc = split_rounds(P, depth > 0 ? depth : first_split_depth(shard_count, tgt), tgt, shard_count,
+                               depth <= 0))) return rc;
         if ((unsigned long long)P->frontier <= P->front_cap) break;
         P->front_cap = (unsigned long long)P->frontier + (unsigned long long)P->frontier / 4 + 1024;
     }
     P->split_kept = true;  // the split's rows / nodes belong to this plan's claim run
+    P->claim_devices = shard_count;
     if (count) *count = P->frontier;
     return WPM_OK;
 }
