@@ -159,7 +159,7 @@ LAUNCHES_PER_STEP = 3
 def _profile_summary(n):
     """traffic / instructions-per-node of kernel 3 from the committed ncu capture."""
     out = {}
-    for tag in ("r02c", "r02", "r01"):  # the newest capture committed
+    for tag in ("r02g", "r02c", "r02", "r01"):  # the newest capture committed
         path = os.path.join(ROOT, "profiles", f"{tag}_k3_n{n}_ncu.txt")
         if os.path.exists(path):
             out["source"] = f"profiles/{tag}_k3_n{n}_ncu.txt"
@@ -597,17 +597,20 @@ def e2e_dropin(n, dev):
 
 def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)), max_w=8, per_gpu=None):
     """1-GPU PROJECTION of the multi-GPU job (labelled as such; the driver's
-    SCALE run measures the real thing).  The job as max_w GPUs would run it:
-    every GPU splits its share of the root tasks below the root until >= per_gpu
-    records (the library's frontier_target; each shard timed here one after another; T_W takes the slowest
-    shard of W), then the claim phase over the concatenated frontier with
-    per-record node accounting.  From the measured
-    per-record nodes, for W = 1, 2, 4, 8: the static strided split's max/mean
-    and a list schedule of the records in claim order over W GPUs (the
-    shared counter hands each record to the first free GPU) at the measured
-    single-GPU rate; projected T_W = t_split + makespan_W / rate (and, as a
-    conservative bound, with the static strided split's largest share).
-    Speed-ups are against the measured direct 1-GPU run (one_gpu_run_ms)."""
+    SCALE run measures the real thing), built from measured pieces:
+      * t_split(W): every GPU splits its share of the root tasks below the
+        root until >= per_gpu records (the library's frontier target); the
+        W shards are timed one after another here, the slowest counts;
+      * t_claim(W): with ~5 k records and ~4 k warps per GPU, every record is
+        claimed at launch, so each GPU works through about 1/W of the
+        frontier with only donation to spread it over its warps.  Each of the
+        W strided shards of the concatenated frontier is run as a claim phase
+        on its own (a fresh plan: one GPU, its shard only, kernel-3 device
+        time), and the slowest shard counts.
+    projected T_W = t_split(W) + max_s t_claim(W, s); speed-ups are against the
+    measured direct 1-GPU run.  Also reported: the per-record node counts'
+    static max/mean and a list schedule in claim order (the bound if GPUs
+    could keep claiming single records), both at the 1-GPU claim rate."""
     import heapq
     import sys as _sys
 
@@ -630,14 +633,13 @@ def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)
             u = C.synthetic_universe(1, d)
             mk = lambda: wpm.Plan.universes(15, 11, [u], facet_cap=252, device=dev)  # noqa: E731
             name = f"synthetic (15, 11) d={d} seed 1"
-        with mk() as p:
+        with mk() as p, mk() as q:
             p.run()
             flush.zero_()
             torch.cuda.synchronize(dev)
             p.run()
             t_one = p.timing()["ms_total"]
-            p.set_root_stats(True)
-            # the split as max_w GPUs run it: every GPU splits its share of the
+            # the split as W GPUs run it: every GPU splits its share of the
             # root tasks; the shards run one after another here, timed apiece
             t_shard = {}
             for W in (1, 2, 4, 8):
@@ -657,22 +659,33 @@ def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)
                 parts.append(torch.as_tensor(wpm_dist._wrap_device(ptr, cnt * recw, torch.int32, dev)).clone())
             recs = torch.cat(parts)
             F = recs.numel() // recw
+            rv = recs.view(F, recw)
             ctr, _ = wpm.claim_counter_create(dev)
             try:
-                p.load_frontier(recs.data_ptr(), F)
-                torch.cuda.synchronize(dev)
-                t0 = time.perf_counter()
-                p.run_claim(ctr)
-                t_claim = (time.perf_counter() - t0) * 1e3 - p.stats()["ms_sort"]
+                # per-record nodes: the whole frontier claimed by one GPU
+                q.set_root_stats(True)
+                q.load_frontier(recs.data_ptr(), F)
+                wpm.claim_counter_reset(dev, ctr)
+                q.run_claim(ctr)
+                t_main = q.stats()["ms_search"]
+                per, _ = q.root_nodes()
+                q.set_root_stats(False)
+                # the W-GPU claim phase: each GPU's 1/W of the records on its own
+                t_claim = {}
+                for W in (1, 2, 4, 8):
+                    ts = []
+                    for sidx in range(W):
+                        sub = rv[sidx::W].contiguous()
+                        q.load_frontier(sub.data_ptr(), sub.shape[0])
+                        wpm.claim_counter_reset(dev, ctr)
+                        q.run_claim(ctr)
+                        ts.append(q.stats()["ms_search"])
+                    t_claim[W] = (max(ts), float(np.mean(ts)))
             finally:
                 wpm.claim_counter_close(dev, ctr, False)
-            t_split = t_shard[max_w]
-            st = p.stats()
-            per, split_nodes = p.root_nodes()
         per = per.astype(np.float64)
         tot = per.sum()
-        t_main = max(t_claim, 1e-3)  # host-timed claim phase (the run blocks), sort excluded
-        rate = tot / t_main  # nodes per ms, claim phase
+        rate = tot / max(t_main, 1e-3)  # nodes per ms, one GPU claiming the whole frontier
         rows = []
         for W in (1, 2, 4, 8):
             loads = np.zeros(W)
@@ -683,19 +696,22 @@ def scaling_projection(wpm, dev, flush, cases=((8, None), (11, None), (11, 0.80)
                 t, i = heapq.heappop(h)
                 heapq.heappush(h, (t + x, i))
             mk_nodes = max(t for t, _ in h)
-            t_w = t_shard[W] + mk_nodes / rate
-            t_s = t_shard[W] + loads.max() / rate
-            rows.append({"W": W, "static_max_over_mean": float(loads.max() / loads.mean()),
+            t_w = t_shard[W] + t_claim[W][0]
+            rows.append({"W": W, "claim_ms_slowest_shard": round(t_claim[W][0], 3),
+                         "claim_ms_mean_shard": round(t_claim[W][1], 3),
+                         "static_max_over_mean": float(loads.max() / loads.mean()),
                          "dynamic_makespan_over_mean": float(mk_nodes / (tot / W)),
                          "projected_ms": round(t_w, 3), "projected_speedup": round(t_one / t_w, 3),
-                         "projected_speedup_static_split": round(t_one / t_s, 3)})
-        out.append({"case": name, "per_gpu_target": per_gpu, "frontier_records": int(F), "split_ms_host": round(t_split, 3),
+                         "list_schedule_bound_speedup": round(t_one / (t_shard[W] + mk_nodes / rate), 3)})
+        out.append({"case": name, "per_gpu_target": per_gpu, "frontier_records": int(F),
+                    "split_ms_host": round(t_shard[max_w], 3),
                     "split_ms_by_W": {str(k): round(v, 3) for k, v in t_shard.items()},
-                    "claim_ms": round(t_main, 3), "one_gpu_run_ms": round(t_one, 3),
-                    "split_nodes": int(split_nodes), "claim_nodes": int(tot),
+                    "claim_ms_one_gpu_all_records": round(t_main, 3), "one_gpu_run_ms": round(t_one, 3),
+                    "claim_nodes": int(tot),
                     "largest_record_frac": float(per.max() / tot) if tot else None, "by_W": rows})
-    return {"note": "PROJECTION from measured per-frontier-record node counts on 1 B200 (not a multi-GPU run); "
-                    "excludes the NCCL frontier broadcast and the rank-0 gather", "cases": out}
+    return {"note": "PROJECTION from 1-B200 runs (not a multi-GPU run): each W-GPU shard's split and claim "
+                    "phase timed on its own; excludes the NCCL frontier broadcast and the rank-0 gather",
+            "cases": out}
 
 
 if __name__ == "__main__":

@@ -1098,6 +1098,10 @@ static int k3_launch(wpm_plan* P, const K3Launch& L, int frame_cap) {
     sp.check_every = P->maxN <= 256 ? 16 : 32;
     if (const char* e = std::getenv("WPM_CHECK_EVERY")) sp.check_every = std::max(1, std::atoi(e));
     sp.first_check = sp.check_every;
+    sp.starve_at = 1 << 30;
+    sp.starve_check = sp.check_every;
+    if (const char* e = std::getenv("WPM_STARVE_AT")) sp.starve_at = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("WPM_STARVE_CHECK")) sp.starve_check = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("WPM_FIRST_CHECK")) sp.first_check = std::max(1, std::min(sp.check_every, std::atoi(e)));
     sp.donate_max = 1;
     if (const char* e = std::getenv("WPM_DONATE_MAX")) sp.donate_max = std::max(1, std::atoi(e));
@@ -1912,10 +1916,12 @@ extern "C" int wpm_plan_run_claim(wpm_plan_t* P, void* counter, int64_t* total_o
     g_alloc_stream = P->stream;
     P->ran = false;
     int rc;
-    if (!P->split_kept) {
+    if (!P->split_kept) {  // a plan that did not split: the loaded frontier is all it claims from
+        const long long loaded = P->frontier;
         if ((rc = search_prepare(P, 0, 1))) return rc;
         CU(cudaEventRecord(P->ev[4], P->stream));
         if ((rc = search_reset(P))) return rc;
+        P->frontier = loaded;  // (search_reset clears the split count)
     }
     P->claim_count = P->frontier;
     P->claim_ctr = static_cast<unsigned long long*>(counter);

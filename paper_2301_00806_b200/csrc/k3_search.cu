@@ -1162,9 +1162,11 @@ __global__ void __launch_bounds__(32 * C::WPB, C::MIN_BLOCKS) k3_search(const __
             if (tn >= chk) {
                 nodes += tn;
                 tn = 0;
-                chk = (unsigned)p.check_every;
                 // waiting warps <=> the head ticket ran ahead of the tail
                 const long long queued = (long long)(qword >> 32) - (long long)(qword & 0xFFFFFFFFull);
+                // many warps waiting (a ramp, a tail, a GPU holding few
+                // frontier records): look again sooner
+                chk = queued < -(long long)p.starve_at ? (unsigned)p.starve_check : (unsigned)p.check_every;
                 if (queued < (long long)p.hungry) {
                     // warps are waiting (head ran past tail): hand out up to
                     // donate_max frames at once, shallowest first

@@ -66,6 +66,7 @@ struct SearchParams {
     int backoff_max;            // ns, idle warps' polling backoff cap
     int check_every;            // search nodes between looks at the queue word (donation check)
     int first_check;            // ... and before the first look of a task (<= check_every)
+    int starve_at, starve_check;  // more than starve_at warps waiting: look every starve_check nodes
     int donate_max;             // frames donated per check while warps wait
     // output: one key row per WPM = kw bitset words (zero padded) + the map id
     uint32_t* out_keys;         // out_cap * rw

@@ -90,6 +90,34 @@ def test_claim_two_plans_sequential(wpm):
         _same(a.fetch(), want)
 
 
+def test_claim_loaded_plan_claims_first(wpm):
+    """A plan that did not split (wpm_plan_load_frontier + run_claim) claims
+    the shared frontier itself: run first it takes every record, the
+    splitting plan keeps only the rows found above the frontier; together
+    they are the full result."""
+    import numpy as np
+
+    n = 6
+    with wpm.Plan.orbits(n) as a, wpm.Plan.orbits(n) as b:
+        a.run()
+        want = a.fetch()
+        a.split(3, 1024)
+        ptr, cnt, recw = a.frontier()
+        b.load_frontier(ptr, cnt)
+        ctr, _ = wpm.claim_counter_create(0)
+        try:
+            tb = b.run_claim(ctr)
+            ta = a.run_claim(ctr)
+        finally:
+            wpm.claim_counter_close(0, ctr, False)
+        assert tb > 0 and ta + tb == want.total
+        ra, rb = a.fetch(), b.fetch()
+        for i in range(want.num_maps):
+            got = np.concatenate([ra.map_bits(i), rb.map_bits(i)])
+            rows = sorted(map(bytes, got))
+            assert rows == sorted(map(bytes, want.map_bits(i))), i
+
+
 @pytest.mark.parametrize("n", [5, 9])
 def test_progress_callback(wpm, golden, n):
     """SearchJob::progress (search.hpp:54, :244): called while the search
