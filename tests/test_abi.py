@@ -148,3 +148,39 @@ def test_idcm_orbits_host_matches_goldens(wpm, oracle, golden):
         assert got == golden["orbits"][str(n)], n
     for n, p in ((2, 3), (3, 3), (4, 3), (2, 5), (3, 5)):  # the oracle returns <= 64 orbits
         assert [d.rows for d in wpm.idcm_orbits(n, p)] == oracle.idcm_orbits(n, p), (n, p)
+
+
+@pytest.mark.skipif(shutil.which("g++") is None, reason="no g++")
+def test_cpp_host_pool_visits_every_item_once():
+    """detail::HostPool (the drop-in's PureComplex builder): every index of
+    every parallel region exactly once, regions back to back, small and empty
+    regions -- host C++ only, no device."""
+    src = r'''
+#include "plseeds_b200.hpp"
+#include <atomic>
+#include <cstdio>
+#include <vector>
+int main() {
+    auto& pool = plseeds_b200::detail::HostPool::get();
+    for (std::size_t items : {0, 1, 2, 7, 1000, 100000}) {
+        for (int rep = 0; rep < 3; ++rep) {
+            std::vector<std::atomic<int>> hit(items);
+            for (auto& h : hit) h.store(0);
+            pool.run(items, [&](std::size_t i) { hit[i].fetch_add(1); });
+            for (std::size_t i = 0; i < items; ++i)
+                if (hit[i].load() != 1) { std::printf("item %zu of %zu hit %d\n", i, items, hit[i].load()); return 1; }
+        }
+    }
+    std::printf("ok\n");
+    return 0;
+}
+'''
+    with tempfile.TemporaryDirectory() as td:
+        p = os.path.join(td, "t.cpp")
+        open(p, "w").write(src)
+        exe = os.path.join(td, "t")
+        r = subprocess.run(["g++", "-std=c++17", "-O1", "-pthread", "-Wall", "-I", os.path.join(ROOT, "include"), p,
+                            "-o", exe, LIB, f"-Wl,-rpath,{os.path.dirname(LIB)}"], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
