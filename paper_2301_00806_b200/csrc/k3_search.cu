@@ -300,7 +300,6 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 // ridge byte = c | a << 2: c = IN candidates (0..2), a = undecided candidates.
 // open: c == 1.  b1: c == 1 && a == 1.  dead: c == 1 && a == 0.
 
-// a -= 1 on every ridge of the facets trail[lo..hi) (already marked OUT)
 // Flattened (decision, ridge) pairs of trail[lo..hi): body(act, e, k) per
 // lane, k = the ridge slot of trail entry e.  Up to n = 8 a facet takes a
 // power-of-two lane group (n = 5: 4 facets x 8 lanes per pass); the n >= 9
